@@ -1,0 +1,295 @@
+"""CPU pins of the oracle's budget, RNG and routing against what the paper,
+the spec's worked examples, library vectors and the mathematics fix.
+
+Each test names the passage it follows.  None of the expected values comes
+from the oracle itself or from the CUDA path.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import brute
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+# ---------------------------------------------------------------- RNG ------
+def test_philox_known_answer_vectors():
+    """Random123 KAT (SC'11); reading R-11 selects Philox4x32-10."""
+    for vec in _gold("philox_kat.json")["vectors"]:
+        ctr = [int(x, 16) for x in vec["ctr"]]
+        key = [int(x, 16) for x in vec["key"]]
+        want = [int(x, 16) for x in vec["out"]]
+        assert list(oracle.philox(ctr, key)) == want
+        got_np = brute.philox4x32_10(np.array([ctr], dtype=np.uint32), key)[0]
+        assert list(got_np) == want
+
+
+def test_layer_seed_splitmix_vectors():
+    """SplitMix64 reference outputs; reading R-11 (PAPER.md:308 layer independence)."""
+    for vec in _gold("splitmix64.json")["vectors"]:
+        assert oracle.layer_seed(int(vec["seed"]), vec["layer"]) == int(vec["out"], 16)
+
+
+def test_gumbel_uniform_map_bounds():
+    """R-12: u = (x0+0.5)2^-32 lies strictly inside (0,1); g in [-3.13, 22.87]."""
+    lo = -math.log(-math.log(0.5 * 2.0 ** -32))
+    hi = -math.log(-math.log((2.0 ** 32 - 0.5) * 2.0 ** -32))
+    assert -3.14 < lo < -3.12 and 22.8 < hi < 22.9
+    g = [oracle.gumbel(123, 5, 3, i, j) for i in range(20) for j in range(20)]
+    assert all(lo <= x <= hi for x in g)
+    # oracle C and NumPy twin draw the same grid
+    grid = brute.gumbel_grid(123, 5, 3, 20, 20)
+    assert np.allclose(np.array(g).reshape(20, 20), grid, rtol=0, atol=1e-12)
+
+
+# ------------------------------------------------------------- budget ------
+def test_density_to_k_worked_examples():
+    for ex in _gold("spec_examples.json")["density_to_k"]:
+        assert oracle.density_to_k(ex["rho"], ex["n"]) == ex["k"], ex["cite"]
+
+
+def test_density_to_k_round_half_up():
+    """R-14: k = floor(rho N + 1/2): 0.15*1182 = 177.3 -> 177; 0.5*5 = 2.5 -> 3."""
+    assert oracle.density_to_k(0.15, 1182) == 177
+    assert oracle.density_to_k(0.5, 5) == 3
+    assert oracle.density_to_k(0.15, 275) == 41
+
+
+def test_l1_curve_worked_example():
+    """adjacent mean-L1 of [0],[1],[3] is [1, 2] (velocity input)."""
+    ex = _gold("spec_examples.json")["l1_curve"]
+    t = [np.array(x) for x in ex["tensors"]]
+    curve = [oracle.l1(t[i + 1], t[i], kind=1) for i in range(len(t) - 1)]
+    assert curve == ex["curve"]
+
+
+def _velocity_pair(l):
+    """Two velocity fields whose mean |difference| is exactly l."""
+    a = np.zeros(8)
+    return a + l, a
+
+
+def test_schedule_worked_examples():
+    """Eqs. 9-11 worked through SPEC.md:406-407 (clip rule R-18)."""
+    for ex in _gold("spec_examples.json")["schedule"]:
+        ls = ex["l"]
+        lbar = sum(ls) / len(ls)
+        T = 10 + len(ls)
+        for n, (l, want) in enumerate(zip(ls, ex["rho_t"])):
+            x_t, x_tm1 = _velocity_pair(l)
+            out = oracle.budget(x_t, x_tm1, kind=1, T=T, step=10 + n, rho=ex["rho"],
+                                dense_frac=0.2, l1_mean=lbar)
+            assert out["l1"] == l
+            assert out["rho_t"] == pytest.approx(want, rel=1e-15, abs=1e-15), ex["cite"]
+            assert out["clipped"] == ex["clipped"][n]
+            assert not out["dense"]
+        if "alpha" in ex:
+            for n, (l, a) in enumerate(zip(ls, ex["alpha"])):
+                x_t, x_tm1 = _velocity_pair(l)
+                out = oracle.budget(x_t, x_tm1, kind=1, T=T, step=10 + n, rho=ex["rho"],
+                                    l1_mean=lbar)
+                assert out["alpha"] == pytest.approx(a, rel=1e-15)
+
+
+def test_dense_prefix():
+    """full attention on the first 20% of T = 50 steps -> steps 0..9."""
+    ex = _gold("spec_examples.json")["dense_prefix"]
+    x = np.zeros(4)
+    dense = [oracle.budget(x + 1, x, x - 1, T=ex["T"], step=t, dense_frac=ex["dense_frac"],
+                           l1_mean=1.0)["dense"] for t in range(ex["T"])]
+    assert sum(dense) == ex["n_dense"] and all(dense[:ex["n_dense"]])
+
+
+def test_budget_conservation_eq11_and_scale_invariance():
+    """sum_{t in T_sparse} rho_t = rho |T_sparse| (unit-mean alpha);
+    Eq. 10 is invariant to scaling the l-curve."""
+    rng = np.random.default_rng(0)
+    T, rho = 50, 0.15
+    ls = rng.uniform(0.2, 1.0, size=40)  # small enough that nothing clips
+    for scale in (1.0, 7.5):
+        lbar = float(np.mean(ls * scale))
+        rts = []
+        for n, l in enumerate(ls * scale):
+            x_t, x_tm1 = _velocity_pair(l)
+            rts.append(oracle.budget(x_t, x_tm1, kind=1, T=T, step=10 + n, rho=rho,
+                                     l1_mean=lbar)["rho_t"])
+        assert sum(rts) == pytest.approx(rho * 40, rel=1e-12)
+        if scale == 1.0:
+            base = rts
+        else:
+            assert np.allclose(rts, base, rtol=1e-12, atol=0)
+
+
+def test_constant_curve_reduces_to_pisa():
+    """constant l-curve -> alpha = 1, rho_t = rho (uniform PISA budget)."""
+    x_t, x_tm1 = _velocity_pair(0.375)
+    for t in range(10, 50):
+        out = oracle.budget(x_t, x_tm1, kind=1, T=50, step=t, rho=0.15, l1_mean=0.375)
+        assert out["alpha"] == 1.0 and out["rho_t"] == 0.15
+
+
+def test_rho_table_mode():
+    """R-17: table mode reproduces the offline Eqs. 9-11 verbatim."""
+    tab = np.linspace(0.1, 0.3, 50)
+    x = np.zeros(4)
+    for t in (10, 25, 49):
+        out = oracle.budget(x + 2, x + 1, x, T=50, step=t, rho_table=tab, l1_mean=1.0)
+        assert out["rho_t"] == tab[t]
+
+
+def test_quadratic_trajectory_closed_form():
+    """B1 on x(sigma) = a + b sigma + c sigma^2 with unit steps: second difference
+    is 2c exactly, so l = 2 mean|c|; linear trajectories give l = 0."""
+    rng = np.random.default_rng(1)
+    n = 1000
+    a, b, c = (rng.integers(-50, 50, n).astype(np.float64) for _ in range(3))
+    xs = [a + b * s + c * s * s for s in (3.0, 4.0, 5.0)]
+    l = oracle.l1(xs[2], xs[1], xs[0], kind=0, h_t=1.0, h_tm1=1.0)
+    assert l == 2.0 * np.mean(np.abs(c))
+    lin = [a + b * s for s in (3.0, 4.0, 5.0)]
+    assert oracle.l1(lin[2], lin[1], lin[0]) == 0.0
+
+
+def test_budget_rejects_degenerate():
+    """l-bar <= 0 is rejected; h = 0 and step outside [0,T) too."""
+    x = np.zeros(4)
+    with pytest.raises(ValueError):
+        oracle.budget(x, x, x, l1_mean=0.0)
+    with pytest.raises(ValueError):
+        oracle.budget(x, x, x, h_t=0.0)
+    with pytest.raises(ValueError):
+        oracle.budget(x, x, x, T=50, step=50)
+
+
+def test_three_phase_trajectory_expectation():
+    """Online l_t on the synthetic trajectory matches E|v_{t-1} - v_{t-2}| =
+    sqrt(2/pi) sqrt(a_{t-1}^2 + a_{t-2}^2) (Gaussian mean absolute value)."""
+    import synth
+    tp = synth.ThreePhase(shape=(200_000,), T=50, seed=7)
+    for t in (11, 30, 48):
+        x_t, x_tm1, x_tm2 = tp.latents(t)
+        l = oracle.l1(x_t, x_tm1, x_tm2, kind=0, h_t=1 / 50, h_tm1=1 / 50)
+        assert l == pytest.approx(tp.expected_l1(t), rel=1.5e-2)
+    assert tp.expected_l1_mean() == pytest.approx(0.8352, abs=1e-4)
+
+
+# ------------------------------------------------------------- routing -----
+def _qk_from_scores(scores):
+    """D = 1, Bq = len, Bk = 1: Qbar = 1, Kbar_j = scores[j], s = 1 -> r = scores."""
+    n = len(scores)
+    q = np.ones((1, n, 1, 1))
+    k = np.array(scores, dtype=np.float64).reshape(1, n, 1, 1)
+    return q, k
+
+
+@pytest.mark.parametrize("name", ["topk", "topk_tie"])
+def test_topk_worked_examples(name):
+    ex = _gold("spec_examples.json")[name]
+    q, k = _qk_from_scores(ex["scores"])
+    r = oracle.route(q, k, Bq=len(ex["scores"]), Bk=1, beta=0.0, kk=ex["k"])
+    assert list(r["idx"][0, 0]) == ex["selected"], ex["cite"]
+
+
+def test_route_full_budget_selects_all():
+    rng = np.random.default_rng(2)
+    q, k = rng.standard_normal((2, 300, 2, 16)), rng.standard_normal((2, 300, 2, 16))
+    r = oracle.route(q, k, Bq=32, Bk=16, beta=0.1, rho_t=1.0)
+    NK = (300 + 15) // 16
+    assert r["kk"] == NK
+    assert (r["idx"] == np.arange(NK)).all()
+    assert (r["mask"][..., 0] == (1 << NK) - 1).all()
+
+
+def test_route_beta0_equals_full_sort_and_brute():
+    """beta = 0 -> deterministic top-k (north star), equal to a full lexsort, and the
+    C oracle agrees with the NumPy twin (beta = 0.1 too, bit-exact indices)."""
+    rng = np.random.default_rng(3)
+    B, S, H, D = 1, 777, 2, 32
+    q, k = rng.standard_normal((B, S, H, D)), rng.standard_normal((B, S, H, D))
+    for beta in (0.0, 0.1):
+        r = oracle.route(q, k, Bq=64, Bk=32, beta=beta, seed=99, step=17, kk=7,
+                         want_scores=True)
+        for h in range(H):
+            sel, rt = brute.route_head(q[0, :, h], k[0, :, h], 64, 32, 7, beta, 99, 17, h)
+            assert np.allclose(rt, r["scores"][h], rtol=0, atol=1e-12)
+            for i, s in enumerate(sel):
+                assert list(r["idx"][h, i]) == list(s)
+
+
+def test_route_row_constant_key_shift_invariant():
+    """K + 1 c^T adds s Qbar_i.c to every score of row i: sigma_i unchanged, ranking
+    unchanged (c chosen as a power of two so the shift is exact)."""
+    rng = np.random.default_rng(4)
+    q = rng.integers(-4, 4, (1, 256, 1, 8)).astype(np.float64)
+    k = rng.integers(-4, 4, (1, 256, 1, 8)).astype(np.float64)
+    a = oracle.route(q, k, Bq=64, Bk=16, beta=0.0, kk=5)
+    b = oracle.route(q, k + 2.0, Bq=64, Bk=16, beta=0.0, kk=5)
+    assert (a["idx"] == b["idx"]).all()
+
+
+def test_gumbel_max_law_k1():
+    """R-10: with k = 1, P(select j) = softmax(r_j / (beta sigma)) (Gumbel-max).
+    All query blocks share one Qbar; each row i draws independently."""
+    NQ, NK = 20000, 4
+    kbar = np.array([0.0, 0.5, 1.0, 1.5])
+    q = np.ones((1, NQ, 1, 1))
+    k = np.repeat(kbar, NQ // NK).reshape(1, NQ, 1, 1)  # 4 constant key blocks
+    beta = 2.0
+    r = oracle.route(q, k, Bq=1, Bk=NQ // NK, beta=beta, seed=2024, step=3, kk=1)
+    counts = np.bincount(r["idx"][0, :, 0], minlength=NK)
+    sigma = kbar.std()
+    p = np.exp(kbar / (beta * sigma))
+    p /= p.sum()
+    chi2 = float(((counts - NQ * p) ** 2 / (NQ * p)).sum())
+    assert chi2 < 16.27  # chi^2_3 at 0.001
+    assert np.allclose(counts / NQ, p, atol=0.015)
+
+
+def test_bias_entropy_increases_with_beta():
+    """SPEC.md:603 / PAPER.md:304 Fig. 4: the bias redistributes selections;
+    entropy of selection counts is non-decreasing in beta."""
+    rng = np.random.default_rng(5)
+    NQ, NK = 4000, 16
+    kbar = np.sort(rng.standard_normal(NK))
+    q = np.ones((1, NQ, 1, 1))
+    k = np.repeat(kbar, NQ // NK).reshape(1, NQ, 1, 1)
+    ent = []
+    for beta in (0.0, 0.1, 1.0):
+        r = oracle.route(q, k, Bq=1, Bk=NQ // NK, beta=beta, seed=11, step=0, kk=4)
+        c = np.bincount(r["idx"].ravel(), minlength=NK).astype(float)
+        p = c / c.sum()
+        ent.append(float(-(p[p > 0] * np.log(p[p > 0])).sum()))
+    assert ent[0] <= ent[1] <= ent[2]
+    assert ent[2] > ent[0] + 0.5
+
+
+def test_route_replay_and_global_head_keying():
+    """R-11/R-20: the draw depends on the global head gh = b*H_total + off + h, so
+    routing 2 local heads at offset 2 equals heads 2,3 of a 4-head call."""
+    rng = np.random.default_rng(6)
+    q, k = rng.standard_normal((1, 512, 4, 16)), rng.standard_normal((1, 512, 4, 16))
+    full = oracle.route(q, k, Bq=64, Bk=32, beta=0.5, seed=5, step=12, kk=4)
+    part = oracle.route(q[:, :, 2:], k[:, :, 2:], Bq=64, Bk=32, beta=0.5, seed=5, step=12,
+                        kk=4, H_total=4, head_offset=2)
+    assert (full["idx"][2:] == part["idx"]).all()
+    again = oracle.route(q, k, Bq=64, Bk=32, beta=0.5, seed=5, step=12, kk=4)
+    assert (full["idx"] == again["idx"]).all()
+    other = oracle.route(q, k, Bq=64, Bk=32, beta=0.5, seed=5, step=13, kk=4)
+    assert (full["idx"] != other["idx"]).any()
+
+
+def test_block_means_constant_block_exact():
+    """A constant dyadic block returns the constant exactly (R1; sums are exact)."""
+    x = np.full((100, 3), 0.375)
+    m = oracle.block_means(x, 32)
+    assert (m == 0.375).all()
