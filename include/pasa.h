@@ -1,0 +1,200 @@
+/*
+ * pasa.h -- C ABI of libpasa.so, a B200 (sm_100a) implementation of PASA's
+ * per-step sparse self-attention: budget -> route -> attn.
+ *
+ * Paper: "Ride the Wave: Precision-Allocated Sparse Attention for Smooth
+ * Video Generation", arXiv 2604.12219 (cited PAPER.md:<line>).  Readings of
+ * the paper where it is silent are numbered R-1..R-24 in DESIGN.md §3.
+ *
+ * Conventions shared by every call
+ * --------------------------------
+ *  - Every tensor pointer is a DEVICE pointer unless the argument says HOST.
+ *    The caller owns all memory, including the device workspaces (allocate
+ *    them with torch.empty / cudaMalloc); the library never allocates or
+ *    frees device memory, so every launching call can be captured in a CUDA
+ *    graph.  Handles are small host structs that point into a workspace.
+ *  - Launching calls are asynchronous on `stream` (a cudaStream_t passed as
+ *    void*; NULL = legacy default stream).  They validate on the host first
+ *    and launch nothing when validation fails.  Device faults surface at the
+ *    caller's next synchronisation (CUDA semantics).
+ *  - Return value: PASA_OK or an error status; pasa_last_error() returns a
+ *    thread-local message describing the last failure on this thread.
+ *  - Non-finite inputs are not checked on the hot path (the result is
+ *    undefined).
+ *  - A handle must not be used concurrently on two streams.
+ */
+#ifndef PASA_H
+#define PASA_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    PASA_OK = 0,
+    PASA_EINVAL = 1,        /* bad scalar argument (beta < 0, h = 0, step outside [0,T), ...) */
+    PASA_ESHAPE = 2,        /* shape / stride mismatch between tensors or with the handle      */
+    PASA_EDTYPE = 3,        /* dtype mismatch                                                    */
+    PASA_EUNSUPPORTED = 4,  /* D not in {64,128}, Bq not in {64,128}, Bk != 64, ...              */
+    PASA_EDEGENERATE = 5,   /* l-bar <= 0 (Eq. 10 cannot normalise)                 */
+    PASA_ECUDA = 6,         /* a CUDA launch or driver call failed                               */
+    PASA_ENOSPACE = 7       /* workspace smaller than the *_workspace_bytes() requirement        */
+} pasa_status;
+
+typedef enum { PASA_BF16 = 0, PASA_F32 = 1 } pasa_dtype;
+
+/* A [B, S, H, D] activation.  Strides are in ELEMENTS; D is contiguous (stride 1).
+ * The default DiT projection output is BSHD contiguous: sB = S*H*D, sS = H*D,
+ * sH = D.  data must be 16-byte aligned and sS, sH, sB multiples of 8 elements
+ * (TMA requirement).  (X in R^{B x N x S x D}; any stride order.) */
+typedef struct {
+    void* data;
+    int32_t dtype;          /* pasa_dtype */
+    int32_t _pad;
+    int64_t B, S, H, D;
+    int64_t sB, sS, sH;
+} pasa_tensor;
+
+/* A contiguous latent (or velocity) tensor of numel elements, fp32 or bf16. */
+typedef struct {
+    const void* data;
+    int32_t dtype;          /* pasa_dtype */
+    int32_t _pad;
+    int64_t numel;
+} pasa_latent;
+
+typedef enum { PASA_IN_LATENT = 0, PASA_IN_VELOCITY = 1 } pasa_budget_input;
+
+/* Budget schedule (Eqs. 9-11). */
+typedef struct {
+    int32_t T;               /* total denoising steps (50)                                     */
+    int32_t step;            /* current step t, 0-based, in [0, T)                             */
+    double rho;              /* baseline density rho (0.15 = "85% sparsity")     */
+    double dense_frac;       /* dense prefix fraction (0.20)                     */
+    double l1_mean;          /* l-bar of Eq. 9 from calibration; must be > 0                   */
+    double h_t, h_tm1;       /* sigma_t - sigma_{t-1}, sigma_{t-1} - sigma_{t-2}; != 0 (R-16)   */
+    double rho_max;          /* clip for rho_t (1.0, R-18)                                     */
+    const double* rho_table; /* HOST, optional length-T per-step rho_t (offline Eqs. 9-11), or NULL */
+    int32_t kind;            /* pasa_budget_input                                              */
+    int32_t _pad;
+} pasa_schedule;
+
+typedef enum { PASA_COMP_GROUPED = 0, PASA_COMP_ZEROTH = 1, PASA_COMP_NONE = 2 } pasa_comp;
+
+/* Routing / attention configuration (fixed per route handle). */
+typedef struct {
+    int32_t Bq;              /* query block: 64 or 128 (reading R-7)                           */
+    int32_t Bk;              /* key block: 64                                                  */
+    int32_t G;               /* blocks per group, >= 1 (32 default); G >= N_K = PISA global */
+    int32_t comp;            /* pasa_comp                                                      */
+    double beta;             /* bias scale >= 0 (0.1 default; 0 = deterministic top-k, R-10)   */
+    int64_t H_total;         /* global head count; Philox is keyed on the global head          */
+    int64_t head_offset;     /* this call's buffers hold global heads [off, off + H)           */
+} pasa_route_cfg;
+
+typedef struct pasa_budget_s* pasa_budget_h;
+typedef struct pasa_route_s* pasa_route_h;
+
+/* ---- workspaces and handles --------------------------------------------- */
+/* Budget workspace: the device record {l1, alpha, rho_t, dense, clipped} plus
+ * fixed-size fp64 partials of the reduction (a fixed grid, so l1 is
+ * bit-reproducible run to run). */
+size_t pasa_budget_workspace_bytes(void);
+/* Route workspace for tensors of shape [B, S, H, D]: pooled Qbar/Kbar (fp64),
+ * the low-precision Kbar / Vsum / grouped Hbar used by pasa_attn, the index
+ * list idx [B*H][N_Q][N_K] int32 (first count entries valid), count
+ * [B*H][N_Q] int32 and mask [B*H][N_Q][ceil(N_K/32)] u32.  Returns 0 if the
+ * configuration is invalid (see pasa_last_error()). */
+size_t pasa_route_workspace_bytes(const pasa_route_cfg* cfg, int64_t B, int64_t S, int64_t H,
+                                  int64_t D);
+/* Bind a handle to caller-owned device workspace `dev_ws` of `bytes` bytes.
+ * The handle itself is a host allocation released by *_fini (which never
+ * touches the workspace). */
+pasa_status pasa_budget_init(void* dev_ws, size_t bytes, pasa_budget_h* out);
+pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cfg, int64_t B,
+                            int64_t S, int64_t H, int64_t D, pasa_route_h* out);
+void pasa_budget_fini(pasa_budget_h h);
+void pasa_route_fini(pasa_route_h h);
+
+/* ---- the three calls of the hot path --------------------------------------
+ * pasa_budget -- PAPER.md:269-294, readings R-15..R-18:
+ *   l = mean_e |(x_t - x_{t-1})/h_t - (x_{t-1} - x_{t-2})/h_{t-1}|   (LATENT)
+ *   l = mean_e |x_t - x_{t-1}|                                      (VELOCITY;
+ *        x_tm2 may be NULL)
+ *   alpha = l / l1_mean (Eq. 10); rho_t = 1 in the dense prefix
+ *   (t < round(dense_frac*T) or t < 2), else min(rho*alpha or rho_table[t],
+ *   rho_max) (Eq. 11).  The record stays on the device; nothing syncs.
+ *   Latents: same numel and dtype, fp32 or bf16, contiguous.
+ *   Errors: EINVAL (T<1, step, h==0, NULL data), ESHAPE, EDTYPE,
+ *   EDEGENERATE (l1_mean <= 0). */
+pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
+                        const pasa_schedule* schedule, pasa_budget_h budget, void* stream);
+
+/* pasa_route -- PAPER.md:189-193 (block partition, top-k per query block),
+ * Eq. 8 pooled-logit term, stochastic bias
+ * (PAPER.md:296-308), readings R-6..R-14, R-20:
+ *   Qbar_i, Kbar_j = fp64 block means in ascending token order;
+ *   r_ij = s * dot(Qbar_i, Kbar_j) (fp64 fma chain), s = 1/sqrt(D);
+ *   rt_ij = r_ij + (beta*sigma_i) * Gumbel(Philox4x32-10(ctr=(j,i,gh,step),
+ *           key=seed)), sigma_i the population std of row i;
+ *   k = clamp(floor(rho_t*N_K + 0.5), 1, N_K) computed ON THE DEVICE from the
+ *   budget record; S_i = top-k of rt under (rt desc, j asc), stored ascending.
+ *   q, k: [B,S,H,D], same dtype (bf16 or fp32) and shape as the handle.
+ *   gh = b*H_total + head_offset + h.  `seed` is the per-layer key
+ *   (pasa_layer_seed(seed, layer)); reusing one seed across layers repeats the
+ *   bias and violates PAPER.md:308.
+ *   Errors: ESHAPE, EDTYPE, EINVAL (NULL handle). */
+pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h budget,
+                       uint64_t seed, int32_t step, pasa_route_h route, void* stream);
+
+/* pasa_attn -- Eq. 7 with grouped first-order
+ * compensation (App. B :494-506), readings R-1..R-5, R-21,
+ * R-22:
+ *   for each query row t of block i, with S_i from the route and U_i its
+ *   complement,
+ *   O_t = [ sum_{u in S_i} e^{s q.K_u - m} V_u + sum_{j in U_i} e^{s q.Kbar_j - m} Vsum_j
+ *           + sum_g A_{t,g} s q_t Hbar^(g) ]
+ *       / [ sum_{u in S_i} e^{s q.K_u - m} + sum_{j in U_i} n_j e^{s q.Kbar_j - m} ],
+ *   A_{t,g} = sum_{j in U_i cap G_g} e^{s q.Kbar_j - m}; comp ZEROTH drops the
+ *   Hbar term, NONE drops every U term.  q and k must be the buffers the route
+ *   was built from; v and out have the same B,S,H,D (out may have its own
+ *   strides).  bf16 I/O with Bq = 128 and G % 32 == 0 (or G >= N_K) runs the
+ *   tcgen05/TMEM/TMA kernel (fp32 accumulate; Kbar, Vsum, Hbar stored bf16,
+ *   R-21); fp32 I/O, Bq = 64 or finer groups run the fp32 CUDA-core kernel.
+ *   Errors: ESHAPE, EDTYPE, EINVAL (route never built). */
+pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                      pasa_route_h route, pasa_tensor* out, void* stream);
+
+/* pasa_attn with flags: PASA_ATTN_FORCE_SIMT runs the CUDA-core kernel even
+ * for bf16 I/O (cross-check of the tensor-core kernel). */
+#define PASA_ATTN_FORCE_SIMT 1u
+pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                         pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
+
+/* SplitMix64 finaliser of seed + (layer+1)*0x9E3779B97F4A7C15 (reading R-11):
+ * one independent Philox key per layer. */
+uint64_t pasa_layer_seed(uint64_t seed, int32_t layer);
+
+/* ---- synchronous diagnostics (tests) ------------------------------------- */
+/* out (HOST) = {l1, alpha, rho_t, dense, clipped}. Synchronises `stream`. */
+pasa_status pasa_budget_read(pasa_budget_h budget, double out[5], void* stream);
+/* HOST outputs, each may be NULL: k (1 int), idx [B*H][N_Q][N_K], count
+ * [B*H][N_Q], mask [B*H][N_Q][ceil(N_K/32)].  Synchronises `stream`. */
+pasa_status pasa_route_read(pasa_route_h route, int32_t* k, int32_t* idx, int32_t* count,
+                            uint32_t* mask, void* stream);
+/* HOST outputs (may be NULL): qbar [B*H][N_Q][D], kbar [B*H][N_K][D] fp64. */
+pasa_status pasa_route_pooled_read(pasa_route_h route, double* qbar, double* kbar, void* stream);
+/* Geometry of a handle: dims[0..6] = {B, S, H, D, N_Q, N_K, N_G}. */
+pasa_status pasa_route_dims(pasa_route_h route, int64_t dims[7]);
+/* Number of kernel launches the last pasa_budget / pasa_route / pasa_attn
+ * call on this thread issued (bench accounting). */
+int32_t pasa_last_launch_count(void);
+const char* pasa_last_error(void);
+const char* pasa_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PASA_H */

@@ -1,0 +1,7 @@
+"""PASA (arXiv 2604.12219) per-step sparse self-attention on B200 (sm_100a).
+
+budget -> route -> attn through the C ABI of libpasa.so (include/pasa.h).
+"""
+from .api import Budget, Route, RouteCfg, attn, last_launch_count, layer_seed  # noqa: F401
+
+__all__ = ["Budget", "Route", "RouteCfg", "attn", "layer_seed", "last_launch_count"]

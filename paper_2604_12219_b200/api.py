@@ -1,0 +1,187 @@
+"""Python face of libpasa.so: torch tensors in, C-ABI calls out.
+
+PyTorch supplies device memory (workspaces via ``torch.empty``), the current
+CUDA stream and nothing else; every arithmetic step runs in the library's
+CUDA kernels.  Names follow include/pasa.h: ``Budget`` wraps
+``pasa_budget``, ``Route`` wraps ``pasa_route``, ``attn`` wraps ``pasa_attn``.
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _C
+
+_DT = {torch.bfloat16: _C.PASA_BF16, torch.float32: _C.PASA_F32}
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream] = None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def tensor_desc(x: torch.Tensor) -> _C.PasaTensor:
+    """[B, S, H, D] CUDA tensor (D contiguous) -> pasa_tensor."""
+    if x.dim() != 4:
+        raise ValueError(f"expected [B, S, H, D], got shape {tuple(x.shape)}")
+    if not x.is_cuda:
+        raise ValueError("pasa tensors must live on a CUDA device")
+    if x.dtype not in _DT:
+        raise TypeError(f"dtype {x.dtype} not supported (bf16 or fp32)")
+    if x.stride(3) != 1:
+        raise ValueError("the head dimension D must be contiguous")
+    B, S, H, D = x.shape
+    return _C.PasaTensor(x.data_ptr(), _DT[x.dtype], 0, B, S, H, D, x.stride(0), x.stride(1),
+                         x.stride(2))
+
+
+def latent_desc(x: torch.Tensor) -> _C.PasaLatent:
+    if not x.is_cuda or not x.is_contiguous():
+        raise ValueError("latents must be contiguous CUDA tensors")
+    if x.dtype not in _DT:
+        raise TypeError(f"latent dtype {x.dtype} not supported")
+    return _C.PasaLatent(x.data_ptr(), _DT[x.dtype], 0, x.numel())
+
+
+def layer_seed(seed: int, layer: int) -> int:
+    """Per-layer Philox key (reading R-11): pasa_layer_seed(seed, layer)."""
+    return int(_C.lib().pasa_layer_seed(seed, layer))
+
+
+def last_launch_count() -> int:
+    return int(_C.lib().pasa_last_launch_count())
+
+
+class Budget:
+    """Device-resident budget record {l1, alpha, rho_t, dense, clipped} (Eqs. 9-11)."""
+
+    def __init__(self, device=None):
+        L = _C.lib()
+        self.device = torch.device(device if device is not None else "cuda")
+        n = L.pasa_budget_workspace_bytes()
+        self.ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _C.check(L.pasa_budget_init(ctypes.c_void_p(self.ws.data_ptr()), n, ctypes.byref(h)),
+                 "pasa_budget_init")
+        self.handle = h
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _C.lib().pasa_budget_fini(self.handle)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
+
+    def __call__(self, x_t, x_tm1, x_tm2=None, *, T=50, step=25, rho=0.15, dense_frac=0.2,
+                 l1_mean=1.0, h_t=1.0, h_tm1=1.0, rho_max=1.0, rho_table=None, kind="latent",
+                 stream=None):
+        kind_i = _C.PASA_IN_VELOCITY if kind == "velocity" else _C.PASA_IN_LATENT
+        a, b = latent_desc(x_t), latent_desc(x_tm1)
+        c = latent_desc(x_tm2) if x_tm2 is not None else None
+        tab = None
+        if rho_table is not None:
+            self._tab = np.ascontiguousarray(np.asarray(rho_table, dtype=np.float64))
+            tab = self._tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+        sc = _C.PasaSchedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, tab, kind_i, 0)
+        st = _C.lib().pasa_budget(ctypes.byref(a), ctypes.byref(b),
+                                  ctypes.byref(c) if c is not None else None, ctypes.byref(sc),
+                                  self.handle, _stream_ptr(stream))
+        _C.check(st, "pasa_budget")
+        return self
+
+    def read(self, stream=None) -> dict:
+        out = (ctypes.c_double * 5)()
+        _C.check(_C.lib().pasa_budget_read(self.handle, out, _stream_ptr(stream)),
+                 "pasa_budget_read")
+        return dict(l1=out[0], alpha=out[1], rho_t=out[2], dense=bool(out[3]),
+                    clipped=bool(out[4]))
+
+
+@dataclass
+class RouteCfg:
+    Bq: int = 128
+    Bk: int = 64
+    G: int = 32
+    comp: str = "grouped"
+    beta: float = 0.1
+    H_total: Optional[int] = None
+    head_offset: int = 0
+
+    def to_c(self, H: int) -> _C.PasaRouteCfg:
+        return _C.PasaRouteCfg(self.Bq, self.Bk, self.G, _C.COMP[self.comp], self.beta,
+                               self.H_total if self.H_total is not None else H, self.head_offset)
+
+
+class Route:
+    """Route workspace + handle for [B, S, H, D] activations (pasa_route_init)."""
+
+    def __init__(self, B, S, H, D, cfg: Optional[RouteCfg] = None, device=None):
+        L = _C.lib()
+        self.cfg = cfg or RouteCfg()
+        self.shape = (B, S, H, D)
+        self.device = torch.device(device if device is not None else "cuda")
+        c = self.cfg.to_c(H)
+        self._c = c
+        n = L.pasa_route_workspace_bytes(ctypes.byref(c), B, S, H, D)
+        if n == 0:
+            raise _C.PasaError(_C.PASA_EINVAL, "pasa_route_workspace_bytes",
+                               L.pasa_last_error().decode())
+        self.ws = torch.empty(n, dtype=torch.uint8, device=self.device)
+        h = ctypes.c_void_p()
+        _C.check(L.pasa_route_init(ctypes.c_void_p(self.ws.data_ptr()), n, ctypes.byref(c), B, S,
+                                   H, D, ctypes.byref(h)), "pasa_route_init")
+        self.handle = h
+        dims = (ctypes.c_int64 * 7)()
+        _C.check(L.pasa_route_dims(h, dims), "pasa_route_dims")
+        self.NQ, self.NK, self.NG = dims[4], dims[5], dims[6]
+        self.W = (self.NK + 31) // 32
+
+    def __del__(self):
+        try:
+            if getattr(self, "handle", None):
+                _C.lib().pasa_route_fini(self.handle)
+        except Exception:  # pragma: no cover
+            pass
+
+    def __call__(self, q, k, budget: Budget, seed: int, step: int, stream=None):
+        qd, kd = tensor_desc(q), tensor_desc(k)
+        _C.check(_C.lib().pasa_route(ctypes.byref(qd), ctypes.byref(kd), budget.handle, seed,
+                                     step, self.handle, _stream_ptr(stream)), "pasa_route")
+        return self
+
+    def read(self, stream=None) -> dict:
+        B, S, H, D = self.shape
+        BH = B * H
+        k = np.zeros(1, np.int32)
+        idx = np.zeros((BH, self.NQ, self.NK), np.int32)
+        cnt = np.zeros((BH, self.NQ), np.int32)
+        mask = np.zeros((BH, self.NQ, self.W), np.uint32)
+        P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+        _C.check(_C.lib().pasa_route_read(self.handle, P(k), P(idx), P(cnt), P(mask),
+                                          _stream_ptr(stream)), "pasa_route_read")
+        return dict(k=int(k[0]), idx=idx, count=cnt, mask=mask)
+
+    def pooled(self, stream=None):
+        B, S, H, D = self.shape
+        qb = np.zeros((B * H, self.NQ, D))
+        kb = np.zeros((B * H, self.NK, D))
+        _C.check(_C.lib().pasa_route_pooled_read(self.handle, ctypes.c_void_p(qb.ctypes.data),
+                                                 ctypes.c_void_p(kb.ctypes.data),
+                                                 _stream_ptr(stream)), "pasa_route_pooled_read")
+        return qb, kb
+
+
+def attn(q, k, v, route: Route, out=None, *, force_simt=False, stream=None):
+    """pasa_attn: returns out ([B, S, H, D], q's dtype)."""
+    if out is None:
+        out = torch.empty_like(q)
+    qd, kd, vd, od = tensor_desc(q), tensor_desc(k), tensor_desc(v), tensor_desc(out)
+    flags = _C.PASA_ATTN_FORCE_SIMT if force_simt else 0
+    _C.check(_C.lib().pasa_attn_ex(ctypes.byref(qd), ctypes.byref(kd), ctypes.byref(vd),
+                                   route.handle, ctypes.byref(od), flags, _stream_ptr(stream)),
+             "pasa_attn")
+    return out

@@ -1,0 +1,331 @@
+// api.cpp -- the C ABI of libpasa.so (include/pasa.h): argument validation,
+// workspace layout and kernel launches.  Every entry point validates on the
+// host and launches nothing on failure; no call allocates device memory.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "pasa_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_launches = 0;
+
+pasa_status fail(pasa_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+pasa_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return PASA_OK;
+    return fail(PASA_ECUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+constexpr size_t kAlign = 1024;
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct RouteLayout {
+    int64_t NQ, NK, NG, W, BH;
+    size_t off_hdr, off_qbar, off_kbar, off_scores, off_kbar_lp, off_vsum, off_ht, off_idx,
+        off_count, off_mask, total;
+};
+
+pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int64_t D) {
+    if (!c) return fail(PASA_EINVAL, "route cfg is NULL");
+    if (B < 1 || S < 1 || H < 1) return fail(PASA_ESHAPE, "B, S, H must be >= 1");
+    if (D != 64 && D != 128) return fail(PASA_EUNSUPPORTED, "D=%lld not in {64,128}", (long long)D);
+    if (c->Bq != 64 && c->Bq != 128)
+        return fail(PASA_EUNSUPPORTED, "Bq=%d not in {64,128}", c->Bq);
+    if (c->Bk != 64) return fail(PASA_EUNSUPPORTED, "Bk=%d != 64", c->Bk);
+    if (c->G < 1) return fail(PASA_EINVAL, "G=%d < 1", c->G);
+    if (c->comp < 0 || c->comp > 2) return fail(PASA_EINVAL, "comp=%d", c->comp);
+    if (!(c->beta >= 0.0) || !std::isfinite(c->beta))
+        return fail(PASA_EINVAL, "beta must be finite and >= 0");
+    if (c->head_offset < 0 || c->H_total < c->head_offset + H)
+        return fail(PASA_EINVAL, "head_offset=%lld H=%lld exceed H_total=%lld",
+                    (long long)c->head_offset, (long long)H, (long long)c->H_total);
+    const int64_t NK = (S + c->Bk - 1) / c->Bk;
+    if (NK > 2048) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 2048 (S too long)", (long long)NK);
+    return PASA_OK;
+}
+
+RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int64_t D) {
+    RouteLayout L;
+    L.NQ = (S + c->Bq - 1) / c->Bq;
+    L.NK = (S + c->Bk - 1) / c->Bk;
+    L.NG = (L.NK + c->G - 1) / c->G;
+    L.W = (L.NK + 31) / 32;
+    L.BH = B * H;
+    size_t o = 0;
+    L.off_hdr = o;      o = align_up(o + 64);
+    L.off_qbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NQ * D);
+    L.off_kbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NK * D);
+    L.off_scores = o;   o = align_up(o + sizeof(double) * L.BH * L.NQ * L.NK);
+    L.off_kbar_lp = o;  o = align_up(o + 4 * L.BH * L.NK * D);
+    L.off_vsum = o;     o = align_up(o + 4 * L.BH * L.NK * D);
+    L.off_ht = o;       o = align_up(o + 4 * L.BH * L.NG * D * D);
+    L.off_idx = o;      o = align_up(o + sizeof(int32_t) * L.BH * L.NQ * L.NK);
+    L.off_count = o;    o = align_up(o + sizeof(int32_t) * L.BH * L.NQ);
+    L.off_mask = o;     o = align_up(o + sizeof(uint32_t) * L.BH * L.NQ * L.W);
+    L.total = o;
+    return L;
+}
+
+size_t elem_size(int32_t dt) { return dt == PASA_F32 ? 4 : 2; }
+
+pasa_status check_tensor(const pasa_tensor* t, const char* name) {
+    if (!t || !t->data) return fail(PASA_EINVAL, "%s is NULL", name);
+    if (t->dtype != PASA_BF16 && t->dtype != PASA_F32)
+        return fail(PASA_EDTYPE, "%s dtype %d", name, t->dtype);
+    if (t->B < 1 || t->S < 1 || t->H < 1) return fail(PASA_ESHAPE, "%s has an empty dim", name);
+    if ((reinterpret_cast<uintptr_t>(t->data) & 15) != 0)
+        return fail(PASA_ESHAPE, "%s data not 16-byte aligned", name);
+    const int64_t m = 16 / (int64_t)elem_size(t->dtype);
+    if (t->sS % m || t->sH % m || t->sB % m || t->sS <= 0 || t->sH <= 0 || t->sB <= 0)
+        return fail(PASA_ESHAPE, "%s strides (%lld,%lld,%lld) must be positive multiples of 16 B",
+                    name, (long long)t->sB, (long long)t->sS, (long long)t->sH);
+    return PASA_OK;
+}
+
+pasa_status match_route(const pasa_tensor* t, const pasa_route_s* r, const char* name) {
+    if (t->B != r->B || t->S != r->S || t->H != r->H || t->D != r->D)
+        return fail(PASA_ESHAPE, "%s shape [%lld,%lld,%lld,%lld] != route [%lld,%lld,%lld,%lld]",
+                    name, (long long)t->B, (long long)t->S, (long long)t->H, (long long)t->D,
+                    (long long)r->B, (long long)r->S, (long long)r->H, (long long)r->D);
+    return PASA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pasa_last_error(void) { return g_err.c_str(); }
+int32_t pasa_last_launch_count(void) { return g_launches; }
+const char* pasa_version(void) { return "pasa-b200 0.1 (sm_100a)"; }
+
+uint64_t pasa_layer_seed(uint64_t seed, int32_t layer) {
+    uint64_t z = seed + (uint64_t)((int64_t)layer + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+size_t pasa_budget_workspace_bytes(void) {
+    return sizeof(pasa::BudgetRec) + sizeof(double) * pasa::kBudgetParts;
+}
+
+size_t pasa_route_workspace_bytes(const pasa_route_cfg* cfg, int64_t B, int64_t S, int64_t H,
+                                  int64_t D) {
+    if (check_cfg(cfg, B, S, H, D) != PASA_OK) return 0;
+    return layout(cfg, B, S, H, D).total;
+}
+
+pasa_status pasa_budget_init(void* dev_ws, size_t bytes, pasa_budget_h* out) {
+    if (!dev_ws || !out) return fail(PASA_EINVAL, "NULL workspace or handle pointer");
+    if (bytes < pasa_budget_workspace_bytes())
+        return fail(PASA_ENOSPACE, "budget workspace %zu < %zu", bytes,
+                    pasa_budget_workspace_bytes());
+    if (reinterpret_cast<uintptr_t>(dev_ws) & 15) return fail(PASA_EINVAL, "workspace misaligned");
+    auto* h = new (std::nothrow) pasa_budget_s;
+    if (!h) return fail(PASA_EINVAL, "out of host memory");
+    h->rec = reinterpret_cast<pasa::BudgetRec*>(dev_ws);
+    h->partials = reinterpret_cast<double*>(reinterpret_cast<char*>(dev_ws) +
+                                            sizeof(pasa::BudgetRec));
+    *out = h;
+    return PASA_OK;
+}
+
+pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cfg, int64_t B,
+                            int64_t S, int64_t H, int64_t D, pasa_route_h* out) {
+    pasa_status st = check_cfg(cfg, B, S, H, D);
+    if (st != PASA_OK) return st;
+    if (!dev_ws || !out) return fail(PASA_EINVAL, "NULL workspace or handle pointer");
+    if (reinterpret_cast<uintptr_t>(dev_ws) % 256) return fail(PASA_EINVAL, "workspace must be 256-byte aligned");
+    RouteLayout L = layout(cfg, B, S, H, D);
+    if (bytes < L.total) return fail(PASA_ENOSPACE, "route workspace %zu < %zu", bytes, L.total);
+    auto* r = new (std::nothrow) pasa_route_s;
+    if (!r) return fail(PASA_EINVAL, "out of host memory");
+    char* w = reinterpret_cast<char*>(dev_ws);
+    r->cfg = *cfg;
+    r->B = B; r->S = S; r->H = H; r->D = D;
+    r->NQ = L.NQ; r->NK = L.NK; r->NG = L.NG; r->W = L.W; r->BH = L.BH;
+    r->hdr = reinterpret_cast<int32_t*>(w + L.off_hdr);
+    r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
+    r->kbar = reinterpret_cast<double*>(w + L.off_kbar);
+    r->scores = reinterpret_cast<double*>(w + L.off_scores);
+    r->kbar_lp = w + L.off_kbar_lp;
+    r->vsum_lp = w + L.off_vsum;
+    r->ht = w + L.off_ht;
+    r->idx = reinterpret_cast<int32_t*>(w + L.off_idx);
+    r->count = reinterpret_cast<int32_t*>(w + L.off_count);
+    r->mask = reinterpret_cast<uint32_t*>(w + L.off_mask);
+    r->route_dtype = -1;
+    *out = r;
+    return PASA_OK;
+}
+
+void pasa_budget_fini(pasa_budget_h h) { delete h; }
+void pasa_route_fini(pasa_route_h h) { delete h; }
+
+pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
+                        const pasa_schedule* sc, pasa_budget_h budget, void* stream) {
+    g_launches = 0;
+    if (!budget || !sc || !x_t || !x_tm1) return fail(PASA_EINVAL, "NULL argument");
+    const bool vel = sc->kind == PASA_IN_VELOCITY;
+    if (sc->kind != PASA_IN_LATENT && !vel) return fail(PASA_EINVAL, "kind=%d", sc->kind);
+    if (!vel && !x_tm2) return fail(PASA_EINVAL, "x_tm2 is NULL for latent input");
+    if (sc->T < 1 || sc->step < 0 || sc->step >= sc->T)
+        return fail(PASA_EINVAL, "step=%d outside [0, T=%d)", sc->step, sc->T);
+    if (!vel && (sc->h_t == 0.0 || sc->h_tm1 == 0.0)) return fail(PASA_EINVAL, "h == 0");
+    if (!(sc->l1_mean > 0.0)) return fail(PASA_EDEGENERATE, "l1_mean must be > 0 (Eq. 10)");
+    if (!(sc->rho >= 0.0) || !(sc->rho_max > 0.0) || !(sc->dense_frac >= 0.0))
+        return fail(PASA_EINVAL, "rho / rho_max / dense_frac out of range");
+    const pasa_latent* xs[3] = {x_t, x_tm1, vel ? x_tm1 : x_tm2};
+    for (int i = 0; i < 3; ++i) {
+        if (!xs[i]->data) return fail(PASA_EINVAL, "latent %d data is NULL", i);
+        if (xs[i]->dtype != x_t->dtype) return fail(PASA_EDTYPE, "latent dtypes differ");
+        if (xs[i]->dtype != PASA_BF16 && xs[i]->dtype != PASA_F32)
+            return fail(PASA_EDTYPE, "latent dtype %d", xs[i]->dtype);
+        if (xs[i]->numel != x_t->numel) return fail(PASA_ESHAPE, "latent numel differ");
+        if (reinterpret_cast<uintptr_t>(xs[i]->data) & 15)
+            return fail(PASA_ESHAPE, "latent %d not 16-byte aligned", i);
+    }
+    if (x_t->numel < 1) return fail(PASA_ESHAPE, "empty latent");
+    const int32_t dense_steps = (int32_t)std::floor(sc->dense_frac * (double)sc->T + 0.5);
+    const int use_table = sc->rho_table != nullptr;
+    const double tv = use_table ? sc->rho_table[sc->step] : 0.0;
+    int launches = 0;
+    cudaError_t e = pasa::launch_budget(
+        x_t->data, x_tm1->data, xs[2]->data, x_t->numel, x_t->dtype, vel ? 1 : 0, sc->h_t,
+        sc->h_tm1, sc->step, dense_steps, sc->rho, sc->l1_mean, sc->rho_max, use_table, tv,
+        budget, (cudaStream_t)stream, &launches);
+    g_launches = launches;
+    return cuda_status(e, "pasa_budget launch");
+}
+
+pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h budget,
+                       uint64_t seed, int32_t step, pasa_route_h route, void* stream) {
+    g_launches = 0;
+    if (!route || !budget) return fail(PASA_EINVAL, "NULL handle");
+    pasa_status st;
+    if ((st = check_tensor(q, "q")) != PASA_OK) return st;
+    if ((st = check_tensor(k, "k")) != PASA_OK) return st;
+    if (q->dtype != k->dtype) return fail(PASA_EDTYPE, "q and k dtypes differ");
+    if ((st = match_route(q, route, "q")) != PASA_OK) return st;
+    if ((st = match_route(k, route, "k")) != PASA_OK) return st;
+    int launches = 0;
+    cudaError_t e = pasa::launch_route(*q, *k, budget, seed, step, route, (cudaStream_t)stream,
+                                       &launches);
+    g_launches = launches;
+    if (e == cudaSuccess) route->route_dtype = q->dtype;
+    return cuda_status(e, "pasa_route launch");
+}
+
+pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                         pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream) {
+    g_launches = 0;
+    if (!route) return fail(PASA_EINVAL, "NULL route");
+    pasa_status st;
+    if ((st = check_tensor(q, "q")) != PASA_OK) return st;
+    if ((st = check_tensor(k, "k")) != PASA_OK) return st;
+    if ((st = check_tensor(v, "v")) != PASA_OK) return st;
+    if ((st = check_tensor(out, "out")) != PASA_OK) return st;
+    if (q->dtype != k->dtype || q->dtype != v->dtype || q->dtype != out->dtype)
+        return fail(PASA_EDTYPE, "q, k, v, out dtypes differ");
+    if ((st = match_route(q, route, "q")) != PASA_OK) return st;
+    if ((st = match_route(k, route, "k")) != PASA_OK) return st;
+    if ((st = match_route(v, route, "v")) != PASA_OK) return st;
+    if ((st = match_route(out, route, "out")) != PASA_OK) return st;
+    if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route)");
+    int launches = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = pasa::launch_kv_stats(*k, *v, route, s, &launches);
+    if (e != cudaSuccess) { g_launches = launches; return cuda_status(e, "kv_stats launch"); }
+    // The tensor-core kernel covers bf16 I/O with Bq = 128 and G % 32 == 0 (or one
+    // global group); fp32 I/O, Bq = 64 and finer groups run the CUDA-core kernel
+    // (documented in include/pasa.h and DESIGN.md §7).
+    const pasa_route_cfg& c = route->cfg;
+    const bool fine_groups = c.comp == PASA_COMP_GROUPED && c.G % 32 != 0 && c.G < route->NK;
+    const bool simt = q->dtype == PASA_F32 || (flags & PASA_ATTN_FORCE_SIMT) || c.Bq != 128 ||
+                      fine_groups;
+    if (simt) {
+        e = pasa::launch_attn_simt(*q, *k, *v, route, *out, s, &launches);
+    } else {
+        char why[256] = {0};
+        e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        if (e == cudaErrorNotSupported) {
+            g_launches = launches;
+            return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);
+        }
+    }
+    g_launches = launches;
+    return cuda_status(e, "attention launch");
+}
+
+pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                      pasa_route_h route, pasa_tensor* out, void* stream) {
+    return pasa_attn_ex(q, k, v, route, out, 0u, stream);
+}
+
+pasa_status pasa_budget_read(pasa_budget_h budget, double out[5], void* stream) {
+    if (!budget || !out) return fail(PASA_EINVAL, "NULL argument");
+    pasa::BudgetRec rec;
+    cudaError_t e = cudaMemcpyAsync(&rec, budget->rec, sizeof(rec), cudaMemcpyDeviceToHost,
+                                    (cudaStream_t)stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize((cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_status(e, "pasa_budget_read");
+    out[0] = rec.l1; out[1] = rec.alpha; out[2] = rec.rho_t; out[3] = rec.dense; out[4] = rec.clipped;
+    return PASA_OK;
+}
+
+pasa_status pasa_route_read(pasa_route_h r, int32_t* k, int32_t* idx, int32_t* count,
+                            uint32_t* mask, void* stream) {
+    if (!r) return fail(PASA_EINVAL, "NULL route");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (k && e == cudaSuccess) e = cudaMemcpyAsync(k, r->hdr, 4, cudaMemcpyDeviceToHost, s);
+    if (idx && e == cudaSuccess)
+        e = cudaMemcpyAsync(idx, r->idx, sizeof(int32_t) * r->BH * r->NQ * r->NK,
+                            cudaMemcpyDeviceToHost, s);
+    if (count && e == cudaSuccess)
+        e = cudaMemcpyAsync(count, r->count, sizeof(int32_t) * r->BH * r->NQ,
+                            cudaMemcpyDeviceToHost, s);
+    if (mask && e == cudaSuccess)
+        e = cudaMemcpyAsync(mask, r->mask, sizeof(uint32_t) * r->BH * r->NQ * r->W,
+                            cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e, "pasa_route_read");
+}
+
+pasa_status pasa_route_pooled_read(pasa_route_h r, double* qbar, double* kbar, void* stream) {
+    if (!r) return fail(PASA_EINVAL, "NULL route");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (qbar) e = cudaMemcpyAsync(qbar, r->qbar, sizeof(double) * r->BH * r->NQ * r->D,
+                                  cudaMemcpyDeviceToHost, s);
+    if (kbar && e == cudaSuccess)
+        e = cudaMemcpyAsync(kbar, r->kbar, sizeof(double) * r->BH * r->NK * r->D,
+                            cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e, "pasa_route_pooled_read");
+}
+
+pasa_status pasa_route_dims(pasa_route_h r, int64_t dims[7]) {
+    if (!r || !dims) return fail(PASA_EINVAL, "NULL argument");
+    dims[0] = r->B; dims[1] = r->S; dims[2] = r->H; dims[3] = r->D;
+    dims[4] = r->NQ; dims[5] = r->NK; dims[6] = r->NG;
+    return PASA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,581 @@
+// attn_sm100.cu -- pasa_attn on the Blackwell tensor cores (sm_100a):
+// gather-driven block-sparse attention with the PASA compensation fused into
+// the same online softmax (Eq. 7; grouped first-order term,
+// PAPER.md:310-313 and App. B :503-506; readings R-1..R-5, R-21, R-22 in
+// DESIGN.md §3).  Design notes: DESIGN.md §7.
+//
+// One CTA per (head, 128-row query block); 2 CTAs per SM (TMEM 2 x 256 cols,
+// ~97 KB smem each) so one CTA's softmax overlaps the other's MMAs.
+// Warp roles (256 threads):
+//   warp 0  TMA producer of the K ring (K tiles / Kbar chunks / Hbar^T box 0)
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 2  TMA producer of the V ring (V tiles / Vsum chunks / Hbar^T box 1)
+//   warps 4-7  softmax / correction / epilogue, one query row per thread
+// The CTA walks one "op" list:
+//   E(j)  kept block j:        S = Q K_j^T (SS MMA) -> softmax -> O += P V_j (TS MMA)
+//   C(c)  centroid chunk c:    S = Q Kbar_c^T -> masked to the dropped blocks,
+//                              weights n_j in the denominator -> O += P Vsum_c
+//   F(g)  group g's first order: O += (s A_g (.) Q) Hbar^(g)  (TS MMA, A from TMEM)
+// The running max only moves up by more than 2^8 (log2 domain) before O is
+// rescaled, so O corrections are rare; they wait for the previous MMA first.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "pasa_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace pasa {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 256;
+constexpr int kBQ = 128, kBK = 64;
+constexpr int kMaxOps = 2048 + 32 + 64 + 64;
+constexpr int kTmemCols = 256;
+constexpr int kColS = 128;            // S/P/Aq buffers at TMEM columns 128 and 192
+constexpr float kRescaleThresh = 8.f; // log2 units
+
+enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
+__device__ __forceinline__ int32_t op_make(int32_t type, int32_t v) { return (type << 24) | v; }
+__device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 24; }
+__device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0xFFFFFF; }
+
+template <int D>
+struct Geo {
+    static constexpr int NBOX = D / 64;
+    static constexpr int QBOX = kBQ * 128;          // bytes per 64-col box of Q
+    static constexpr int KVBOX = kBK * 128;         // bytes per 64-col box of a K/V tile
+    static constexpr int SLOT = kBK * D * 2;        // bytes per K or V slot
+    static constexpr int HTBOX = D * 128;           // bytes per 64-col box of Hbar^T
+    static constexpr int OFF_Q = 0;
+    static constexpr int OFF_K = kBQ * D * 2;
+    static constexpr int OFF_V = OFF_K + 2 * SLOT;
+    static constexpr int BYTES = OFF_V + 2 * SLOT;
+    static_assert(HTBOX <= SLOT, "an Hbar^T box must fit one ring slot");
+};
+
+struct Params {
+    int64_t S, H, NQ, NK, NG, W;
+    int32_t G, comp;
+    float scale_log2;   // s * log2(e)
+    float s;            // 1/sqrt(D)
+    const int32_t* idx;
+    const int32_t* count;
+    const uint32_t* mask;
+    __nv_bfloat16* out;
+    int64_t osB, osS, osH;
+};
+
+struct Ctl {
+    uint64_t q_full;
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t s_full[2], p_full[2], pv_done;
+    uint32_t tmem_base;
+    int32_t nops;
+    uint32_t mask[64];
+    int32_t ops[kMaxOps];
+};
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 2)
+    attn_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
+                      const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV,
+                      const __grid_constant__ CUtensorMap tmKb,
+                      const __grid_constant__ CUtensorMap tmVs,
+                      const __grid_constant__ CUtensorMap tmHt, const Params p) {
+    using G_ = Geo<D>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    __shared__ Ctl ctl;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t i = blockIdx.x, bh = blockIdx.y;
+    const int64_t b = bh / p.H, h = bh % p.H;
+    const int64_t row = bh * p.NQ + i;
+    const int32_t cnt = p.count[row];
+    const int64_t NK = p.NK;
+    const int nchunks = (int)((NK + 63) / 64);
+
+    // ---------------- setup: op list, mask row, barriers, TMEM ----------------
+    for (int w = tid; w < p.W; w += kThreads) ctl.mask[w] = p.mask[row * p.W + w];
+    for (int q = tid; q < cnt; q += kThreads) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
+    if (tid == 0) {
+        mbar_init(&ctl.q_full, 1);
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&ctl.k_full[s], 1);
+            mbar_init(&ctl.k_empty[s], 1);
+            mbar_init(&ctl.v_full[s], 1);
+            mbar_init(&ctl.v_empty[s], 1);
+            mbar_init(&ctl.s_full[s], 1);
+            mbar_init(&ctl.p_full[s], 128);
+        }
+        mbar_init(&ctl.pv_done, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(&ctl.tmem_base, kTmemCols);
+        tmem_relinquish();
+    }
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
+        tma_prefetch(&tmKb); tma_prefetch(&tmVs); tma_prefetch(&tmHt);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        // tail of the op list: centroid chunks with a dropped block, then the
+        // first-order op of every group that ends inside the chunk (G % 32 == 0
+        // or one global group: every 32-block half-chunk lies in one group)
+        int n = cnt;
+        if (p.comp != PASA_COMP_NONE && cnt < NK) {
+            auto dropped = [&](int64_t j) { return ((ctl.mask[j >> 5] >> (j & 31)) & 1u) == 0u; };
+            for (int c = 0; c < nchunks; ++c) {
+                const int64_t j0 = 64 * (int64_t)c, j1 = min(j0 + 64, NK);
+                bool any = false;
+                for (int64_t j = j0; j < j1 && !any; ++j) any = dropped(j);
+                if (any) ctl.ops[n++] = op_make(OP_C, c);
+                if (p.comp == PASA_COMP_GROUPED) {
+                    for (int64_t g = j0 / p.G; g <= (j1 - 1) / p.G; ++g) {
+                        const int64_t ge = min((g + 1) * (int64_t)p.G, NK) - 1;  // last block
+                        if (ge < j0 || ge >= j1) continue;
+                        bool anyg = false;
+                        for (int64_t j = g * p.G; j <= ge && !anyg; ++j) anyg = dropped(j);
+                        if (anyg) ctl.ops[n++] = op_make(OP_F, (int32_t)g);
+                    }
+                }
+            }
+        }
+        ctl.nops = n;
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const int nops = ctl.nops;
+    const uint32_t tbase = ctl.tmem_base;
+
+    if (warp == 0) {
+        // ======================= K-ring producer =======================
+        if (lane == 0) {
+            mbar_arrive_expect_tx(&ctl.q_full, kBQ * D * 2);
+#pragma unroll
+            for (int a = 0; a < G_::NBOX; ++a)
+                tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
+                            (int)(i * kBQ), (int)h, (int)b);
+            for (int n = 0; n < nops; ++n) {
+                const int s = n & 1;
+                mbar_wait(&ctl.k_empty[s], ((n >> 1) & 1) ^ 1);
+                uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
+                const int32_t op = ctl.ops[n];
+                const int v = op_val(op);
+                if (op_type(op) == OP_F) {
+                    mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
+                    tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
+                } else {
+                    mbar_arrive_expect_tx(&ctl.k_full[s], G_::SLOT);
+#pragma unroll
+                    for (int a = 0; a < G_::NBOX; ++a) {
+                        if (op_type(op) == OP_E)
+                            tma_load_4d(dst + a * G_::KVBOX, &tmK, &ctl.k_full[s], 64 * a, v * kBK,
+                                        (int)h, (int)b);
+                        else
+                            tma_load_3d(dst + a * G_::KVBOX, &tmKb, &ctl.k_full[s], 64 * a, v * 64,
+                                        (int)bh);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 2) {
+        // ======================= V-ring producer =======================
+        if (lane == 0) {
+            for (int n = 0; n < nops; ++n) {
+                const int s = n & 1;
+                mbar_wait(&ctl.v_empty[s], ((n >> 1) & 1) ^ 1);
+                uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
+                const int32_t op = ctl.ops[n];
+                const int v = op_val(op);
+                if (op_type(op) == OP_F) {
+                    if (G_::NBOX == 2) {
+                        mbar_arrive_expect_tx(&ctl.v_full[s], G_::HTBOX);
+                        tma_load_3d(dst, &tmHt, &ctl.v_full[s], 64, v * D, (int)bh);
+                    } else {
+                        mbar_arrive(&ctl.v_full[s]);
+                    }
+                } else {
+                    mbar_arrive_expect_tx(&ctl.v_full[s], G_::SLOT);
+#pragma unroll
+                    for (int a = 0; a < G_::NBOX; ++a) {
+                        if (op_type(op) == OP_E)
+                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.v_full[s], 64 * a, v * kBK,
+                                        (int)h, (int)b);
+                        else
+                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.v_full[s], 64 * a, v * 64,
+                                        (int)bh);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ======================= MMA issuer =======================
+        constexpr uint32_t kIdQK = idesc_bf16_f32(128, kBK, 0, 0);   // Q (K-major) x K^T (K-major)
+        constexpr uint32_t kIdPV = idesc_bf16_f32(128, D, 0, 1);     // P (TMEM) x V (MN-major)
+        constexpr uint32_t kIdF = idesc_bf16_f32(128, D, 0, 0);      // Aq (TMEM) x Hbar^T (K-major)
+        const uint32_t q_base = smem_u32(smem + G_::OFF_Q);
+        const uint32_t k_base = smem_u32(smem + G_::OFF_K);
+        const uint32_t v_base = smem_u32(smem + G_::OFF_V);
+        auto issue_qk = [&](int n) {
+            const int s = n & 1;
+            mbar_wait(&ctl.k_full[s], (n >> 1) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+                const uint32_t d = tbase + kColS + 64 * s;
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t off = (kk >> 2) * 0 + (kk & 3) * 32;
+                    const uint64_t ad = umma_desc_sw128(q_base + (kk >> 2) * G_::QBOX + off, 16, 1024);
+                    const uint64_t bd =
+                        umma_desc_sw128(k_base + s * G_::SLOT + (kk >> 2) * G_::KVBOX + off, 16, 1024);
+                    mma_ss(d, ad, bd, kIdQK, kk > 0);
+                }
+                mma_commit(&ctl.s_full[s]);
+                mma_commit(&ctl.k_empty[s]);
+            }
+            __syncwarp();
+        };
+        mbar_wait(&ctl.q_full, 0);
+        tc_fence_after();
+        if (nops > 0) issue_qk(0);
+        for (int n = 0; n < nops; ++n) {
+            const int s = n & 1;
+            if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
+            mbar_wait(&ctl.p_full[s], (n >> 1) & 1);
+            tc_fence_after();
+            mbar_wait(&ctl.v_full[s], (n >> 1) & 1);
+            tc_fence_after();
+            const int32_t op = ctl.ops[n];
+            if (op_type(op) != OP_F) {
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 16; ++kk) {
+                        const uint64_t bd =
+                            umma_desc_sw128(v_base + s * G_::SLOT + kk * 16 * 128, G_::KVBOX, 1024);
+                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdPV,
+                               (n > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    mma_commit(&ctl.v_empty[s]);
+                    mma_commit(&ctl.pv_done);
+                }
+            } else {
+                mbar_wait(&ctl.k_full[s], (n >> 1) & 1);
+                tc_fence_after();
+                if (lane == 0) {
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t box = (kk >> 2) == 0 ? k_base + s * G_::SLOT
+                                                            : v_base + s * G_::SLOT;
+                        const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
+                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdF, 1u);
+                    }
+                    mma_commit(&ctl.k_empty[s]);
+                    mma_commit(&ctl.v_empty[s]);
+                    mma_commit(&ctl.pv_done);
+                }
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // =================== softmax / correction / epilogue ===================
+        const int r = (warp & 3) * 32 + lane;                 // query row in the block
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t t_o = tbase + lane_off;
+        const uint8_t* qrow = smem + G_::OFF_Q;
+        float m = -INFINITY, l = 0.f;
+        float A_cur = 0.f, A_done = 0.f;
+        int64_t g_cur = -1, g_done = -1;
+        int pv_seen = -1;          // pv_done phases consumed (ops whose MMA completed)
+        int sc[2] = {0, 0};        // S-type ops seen per buffer (s_full parity)
+        const int64_t n_last = NK - 1;
+        const int nlast_len = (int)(p.S - n_last * 64);
+        auto consume_pv = [&](int upto) {
+            while (pv_seen < upto) {
+                ++pv_seen;
+                mbar_wait(&ctl.pv_done, pv_seen & 1);
+            }
+        };
+        for (int n = 0; n < nops; ++n) {
+            const int s = n & 1;
+            const int32_t op = ctl.ops[n];
+            const int type = op_type(op), v = op_val(op);
+            const uint32_t t_buf = tbase + lane_off + kColS + 64 * s;
+            if (type != OP_F) {
+                mbar_wait(&ctl.s_full[s], sc[s] & 1);
+                sc[s]++;
+                tc_fence_after();
+                uint32_t sa[32], sb[32];
+                tmem_ld32(t_buf, sa);
+                tmem_ld32(t_buf + 32, sb);
+                tmem_wait_ld();
+                // valid columns and denominator weights
+                uint64_t valid;
+                float wlast = 1.f;     // token count of block n_last (C ops)
+                int clast = -1;        // column of block n_last in this chunk (C ops)
+                if (type == OP_E) {
+                    const int nj = v == n_last ? nlast_len : 64;
+                    valid = nj >= 64 ? ~0ull : ((1ull << nj) - 1ull);
+                } else {
+                    const uint64_t kept = (uint64_t)ctl.mask[2 * v] |
+                                          ((2 * v + 1 < p.W) ? (uint64_t)ctl.mask[2 * v + 1] << 32 : 0ull);
+                    const int64_t rem = NK - 64 * (int64_t)v;
+                    const uint64_t inb = rem >= 64 ? ~0ull : ((1ull << rem) - 1ull);
+                    valid = ~kept & inb;
+                    if (rem <= 64) { clast = (int)(rem - 1); wlast = (float)nlast_len; }
+                }
+                float mx = -INFINITY;
+#pragma unroll
+                for (int c = 0; c < 32; ++c) {
+                    const float x0 = ((valid >> c) & 1ull) ? __uint_as_float(sa[c]) * p.scale_log2
+                                                           : -INFINITY;
+                    const float x1 = ((valid >> (c + 32)) & 1ull)
+                                         ? __uint_as_float(sb[c]) * p.scale_log2 : -INFINITY;
+                    sa[c] = __float_as_uint(x0);
+                    sb[c] = __float_as_uint(x1);
+                    mx = fmaxf(mx, fmaxf(x0, x1));
+                }
+                // logit of the ragged last block (C ops), before sa/sb are overwritten
+                float xlast = -INFINITY;
+                if (clast >= 0) {
+#pragma unroll
+                    for (int c = 0; c < 32; ++c) {
+                        if (c == clast) xlast = __uint_as_float(sa[c]);
+                        if (c + 32 == clast) xlast = __uint_as_float(sb[c]);
+                    }
+                }
+                float corr = 1.f;
+                bool resc = false;
+                if (mx > m + kRescaleThresh) {
+                    corr = ex2(m - mx);       // 0 when m = -inf
+                    resc = n > 0;
+                    m = mx;
+                    l *= corr;
+                    A_cur *= corr;
+                }
+                if (__any_sync(0xffffffffu, resc)) {
+                    consume_pv(n - 1);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int c0 = 0; c0 < D; c0 += 32) {
+                        uint32_t o[32];
+                        tmem_ld32(t_o + c0, o);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int c = 0; c < 32; ++c) o[c] = __float_as_uint(__uint_as_float(o[c]) * corr);
+                        tmem_st32(t_o + c0, o);
+                    }
+                }
+                float h0 = 0.f, h1 = 0.f;
+                uint32_t pk[32];
+#pragma unroll
+                for (int c = 0; c < 16; ++c) {
+                    const float p0 = ex2(__uint_as_float(sa[2 * c]) - m);
+                    const float p1 = ex2(__uint_as_float(sa[2 * c + 1]) - m);
+                    const float p2 = ex2(__uint_as_float(sb[2 * c]) - m);
+                    const float p3 = ex2(__uint_as_float(sb[2 * c + 1]) - m);
+                    h0 += p0 + p1;
+                    h1 += p2 + p3;
+                    pk[c] = pack_bf16(p0, p1);
+                    pk[16 + c] = pack_bf16(p2, p3);
+                }
+                tmem_st32(t_buf, pk);
+                if (type == OP_E) {
+                    l += h0 + h1;
+                } else {
+                    // denominator: n_j * p_j; every dropped block has 64 tokens except the last
+                    const float pl = clast >= 0 ? ex2(xlast - m) : 0.f;
+                    l += 64.f * (h0 + h1) - (64.f - wlast) * pl;
+                    // group sums A_{t,g} (each 32-block half lies in one group)
+                    const int64_t j0 = 64 * (int64_t)v;
+                    const int64_t g0 = j0 / p.G;
+                    if (g0 != g_cur) { A_cur = 0.f; g_cur = g0; }
+                    A_cur += h0;
+                    if (j0 + 32 < NK) {
+                        const int64_t g1 = (j0 + 32) / p.G;
+                        if (g1 != g0) { A_done = A_cur; g_done = g0; A_cur = h1; g_cur = g1; }
+                        else A_cur += h1;
+                    }
+                }
+                tmem_wait_st();
+            } else {
+                // F(g): write Aq = bf16(s * A_{t,g} * q_t) into the TMEM A buffer
+                const float w = p.s * (v == g_done ? A_done : A_cur);
+#pragma unroll
+                for (int a = 0; a < G_::NBOX; ++a) {
+                    uint32_t aq[32];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 u = *reinterpret_cast<const uint4*>(
+                            qrow + a * G_::QBOX + r * 128 + ((c ^ (r & 7)) << 4));
+                        const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float lo = __uint_as_float(uw[e] << 16);
+                            const float hi = __uint_as_float(uw[e] & 0xFFFF0000u);
+                            aq[c * 4 + e] = pack_bf16(w * lo, w * hi);
+                        }
+                    }
+                    tmem_st32(t_buf + 32 * a, aq);
+                }
+                tmem_wait_st();
+            }
+            consume_pv(n - 1);
+            tc_fence_before();
+            mbar_arrive(&ctl.p_full[s]);
+        }
+        // ---- epilogue: O / l -> bf16 -> global ----
+        consume_pv(nops - 1);
+        tc_fence_after();
+        const int64_t t = i * kBQ + r;
+        const float inv = 1.f / l;
+        __nv_bfloat16* orow = p.out + b * p.osB + h * p.osH + t * p.osS;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(t_o + c0, o);
+            tmem_wait_ld();
+            if (t < p.S) {
+                uint4 pkt[4];
+                uint32_t* pw = reinterpret_cast<uint32_t*>(pkt);
+#pragma unroll
+                for (int c = 0; c < 16; ++c)
+                    pw[c] = pack_bf16(__uint_as_float(o[2 * c]) * inv, __uint_as_float(o[2 * c + 1]) * inv);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(orow + c0)[q] = pkt[q];
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tbase, kTmemCols);
+    }
+}
+
+// ---------------------------------------------------------------- host --
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box, char* why, size_t why_len) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) {
+        snprintf(why, why_len, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult rc = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base),
+                     reinterpret_cast<const cuuint64_t*>(dims),
+                     reinterpret_cast<const cuuint64_t*>(strides_bytes),
+                     reinterpret_cast<const cuuint32_t*>(box), estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+        snprintf(why, why_len, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
+        return false;
+    }
+    return true;
+}
+
+template <int D>
+cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                     pasa_route_s* r, const pasa_tensor& out, cudaStream_t st, char* why,
+                     size_t why_len) {
+    CUtensorMap mQ, mK, mV, mKb, mVs, mHt;
+    auto act = [&](CUtensorMap* m, const pasa_tensor& t, uint32_t rows) {
+        uint64_t dims[4] = {(uint64_t)t.D, (uint64_t)t.S, (uint64_t)t.H, (uint64_t)t.B};
+        uint64_t str[3] = {(uint64_t)t.sS * 2, (uint64_t)t.sH * 2, (uint64_t)t.sB * 2};
+        uint32_t box[4] = {64, rows, 1, 1};
+        return make_map(m, t.data, 4, dims, str, box, why, why_len);
+    };
+    if (!act(&mQ, q, kBQ) || !act(&mK, k, kBK) || !act(&mV, v, kBK))
+        return cudaErrorNotSupported;
+    {
+        uint64_t dims[3] = {(uint64_t)D, (uint64_t)r->NK, (uint64_t)r->BH};
+        uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)r->NK * D * 2};
+        uint32_t box[3] = {64, 64, 1};
+        if (!make_map(&mKb, r->kbar_lp, 3, dims, str, box, why, why_len) ||
+            !make_map(&mVs, r->vsum_lp, 3, dims, str, box, why, why_len))
+            return cudaErrorNotSupported;
+    }
+    {
+        uint64_t dims[3] = {(uint64_t)D, (uint64_t)r->NG * D, (uint64_t)r->BH};
+        uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)r->NG * D * D * 2};
+        uint32_t box[3] = {64, (uint32_t)D, 1};
+        if (!make_map(&mHt, r->ht, 3, dims, str, box, why, why_len)) return cudaErrorNotSupported;
+    }
+    Params prm;
+    prm.S = r->S; prm.H = r->H; prm.NQ = r->NQ; prm.NK = r->NK; prm.NG = r->NG; prm.W = r->W;
+    prm.G = r->cfg.G; prm.comp = r->cfg.comp;
+    const double s = 1.0 / sqrt((double)D);
+    prm.s = (float)s;
+    prm.scale_log2 = (float)(s * 1.4426950408889634);
+    prm.idx = r->idx; prm.count = r->count; prm.mask = r->mask;
+    prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
+    prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
+    // request >= 100 KB so at most two CTAs share an SM (2 x 256 TMEM columns)
+    size_t smem = (size_t)Geo<D>::BYTES + 1024;
+    if (smem < 100 * 1024) smem = 100 * 1024;
+    auto kern = attn_sm100_kernel<D>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)r->NQ, (unsigned)r->BH);
+    kern<<<grid, kThreads, smem, st>>>(mQ, mK, mV, mKb, mVs, mHt, prm);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                              pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                              int* launches, char* why, size_t why_len) {
+    if (r->cfg.Bq != kBQ || r->cfg.Bk != kBK) {
+        snprintf(why, why_len, "needs Bq=128, Bk=64");
+        return cudaErrorNotSupported;
+    }
+    if (r->cfg.comp == PASA_COMP_GROUPED && r->cfg.G % 32 != 0 && r->cfg.G < r->NK) {
+        snprintf(why, why_len, "grouped compensation needs G %% 32 == 0 or G >= N_K (G=%d)",
+                 r->cfg.G);
+        return cudaErrorNotSupported;
+    }
+    if (r->W > 64) {
+        snprintf(why, why_len, "N_K > 2048");
+        return cudaErrorNotSupported;
+    }
+    cudaError_t e = r->D == 128 ? launch_d<128>(q, k, v, r, out, st, why, why_len)
+                                : launch_d<64>(q, k, v, r, out, st, why, why_len);
+    if (e == cudaSuccess) *launches += 1;
+    return e;
+}
+
+}  // namespace pasa

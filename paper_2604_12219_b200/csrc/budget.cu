@@ -1,0 +1,140 @@
+// budget.cu -- pasa_budget: the curvature (trajectory-acceleration) reduction
+// over the last three latents and the per-step density of Eqs. 9-11
+// (readings R-15..R-18 in DESIGN.md §3).
+//
+// HBM-bound: reads 3 * n * sizeof(elem) bytes once.  Fixed grid of
+// kBudgetParts CTAs, each reducing one contiguous chunk in fp64 with a fixed
+// shuffle tree, then a single-CTA finaliser that sums the partials in a fixed
+// tree: l1 is bit-identical run to run (not bit-identical to the sequential
+// oracle; tolerance 1e-12 relative).
+#include <cuda_bf16.h>
+
+#include "pasa_internal.h"
+
+namespace pasa {
+namespace {
+
+constexpr int kThreads = 256;
+
+template <typename T>
+__device__ __forceinline__ void load4(const T* p, int64_t e, double out[4]);
+
+template <>
+__device__ __forceinline__ void load4<float>(const float* p, int64_t e, double out[4]) {
+    float4 v = __ldg(reinterpret_cast<const float4*>(p + e));
+    out[0] = v.x; out[1] = v.y; out[2] = v.z; out[3] = v.w;
+}
+template <>
+__device__ __forceinline__ void load4<__nv_bfloat16>(const __nv_bfloat16* p, int64_t e,
+                                                     double out[4]) {
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(p + e));
+    __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&v.x);
+    __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&v.y);
+    out[0] = __bfloat162float(a.x); out[1] = __bfloat162float(a.y);
+    out[2] = __bfloat162float(b.x); out[3] = __bfloat162float(b.y);
+}
+template <typename T>
+__device__ __forceinline__ double load1(const T* p, int64_t e) {
+    if constexpr (sizeof(T) == 4) return (double)__ldg(p + e);
+    else return (double)__bfloat162float(p[e]);
+}
+
+// |dv| for one element, B1 of DESIGN.md §3: two subtractions and two divisions
+// in IEEE double, exactly the per-element arithmetic of the definition.
+__device__ __forceinline__ double accel(double xt, double x1, double x2, int kind, double ht,
+                                        double h1) {
+    if (kind == 1) return fabs(__dsub_rn(xt, x1));
+    double a = __dsub_rn(xt, x1);
+    double b = __dsub_rn(x1, x2);
+    return fabs(__dsub_rn(__ddiv_rn(a, ht), __ddiv_rn(b, h1)));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kThreads) budget_partial_kernel(
+    const T* __restrict__ xt, const T* __restrict__ x1, const T* __restrict__ x2, int64_t n,
+    int kind, double ht, double h1, double* __restrict__ partials) {
+    // chunk of a multiple of 4 elements per CTA (vector loads stay aligned)
+    int64_t chunk = ((n + kBudgetParts - 1) / kBudgetParts + 3) & ~int64_t(3);
+    int64_t e0 = (int64_t)blockIdx.x * chunk;
+    int64_t e1 = min(e0 + chunk, n);
+    double acc = 0.0;
+    if (e0 < e1) {
+        int64_t nv = (e1 - e0) & ~int64_t(3);
+        for (int64_t e = e0 + 4 * (int64_t)threadIdx.x; e < e0 + nv; e += 4 * kThreads) {
+            double a[4], b[4], c[4];
+            load4<T>(xt, e, a);
+            load4<T>(x1, e, b);
+            if (kind == 0) load4<T>(x2, e, c);
+            else { c[0] = c[1] = c[2] = c[3] = 0.0; }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) acc += accel(a[u], b[u], c[u], kind, ht, h1);
+        }
+        for (int64_t e = e0 + nv + threadIdx.x; e < e1; e += kThreads)
+            acc += accel(load1<T>(xt, e), load1<T>(x1, e), kind == 0 ? load1<T>(x2, e) : 0.0,
+                         kind, ht, h1);
+    }
+    // fixed-order reduction: warp shuffle tree, then warp 0 over the warp sums
+    __shared__ double warp_sum[kThreads / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < kThreads / 32 ? warp_sum[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) partials[blockIdx.x] = v;
+    }
+}
+
+// Eq. 10 alpha = l / l-bar; Eq. 11 rho_t = rho * alpha (or the table entry),
+// clipped at rho_max (R-18); dense prefix (R-15) -> rho_t = 1.
+__global__ void budget_finalize_kernel(const double* __restrict__ partials, int64_t n,
+                                       int32_t step, int32_t dense_steps, double rho,
+                                       double l1_mean, double rho_max, int use_table,
+                                       double table_val, BudgetRec* __restrict__ rec) {
+    __shared__ double s[kBudgetParts];
+    for (int i = threadIdx.x; i < kBudgetParts; i += blockDim.x) s[i] = partials[i];
+    __syncthreads();
+    for (int w = kBudgetParts / 2; w > 0; w >>= 1) {
+        for (int i = threadIdx.x; i < w; i += blockDim.x) s[i] = s[i] + s[i + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double l = n > 0 ? s[0] / (double)n : 0.0;
+        double alpha = l / l1_mean;
+        double rho_t, dense = 0.0, clipped = 0.0;
+        if (step < dense_steps || step < 2) {
+            rho_t = 1.0;
+            dense = 1.0;
+        } else {
+            double rp = use_table ? table_val : __dmul_rn(rho, alpha);
+            if (rp > rho_max) { rho_t = rho_max; clipped = 1.0; }
+            else rho_t = rp;
+        }
+        rec->l1 = l; rec->alpha = alpha; rec->rho_t = rho_t; rec->dense = dense;
+        rec->clipped = clipped;
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, int64_t n, int dtype,
+                          int kind, double h_t, double h_tm1, int32_t step, int32_t dense_steps,
+                          double rho, double l1_mean, double rho_max, int use_table,
+                          double table_val, pasa_budget_s* b, cudaStream_t st, int* launches) {
+    if (dtype == PASA_F32)
+        budget_partial_kernel<float><<<kBudgetParts, kThreads, 0, st>>>(
+            (const float*)xt, (const float*)xtm1, (const float*)xtm2, n, kind, h_t, h_tm1,
+            b->partials);
+    else
+        budget_partial_kernel<__nv_bfloat16><<<kBudgetParts, kThreads, 0, st>>>(
+            (const __nv_bfloat16*)xt, (const __nv_bfloat16*)xtm1, (const __nv_bfloat16*)xtm2, n,
+            kind, h_t, h_tm1, b->partials);
+    budget_finalize_kernel<<<1, 256, 0, st>>>(b->partials, n, step, dense_steps, rho, l1_mean,
+                                              rho_max, use_table, table_val, b->rec);
+    *launches += 2;
+    return cudaGetLastError();
+}
+
+}  // namespace pasa

@@ -1,0 +1,65 @@
+// pasa_internal.h -- host-side handle layout and kernel launchers of libpasa.so.
+// Product code: nothing here includes or calls anything under oracle/.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/pasa.h"
+
+namespace pasa {
+
+constexpr int kBudgetParts = 1024;   // fixed reduction grid: l1 is bit-reproducible
+constexpr int kNGMaxTC = 4096;       // no hard limit for the tcgen05 path (groups stream)
+
+struct BudgetRec {                    // device record, 64 bytes
+    double l1, alpha, rho_t, dense, clipped, pad0, pad1, pad2;
+};
+
+}  // namespace pasa
+
+struct pasa_budget_s {
+    pasa::BudgetRec* rec;            // device
+    double* partials;                // device [kBudgetParts]
+};
+
+struct pasa_route_s {
+    pasa_route_cfg cfg;
+    int64_t B, S, H, D, NQ, NK, NG, W, BH;
+    int32_t* hdr;                    // device: [0] = k of the last pasa_route
+    double* qbar;                    // [BH][NQ][D]
+    double* kbar;                    // [BH][NK][D]
+    double* scores;                  // [BH][NQ][NK] scratch (r, fp64)
+    void* kbar_lp;                   // [BH][NK][D]   bf16 or fp32 (4 B/elem capacity)
+    void* vsum_lp;                   // [BH][NK][D]
+    void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)
+    int32_t* idx;                    // [BH][NQ][NK]
+    int32_t* count;                  // [BH][NQ]
+    uint32_t* mask;                  // [BH][NQ][W]
+    int32_t route_dtype;             // dtype of the q/k the route was last built from (-1 = none)
+};
+
+namespace pasa {
+
+// ---- launchers (each returns cudaGetLastError() after its launches) -------
+cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, int64_t n, int dtype,
+                          int kind, double h_t, double h_tm1, int32_t step, int32_t dense_steps,
+                          double rho, double l1_mean, double rho_max, int use_table,
+                          double table_val, pasa_budget_s* b, cudaStream_t st, int* launches);
+
+cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_budget_s* b,
+                         uint64_t seed, int32_t step, pasa_route_s* r, cudaStream_t st,
+                         int* launches);
+
+cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
+                            cudaStream_t st, int* launches);
+
+cudaError_t launch_attn_simt(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                             pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                             int* launches);
+
+// returns cudaErrorNotSupported if the configuration is outside the kernel's domain
+cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                              pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                              int* launches, char* why, size_t why_len);
+
+}  // namespace pasa

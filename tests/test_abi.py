@@ -1,0 +1,131 @@
+"""CPU checks of the C ABI: libpasa.so builds, loads, exports every symbol
+include/pasa.h declares, and validates arguments on the host (no GPU calls)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+from paper_2604_12219_b200 import _C
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    from paper_2604_12219_b200 import build
+    build.build()
+    return _C.lib()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "pasa.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(pasa_[a-z0-9_]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_header_declarations_match_binding():
+    assert declared_functions() == sorted(_C.EXPORTS)
+
+
+def test_library_exports_every_declared_symbol(L):
+    for name in declared_functions():
+        assert hasattr(L, name), name
+    assert b"sm_100a" in L.pasa_version()
+
+
+def test_layer_seed_matches_splitmix_vectors(L):
+    assert L.pasa_layer_seed(0, 0) == 0xE220A8397B1DCDAF
+    assert L.pasa_layer_seed(42, 0) == 0xBDD732262FEB6E95
+
+
+def test_library_has_tcgen05_and_tma_sass():
+    """The tensor-core kernel is compiled to UTCHMMA/UTMALDG/LDTM (sm_100a), not HMMA."""
+    import shutil
+    import subprocess
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        pytest.skip("cuobjdump missing")
+    sass = subprocess.run([exe, "-sass", _C.LIB_PATH], capture_output=True, text=True).stdout
+    for mnem in ("UTCHMMA", "UTMALDG", "LDTM", "STTM", "UTCBAR"):
+        assert mnem in sass, mnem
+
+
+def cfg(**kw):
+    d = dict(Bq=128, Bk=64, G=32, comp=0, beta=0.1, H_total=4, head_offset=0)
+    d.update(kw)
+    return _C.PasaRouteCfg(**d)
+
+
+def test_route_workspace_validation(L):
+    c = cfg()
+    n = L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 75600, 4, 128)
+    assert n > 0
+    for bad, why in [(cfg(Bk=32), "Bk"), (cfg(Bq=96), "Bq"), (cfg(G=0), "G"),
+                     (cfg(beta=-1.0), "beta"), (cfg(head_offset=1), "H_total")]:
+        assert L.pasa_route_workspace_bytes(ctypes.byref(bad), 1, 4096, 4, 128) == 0, why
+        assert L.pasa_last_error()
+    assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 4096, 4, 96) == 0
+    assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 64 * 2049, 4, 128) == 0
+
+
+def test_init_rejects_small_workspace_without_touching_device(L):
+    c = cfg()
+    n = L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 4096, 4, 128)
+    h = ctypes.c_void_p()
+    fake = ctypes.c_void_p(0x10000)  # never dereferenced on the host
+    assert L.pasa_route_init(fake, n - 1, ctypes.byref(c), 1, 4096, 4, 128,
+                             ctypes.byref(h)) == _C.PASA_ENOSPACE
+    assert L.pasa_route_init(fake, n, ctypes.byref(c), 1, 4096, 4, 128, ctypes.byref(h)) == 0
+    dims = (ctypes.c_int64 * 7)()
+    assert L.pasa_route_dims(h, dims) == 0
+    assert list(dims) == [1, 4096, 4, 128, 32, 64, 2]
+    L.pasa_route_fini(h)
+    hb = ctypes.c_void_p()
+    assert L.pasa_budget_init(fake, 8, ctypes.byref(hb)) == _C.PASA_ENOSPACE
+    assert L.pasa_budget_init(fake, L.pasa_budget_workspace_bytes(), ctypes.byref(hb)) == 0
+    L.pasa_budget_fini(hb)
+
+
+def test_budget_host_validation(L):
+    hb = ctypes.c_void_p()
+    fake = ctypes.c_void_p(0x10000)
+    assert L.pasa_budget_init(fake, L.pasa_budget_workspace_bytes(), ctypes.byref(hb)) == 0
+    x = _C.PasaLatent(0x20000, 1, 0, 1024)
+    sc = _C.PasaSchedule(50, 25, 0.15, 0.2, 0.0, 1.0, 1.0, 1.0, None, 0, 0)
+    rc = L.pasa_budget(ctypes.byref(x), ctypes.byref(x), ctypes.byref(x), ctypes.byref(sc), hb, None)
+    assert rc == _C.PASA_EDEGENERATE
+    sc = _C.PasaSchedule(50, 50, 0.15, 0.2, 1.0, 1.0, 1.0, 1.0, None, 0, 0)
+    assert L.pasa_budget(ctypes.byref(x), ctypes.byref(x), ctypes.byref(x), ctypes.byref(sc), hb,
+                         None) == _C.PASA_EINVAL
+    sc = _C.PasaSchedule(50, 20, 0.15, 0.2, 1.0, 0.0, 1.0, 1.0, None, 0, 0)
+    assert L.pasa_budget(ctypes.byref(x), ctypes.byref(x), ctypes.byref(x), ctypes.byref(sc), hb,
+                         None) == _C.PASA_EINVAL
+    y = _C.PasaLatent(0x20000, 0, 0, 1024)  # bf16 vs fp32
+    sc = _C.PasaSchedule(50, 20, 0.15, 0.2, 1.0, 1.0, 1.0, 1.0, None, 0, 0)
+    assert L.pasa_budget(ctypes.byref(x), ctypes.byref(y), ctypes.byref(x), ctypes.byref(sc), hb,
+                         None) == _C.PASA_EDTYPE
+    L.pasa_budget_fini(hb)
+
+
+def test_route_attn_host_validation(L):
+    c = cfg(H_total=2)
+    h = ctypes.c_void_p()
+    fake = ctypes.c_void_p(0x10000)
+    n = L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 1000, 2, 64)
+    assert L.pasa_route_init(fake, n, ctypes.byref(c), 1, 1000, 2, 64, ctypes.byref(h)) == 0
+    hb = ctypes.c_void_p()
+    assert L.pasa_budget_init(fake, L.pasa_budget_workspace_bytes(), ctypes.byref(hb)) == 0
+    good = _C.PasaTensor(0x40000, 0, 0, 1, 1000, 2, 64, 1000 * 128, 128, 64)
+    wrong_s = _C.PasaTensor(0x40000, 0, 0, 1, 999, 2, 64, 1000 * 128, 128, 64)
+    wrong_dt = _C.PasaTensor(0x40000, 1, 0, 1, 1000, 2, 64, 1000 * 128, 128, 64)
+    misalign = _C.PasaTensor(0x40002, 0, 0, 1, 1000, 2, 64, 1000 * 128, 128, 64)
+    assert L.pasa_route(ctypes.byref(wrong_s), ctypes.byref(good), hb, 1, 3, h, None) == _C.PASA_ESHAPE
+    assert L.pasa_route(ctypes.byref(good), ctypes.byref(wrong_dt), hb, 1, 3, h, None) == _C.PASA_EDTYPE
+    assert L.pasa_route(ctypes.byref(misalign), ctypes.byref(good), hb, 1, 3, h, None) == _C.PASA_ESHAPE
+    # attention before any route was built
+    assert L.pasa_attn(ctypes.byref(good), ctypes.byref(good), ctypes.byref(good), h,
+                       ctypes.byref(good), None) == _C.PASA_EINVAL
+    L.pasa_route_fini(h)
+    L.pasa_budget_fini(hb)

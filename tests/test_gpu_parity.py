@@ -1,0 +1,303 @@
+"""GPU <-> oracle parity through the C ABI (libpasa.so).
+
+Comparison protocol:
+* budget: l1 relative error <= 1e-12, rho_t relative <= 1e-12, flags equal;
+* route: pooled means bitwise equal; k, count, idx, mask bit-exact, except
+  documented ties (|rt_a - rt_b| <= 1e-6 max(1,|rt_b|) on the oracle's scores);
+* attention: compared with oracle_attn_with_route(GPU route):
+  max|O_gpu - O_orc| <= 2e-2 max|O_orc| (bf16 I/O), <= 1e-5 max|O_orc| (fp32).
+Inputs are seeded synthetic tensors from ``synth``.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-5}
+
+
+@pytest.fixture(scope="module")
+def pasa():
+    from paper_2604_12219_b200 import build
+    build.build()
+    import paper_2604_12219_b200 as P
+    return P
+
+
+def make_budget(P, rho, step=25, T=50):
+    b = P.Budget()
+    x = torch.zeros(64, device="cuda")
+    b(x, x, x, T=T, step=step, rho_table=[rho] * T, l1_mean=1.0)
+    return b
+
+
+def check_route(P, q, k, cfg, rho, seed=42, step=25, heads=None):
+    """Build the GPU route and compare it with the oracle; returns (route, read)."""
+    B, S, H, D = q.shape
+    route = P.Route(B, S, H, D, cfg)
+    budget = make_budget(P, rho, step)
+    route(q, k, budget, seed, step)
+    got = route.read()
+    NK = route.NK
+    kk = oracle.density_to_k(rho, NK)
+    assert got["k"] == kk
+    assert (got["count"] == kk).all()
+    heads = range(B * H) if heads is None else heads
+    qbar, kbar = route.pooled()
+    ties = 0
+    for bh in heads:
+        b, h = divmod(bh, H)
+        qh = q[b:b + 1, :, h:h + 1]
+        kh = k[b:b + 1, :, h:h + 1]
+        # R1: pooled means are bitwise equal to the oracle's sequential sums
+        assert np.array_equal(qbar[bh], oracle.block_means(oracle.heads(qh)[0], cfg.Bq))
+        assert np.array_equal(kbar[bh], oracle.block_means(oracle.heads(kh)[0], cfg.Bk))
+        gh = b * (cfg.H_total or H) + cfg.head_offset + h   # global head (R-20)
+        want = oracle.route(qh, kh, Bq=cfg.Bq, Bk=cfg.Bk, beta=cfg.beta, seed=seed, step=step,
+                            H_total=gh + 1, head_offset=gh, kk=kk, want_scores=True)
+        gi = got["idx"][bh, :, :kk]
+        wi = want["idx"][0]
+        for i in np.nonzero((gi != wi).any(axis=1))[0]:
+            a = sorted(set(gi[i]) - set(wi[i]))
+            bb = sorted(set(wi[i]) - set(gi[i]))
+            sc = want["scores"][0, i]
+            for x, y in zip(a, bb):
+                assert abs(sc[x] - sc[y]) <= 1e-6 * max(1.0, abs(sc[y])), (bh, i, x, y)
+                ties += 1
+        if ties == 0:
+            assert np.array_equal(got["mask"][bh], want["mask"][0])
+    return route, got, ties
+
+
+def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None):
+    out = P.attn(q, k, v, route, force_simt=force_simt)
+    torch.cuda.synchronize()
+    B, S, H, D = q.shape
+    if pairs is None:
+        ref = oracle.attn_with_route(q, k, v, got["idx"], got["count"], Bq=cfg.Bq, Bk=cfg.Bk,
+                                     G=cfg.G, comp=cfg.comp)
+        o = oracle.f64(out)
+        err = np.abs(o - ref).max() / np.abs(ref).max()
+    else:
+        bhs = sorted({bh for bh, _ in pairs})
+        sub = {bh: n for n, bh in enumerate(bhs)}
+        sel = lambda t: torch.stack([t[bh // H, :, bh % H] for bh in bhs], 0)  # noqa: E731
+        qh, kh, vh = (oracle.f64(sel(t)) for t in (q, k, v))
+        idx = np.stack([got["idx"][bh] for bh in bhs])
+        cnt = np.stack([got["count"][bh] for bh in bhs])
+        lp = [(sub[bh], i) for bh, i in pairs]
+        ref = oracle.attn_pairs(None, None, None, idx, cnt, lp, Bq=cfg.Bq, Bk=cfg.Bk, G=cfg.G,
+                                comp=cfg.comp, qh=qh, kh=kh, vh=vh)
+        err, mx = 0.0, 0.0
+        for n, (bh, i) in enumerate(pairs):
+            rows = min(cfg.Bq, S - i * cfg.Bq)
+            o = oracle.f64(out[bh // H, i * cfg.Bq:i * cfg.Bq + rows, bh % H])
+            err = max(err, np.abs(o - ref[n, :rows]).max())
+            mx = max(mx, np.abs(ref[n, :rows]).max())
+        err /= mx
+    assert np.isfinite(oracle.f64(out)).all()
+    assert err <= TOL[q.dtype], err
+    return out, err
+
+
+# ----------------------------------------------------------------- budget --
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+def test_budget_parity_three_phase(pasa, dtype):
+    tp = synth.ThreePhase(shape=synth.CONFIGS["cogvideox5b"]["latent"], T=50, seed=7,
+                          device="cuda")
+    lbar = tp.expected_l1_mean()
+    b = pasa.Budget()
+    for t in (3, 11, 30, 48):
+        xs = [x.to(dtype).contiguous() for x in tp.latents(t)]
+        b(*xs, T=50, step=t, rho=0.15, dense_frac=0.2, l1_mean=lbar, h_t=1 / 50, h_tm1=1 / 50)
+        got = b.read()
+        want = oracle.budget(*xs, T=50, step=t, rho=0.15, dense_frac=0.2, l1_mean=lbar,
+                             h_t=1 / 50, h_tm1=1 / 50)
+        assert got["l1"] == pytest.approx(want["l1"], rel=1e-12)
+        assert got["alpha"] == pytest.approx(want["alpha"], rel=1e-12)
+        assert got["rho_t"] == pytest.approx(want["rho_t"], rel=1e-12)
+        assert got["dense"] == want["dense"] and got["clipped"] == want["clipped"]
+    # deterministic fixed-grid reduction: bitwise identical run to run
+    b(*xs, T=50, step=48, rho=0.15, l1_mean=lbar, h_t=1 / 50, h_tm1=1 / 50)
+    again = b.read()
+    assert again["l1"] == got["l1"]
+
+
+def test_budget_velocity_table_and_clip(pasa):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    v1 = torch.randn(100_003, device="cuda", generator=g)
+    v0 = torch.randn(100_003, device="cuda", generator=g)
+    b = pasa.Budget()
+    b(v1, v0, None, kind="velocity", T=50, step=20, rho=0.5, l1_mean=0.1)
+    got = b.read()
+    want = oracle.budget(v1, v0, kind=1, T=50, step=20, rho=0.5, l1_mean=0.1)
+    assert got["l1"] == pytest.approx(want["l1"], rel=1e-12)
+    assert got["clipped"] and want["clipped"] and got["rho_t"] == 1.0
+    tab = np.linspace(0.05, 0.4, 50)
+    b(v1, v0, None, kind="velocity", T=50, step=33, rho_table=tab, l1_mean=1.0)
+    assert b.read()["rho_t"] == tab[33]
+    b(v1, v0, None, kind="velocity", T=50, step=4, rho=0.15, l1_mean=1.0)
+    assert b.read()["dense"] and b.read()["rho_t"] == 1.0
+
+
+# ------------------------------------------------------------------ route --
+ROUTE_CASES = [
+    # name, B, S, H, D, Bq, beta, rho, gen
+    ("tiny", 1, 1024, 1, 64, 64, 0.1, 0.5, "video"),
+    ("ragged1000", 1, 1000, 2, 128, 128, 0.1, 0.15, "iid"),
+    ("ragged4100", 2, 4100, 2, 64, 128, 0.1, 0.15, "video"),
+    ("beta0", 1, 4100, 2, 128, 128, 0.0, 0.15, "iid"),
+    ("bigbeta", 1, 2048, 1, 128, 128, 5.0, 0.3, "iid"),
+]
+
+
+def gen_qkv(gen, B, S, H, D, dtype, seed=1000):
+    if gen == "iid":
+        return synth.iid_qkv(B, S, H, D, seed=seed, dtype=dtype, device="cuda")
+    F = max(1, S // (32 * 32))
+    grid = (F, 32, S // (32 * F)) if S % (32 * F) == 0 else (1, 1, S)
+    return synth.video_qkv(B, grid, H, D, seed=seed, dtype=dtype, device="cuda")
+
+
+@pytest.mark.parametrize("case", ROUTE_CASES, ids=[c[0] for c in ROUTE_CASES])
+def test_route_bit_exact(pasa, case):
+    name, B, S, H, D, Bq, beta, rho, gen = case
+    q, k, _ = gen_qkv(gen, B, S, H, D, torch.bfloat16)
+    cfg = pasa.RouteCfg(Bq=Bq, G=32, beta=beta)
+    _, got, ties = check_route(pasa, q, k, cfg, rho, seed=pasa.layer_seed(42, 3), step=17)
+    assert ties <= 2
+
+
+def test_route_fp32_and_head_partition(pasa):
+    """R-20: Philox keyed on the global head -> routing heads [2,4) at offset 2 of 4
+    equals rows 2..3 of the full route, bit for bit."""
+    q, k, _ = synth.iid_qkv(1, 3000, 4, 64, seed=5, dtype=torch.float32, device="cuda")
+    cfg = pasa.RouteCfg(Bq=128, beta=0.3)
+    _, full, _ = check_route(pasa, q, k, cfg, 0.2)
+    cfgp = pasa.RouteCfg(Bq=128, beta=0.3, H_total=4, head_offset=2)
+    qp, kp = q[:, :, 2:].contiguous(), k[:, :, 2:].contiguous()
+    _, part, _ = check_route(pasa, qp, kp, cfgp, 0.2)
+    assert np.array_equal(full["idx"][2:], part["idx"])
+    assert np.array_equal(full["mask"][2:], part["mask"])
+
+
+# -------------------------------------------------------------- attention --
+ATTN_CASES = [
+    # name, B, S, H, D, Bq, G, comp, rho, dtype, gen
+    ("tiny_simt", 1, 1024, 1, 64, 64, 32, "grouped", 0.5, torch.bfloat16, "video"),
+    ("tiny_g4_simt", 1, 1024, 1, 64, 64, 4, "grouped", 0.5, torch.bfloat16, "video"),
+    ("tiny_fp32", 1, 1024, 1, 64, 64, 32, "grouped", 0.5, torch.float32, "video"),
+    ("tc_d128_1000", 1, 1000, 2, 128, 128, 32, "grouped", 0.15, torch.bfloat16, "iid"),
+    ("tc_d128_4100_g32", 1, 4100, 2, 128, 128, 32, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d64_4100_g32", 2, 4100, 2, 64, 128, 32, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d128_4100_g64", 1, 4100, 2, 128, 128, 64, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d128_4100_global", 1, 4100, 2, 128, 128, 4096, "grouped", 0.15, torch.bfloat16, "iid"),
+    ("tc_d128_4100_zeroth", 1, 4100, 2, 128, 128, 32, "zeroth", 0.15, torch.bfloat16, "video"),
+    ("tc_d64_4100_none", 1, 4100, 2, 64, 128, 32, "none", 0.15, torch.bfloat16, "iid"),
+    ("fp32_d128_4100", 1, 4100, 1, 128, 128, 32, "grouped", 0.15, torch.float32, "video"),
+    ("tc_d128_g8_simt", 1, 4100, 1, 128, 128, 8, "grouped", 0.15, torch.bfloat16, "video"),
+]
+
+
+@pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
+def test_attn_parity(pasa, case):
+    name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
+    q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=11)
+    cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, rho)
+    out, err = check_attn(pasa, q, k, v, route, got, cfg)
+    # determinism: no atomics on the output path -> bitwise reproducible
+    out2 = pasa.attn(q, k, v, route)
+    assert torch.equal(out, out2)
+
+
+def test_tensor_core_matches_simt_kernel(pasa):
+    q, k, v = gen_qkv("video", 1, 4100, 2, 128, torch.bfloat16, seed=21)
+    cfg = pasa.RouteCfg(Bq=128, G=32)
+    route, got, _ = check_route(pasa, q, k, cfg, 0.15)
+    a = pasa.attn(q, k, v, route).float()
+    b = pasa.attn(q, k, v, route, force_simt=True).float()
+    assert (a - b).abs().max().item() <= 2e-2 * b.abs().max().item()
+
+
+@pytest.mark.parametrize("D", [64, 128])
+def test_dense_step_equals_library_sdpa(pasa, D):
+    """rho_t = 1 (dense prefix): k = N_K, U empty -> Eq. 1; checked against torch SDPA."""
+    q, k, v = synth.iid_qkv(1, 2000, 2, D, seed=4, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=128)
+    route = pasa.Route(1, 2000, 2, D, cfg)
+    b = pasa.Budget()
+    x = torch.zeros(64, device="cuda")
+    b(x, x, x, T=50, step=3, l1_mean=1.0)          # step 3 < 10: dense prefix
+    assert b.read()["dense"]
+    route(q, k, b, 1, 3)
+    assert route.read()["k"] == route.NK
+    out = pasa.attn(q, k, v, route).float()
+    ref = torch.nn.functional.scaled_dot_product_attention(
+        *(t.float().permute(0, 2, 1, 3) for t in (q, k, v))).permute(0, 2, 1, 3)
+    assert (out - ref).abs().max().item() <= 2e-2 * ref.abs().max().item()
+
+
+def test_head_partition_outputs_bitwise(pasa):
+    """Head-parallel sharding: P = 1 and the rank holding heads
+    [2, 4) produce bitwise identical outputs for those heads."""
+    q, k, v = synth.iid_qkv(1, 3000, 4, 128, seed=8, dtype=torch.bfloat16, device="cuda")
+    full_r = pasa.Route(1, 3000, 4, 128, pasa.RouteCfg(Bq=128, beta=0.2))
+    b = make_budget(pasa, 0.2)
+    full_r(q, k, b, 9, 25)
+    full = pasa.attn(q, k, v, full_r)
+    part_r = pasa.Route(1, 3000, 2, 128, pasa.RouteCfg(Bq=128, beta=0.2, H_total=4,
+                                                         head_offset=2))
+    qs, ks, vs = (t[:, :, 2:].contiguous() for t in (q, k, v))
+    part_r(qs, ks, b, 9, 25)
+    part = pasa.attn(qs, ks, vs, part_r)
+    assert torch.equal(full[:, :, 2:], part)
+
+
+def test_strided_output_and_inputs(pasa):
+    """q/k/v as head-slices of a packed qkv projection, out written into a strided view."""
+    qkv = torch.randn(1, 1500, 3, 2, 128, device="cuda").to(torch.bfloat16)
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]
+    cfg = pasa.RouteCfg(Bq=128)
+    route, got, _ = check_route(pasa, q, k, cfg, 0.25)
+    big = torch.zeros(1, 1500, 4, 128, device="cuda", dtype=torch.bfloat16)
+    out = pasa.attn(q, k, v, route, out=big[:, :, 1:3])
+    ref = oracle.attn_with_route(q, k, v, got["idx"], got["count"], Bq=128, Bk=64, G=32)
+    err = np.abs(oracle.f64(out) - ref).max() / np.abs(ref).max()
+    assert err <= 2e-2
+    assert big[:, :, 0].abs().max().item() == 0 and big[:, :, 3].abs().max().item() == 0
+
+
+# ----------------------------------------------- full BASELINE configs --
+def _pairs(H, NQ, heads, nq):
+    qs = sorted({0, NQ - 1, *np.linspace(0, NQ - 1, nq).astype(int).tolist()})
+    return [(h, int(i)) for h in heads for i in qs]
+
+
+@pytest.mark.parametrize("name,gen,heads,nq", [
+    ("wan13b_480p", "video", [0, 5, 11], 12),
+    ("wan14b_720p", "iid", [0, 39], 6),
+])
+def test_full_config_sampled(pasa, name, gen, heads, nq):
+    """BASELINE.json configs at full size, in the launch configuration bench.py
+    times: route bit-exact on sampled heads, attention on sampled (head, q-block)
+    pairs always including q-block 0 and the ragged last one."""
+    c = synth.CONFIGS[name]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    if gen == "video":
+        q, k, v = synth.video_qkv(B, c["grid"], H, D, seed=1003, dtype=torch.bfloat16,
+                                  device="cuda")
+    else:
+        q, k, v = synth.iid_qkv(B, S, H, D, seed=1003, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=c["Bq"], G=c["G"], beta=0.1)
+    route, got, ties = check_route(pasa, q, k, cfg, c["rho"], seed=pasa.layer_seed(42, 0),
+                                   step=25, heads=heads)
+    assert ties <= 4
+    NQ = route.NQ
+    check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, NQ, heads, nq))
