@@ -1,0 +1,421 @@
+#!/usr/bin/env python
+"""bench.py -- one PASA denoising-step layer (budget -> route -> attn) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl pasa|reference]
+                    [--config wan14b_720p]
+
+A step is one pass of the whole hot path over the BASELINE.json workload
+(default: Wan 2.1-14B 720p, 75,600 tokens, 40 heads, d = 128, rho = 0.15):
+pasa_budget on the three-phase latents, pasa_route and pasa_attn for all heads of
+one layer.  Under torchrun (N > 1) the heads are partitioned across ranks (rank
+r owns heads [r H/N, (r+1) H/N), Philox keyed on the global head); there is no
+collective on the data path.  Rank 0 prints one JSON line.
+
+Metric: TFLOP/s-equiv = 4 S^2 d (B H) / t_step (counts the skipped dense work).
+Inputs are synthetic, seeded, resident in HBM before the timed region, and
+larger than L2 (q, k, v = 2.3 GB >> 126 MB), so no flush is needed.
+``--impl reference`` times the fp64 CPU oracle (the reference arm of this
+tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PASA attn TFLOP/s-equiv & ms/layer at Wan2.1-14B 720p, 1/2/4/8 B200, % of peak"
+UNIT = "TFLOP/s-equiv"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="pasa", choices=["pasa", "reference"])
+    ap.add_argument("--config", default="wan14b_720p")
+    ap.add_argument("--step-t", type=int, default=25, help="denoising step index t")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-qblocks", type=int, default=48, help="oracle sample size")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def algorithmic_flops_per_head(S, D, NK, NG, k, Bk=64):
+    """4 S k Bk d (exact) + 4 S N_K d (centroid logits + zeroth
+    order, as implemented over all N_K) + 2 S d^2 N_G (grouped first order)."""
+    return 4.0 * S * k * Bk * D + 4.0 * S * NK * D + 2.0 * S * D * D * NG
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, val in zip(names, parts[4:8]):
+                if val.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# --------------------------------------------------------------- oracle --
+def oracle_sample(cfg, nqb, seed=1000):
+    """Time the fp64 oracle (as it stands) on a bounded sample of the workload:
+    budget on the full latents, then for one head: block statistics + route +
+    attention for `nqb` query blocks spread over the head.  Returns
+    (TFLOP/s-equiv extrapolated to a full head, seconds, sample description)."""
+    import numpy as np
+    import torch
+
+    import oracle
+    import synth
+
+    S, D, H = cfg["S"], cfg["D"], cfg["H"]
+    Bq, Bk, G, rho = cfg["Bq"], cfg["Bk"], cfg["G"], cfg["rho"]
+    oracle.build()
+    g = torch.Generator().manual_seed(seed)
+    q = torch.randn((1, S, 1, D), generator=g).to(torch.bfloat16)
+    k = torch.randn((1, S, 1, D), generator=g).to(torch.bfloat16)
+    v = torch.randn((1, S, 1, D), generator=g).to(torch.bfloat16)
+    tp = synth.ThreePhase(shape=(int(np.prod(cfg["latent"])),), T=50, seed=7)
+    xs = tp.latents(25)
+    qh, kh, vh = oracle.heads(q), oracle.heads(k), oracle.heads(v)
+    NQ = (S + Bq - 1) // Bq
+    NK = (S + Bk - 1) // Bk
+    t0 = time.perf_counter()
+    rec = oracle.budget(*xs, T=50, step=25, rho=rho, l1_mean=tp.expected_l1_mean(),
+                        h_t=1 / 50, h_tm1=1 / 50)
+    t_budget = time.perf_counter() - t0
+    kk = oracle.density_to_k(rho, NK)
+    t0 = time.perf_counter()
+    r = oracle.route(q, k, Bq=Bq, Bk=Bk, beta=0.1, seed=42, step=25, kk=kk)
+    t_route = time.perf_counter() - t0
+    cnt = np.full((1, NQ), kk, np.int32)
+    blocks = sorted(set(np.linspace(0, NQ - 1, nqb).astype(int).tolist()))
+    t0 = time.perf_counter()
+    oracle.attn_pairs(None, None, None, r["idx"], cnt, [(0, i) for i in blocks], Bq=Bq, Bk=Bk,
+                      G=G, qh=qh, kh=kh, vh=vh)
+    t_attn = time.perf_counter() - t0
+    # attn_pairs recomputes the head's statistics once; the rest scales with q-blocks
+    t_head = t_budget / H + t_route + t_attn * NQ / len(blocks)
+    value = 4.0 * S * S * D / t_head / 1e12
+    desc = (f"1 of {H} heads: budget on full latents (/H), route for the head, stats + "
+            f"attention for {len(blocks)} of {NQ} q-blocks, extrapolated to the full head "
+            f"({t_budget + t_route + t_attn:.1f} s measured)")
+    return value, t_budget + t_route + t_attn, desc, rec["rho_t"]
+
+
+def run_reference(args):
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = synth.CONFIGS[args.config]
+    vals = []
+    total_s = 0.0
+    for it in range(args.warmup + args.steps):
+        nqb = max(2, args.cpu_qblocks // 4)
+        v, secs, desc, _ = oracle_sample(cfg, nqb, seed=1000 + it)
+        if it >= args.warmup:
+            vals.append(v)
+            total_s += secs
+    value = sum(vals) / len(vals)
+    cores = oracle.num_threads()
+    S, D, H = cfg["S"], cfg["D"], cfg["H"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 4.0 * S * S * D * H / (value * 1e12) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.config, "S": S, "H": H, "D": D},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU --
+def run_pasa(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2604_12219_b200 import build as pbuild
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    if rank == 0:
+        pbuild.build()
+    if world > 1:
+        dist.barrier()
+    import paper_2604_12219_b200 as P
+
+    cfg = synth.CONFIGS[args.config]
+    B, S, H, D = cfg["B"], cfg["S"], cfg["H"], cfg["D"]
+    if H % world:
+        raise SystemExit(f"{H} heads do not split over {world} ranks")
+    Hl = H // world
+    off = rank * Hl
+    dev = torch.device("cuda", torch.cuda.current_device())
+    # rank-local heads drawn from a per-global-head seed: same data for any N
+    qs, ks, vs = [], [], []
+    for h in range(off, off + Hl):
+        q1, k1, v1 = synth.iid_qkv(B, S, 1, D, seed=1000 + 7919 * h, dtype=torch.bfloat16,
+                                   device=dev)
+        qs.append(q1); ks.append(k1); vs.append(v1)
+    q = torch.cat(qs, 2).contiguous(); k = torch.cat(ks, 2).contiguous()
+    v = torch.cat(vs, 2).contiguous()
+    del qs, ks, vs
+    out = torch.empty_like(q)
+    tp = synth.ThreePhase(shape=cfg["latent"], T=50, seed=7, device=dev)
+    t_step = args.step_t
+    x_t, x_tm1, x_tm2 = (x.contiguous() for x in tp.latents(t_step))
+    lbar = tp.expected_l1_mean()
+    rcfg = P.RouteCfg(Bq=cfg["Bq"], Bk=cfg["Bk"], G=cfg["G"], comp="grouped", beta=0.1,
+                      H_total=H, head_offset=off)
+    budget = P.Budget(dev)
+    route = P.Route(B, S, Hl, D, rcfg, dev)
+    seed = P.layer_seed(42, 0)
+    stream = torch.cuda.current_stream()
+    launches = [0]
+
+    def step(ev=None):
+        budget(x_t, x_tm1, x_tm2, T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
+               h_t=1 / 50, h_tm1=1 / 50)
+        launches[0] += P.last_launch_count()
+        if ev is not None:
+            ev[0].record(stream)
+        route(q, k, budget, seed, t_step)
+        launches[0] += P.last_launch_count()
+        if ev is not None:
+            ev[1].record(stream)
+        P.attn(q, k, v, route, out, stats_only=True)
+        launches[0] += P.last_launch_count()
+        if ev is not None:
+            ev[2].record(stream)
+        P.attn(q, k, v, route, out, reuse_stats=True)
+        launches[0] += P.last_launch_count()
+        if ev is not None:
+            ev[3].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    rec = budget.read()
+    # k from the device record (same arithmetic as the route kernel, R-14)
+    kk = int(max(1, min(route.NK, math.floor(rec["rho_t"] * route.NK + 0.5))))
+
+    K = args.steps
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    launches[0] = 0
+    with ClockSampler(dev.index) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_start.record(stream)
+        for it in range(K):
+            step(evs[it])
+        e_end.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    gpu_launches = launches[0]
+    ms_total = e_start.elapsed_time(e_end)
+    t_local = ms_total / K
+    # per-kernel durations over the timed region (launch-stream events)
+    ph = np.zeros(4)
+    for it in range(K):
+        prev = e_start if it == 0 else evs[it - 1][3]
+        ph[0] += prev.elapsed_time(evs[it][0])
+        for j in range(1, 4):
+            ph[j] += evs[it][j - 1].elapsed_time(evs[it][j])
+    ph /= K
+    t_max = t_local
+    if world > 1:
+        tt = torch.tensor([t_local] + ph.tolist(), device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt[0])
+        ph = tt[1:].cpu().numpy()
+
+    # ---------------- e2e through the public API with host buffers --------------
+    e2e = None
+    if not args.no_e2e:
+        hq = q.cpu().pin_memory(); hk = k.cpu().pin_memory(); hv = v.cpu().pin_memory()
+        hx = [x.cpu().pin_memory() for x in (x_t, x_tm1, x_tm2)]
+        hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
+        h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
+        d2h = hout.numel() * hout.element_size()
+
+        def e2e_step():
+            for d, hsrc in zip((dq, dk, dv, *dx), (hq, hk, hv, *hx)):
+                d.copy_(hsrc, non_blocking=True)
+            budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
+                   h_t=1 / 50, h_tm1=1 / 50)
+            route(dq, dk, budget, seed, t_step)
+            P.attn(dq, dk, dv, route, out)
+            hout.copy_(out, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        n_e2e = max(2, min(K, 5))
+        a, bq = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if world > 1:
+            dist.barrier()
+        a.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        bq.record(stream)
+        torch.cuda.synchronize()
+        te = a.elapsed_time(bq) / n_e2e
+        if world > 1:
+            tt = torch.tensor([te], device=dev, dtype=torch.float64)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            te = float(tt[0])
+        e2e = {"value": 4.0 * S * S * D * B * H / (te * 1e-3) / 1e12, "unit": UNIT,
+               "ms_per_step": te, "h2d_bytes_per_step": int(h2d * world),
+               "d2h_bytes_per_step": int(d2h * world), "steps": n_e2e}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    pk, which = peaks()
+    NK, NG = route.NK, route.NG
+    flops_head = algorithmic_flops_per_head(S, D, NK, NG, kk)
+    attn_flops = flops_head * B * Hl           # per launch, this rank
+    t_attn = float(ph[3])
+    achieved = attn_flops / (t_attn * 1e-3) / 1e12
+    peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
+            tr = json.load(f)
+            if tr.get("config") == args.config and tr.get("heads") == Hl:
+                traffic = tr.get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    value = 4.0 * S * S * D * B * H / (t_max * 1e-3) / 1e12
+    cpu = None
+    if not args.no_cpu:
+        cv, secs, desc, _ = oracle_sample(cfg, args.cpu_qblocks)
+        import oracle
+        cpu = {"value": cv, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+               "sample": desc}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {
+            "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
+            "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
+            "step_t": t_step, "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
+            "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
+            "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
+            "parallelism": f"head-partition x{world}",
+        },
+        "ms_layer": {"budget": float(ph[0]), "route": float(ph[1]), "kv_stats": float(ph[2]),
+                     "attn": float(ph[3])},
+        "tflops_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12,
+        "pct_of_peak_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12 / peak,
+        "roofline": {"kernel": "attn_sm100_kernel", "bound": "tensor", "achieved": achieved,
+                     "peak": peak, "peak_kind": f"bf16 dense, sustained ({which})",
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "flops_per_launch": attn_flops},
+        "clocks": clk.summary(),
+        "gpu_launches": gpu_launches,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_pasa(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

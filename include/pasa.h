@@ -167,9 +167,16 @@ pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h
 pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                       pasa_route_h route, pasa_tensor* out, void* stream);
 
-/* pasa_attn with flags: PASA_ATTN_FORCE_SIMT runs the CUDA-core kernel even
- * for bf16 I/O (cross-check of the tensor-core kernel). */
+/* pasa_attn with flags:
+ *   PASA_ATTN_FORCE_SIMT   run the CUDA-core kernel even for bf16 I/O (cross-check);
+ *   PASA_ATTN_STATS_ONLY   launch only the K/V statistics pass (Kbar, Vsum, Hbar^(g));
+ *   PASA_ATTN_REUSE_STATS  skip the statistics pass: the caller guarantees that the
+ *                          previous STATS_ONLY call on this route saw the same k, v.
+ * STATS_ONLY followed by REUSE_STATS is exactly pasa_attn, split so that each
+ * kernel can be timed on its own stream position. */
 #define PASA_ATTN_FORCE_SIMT 1u
+#define PASA_ATTN_STATS_ONLY 2u
+#define PASA_ATTN_REUSE_STATS 4u
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 

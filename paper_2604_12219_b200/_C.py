@@ -20,6 +20,8 @@ PASA_BF16, PASA_F32 = 0, 1
 PASA_IN_LATENT, PASA_IN_VELOCITY = 0, 1
 COMP = {"grouped": 0, "zeroth": 1, "none": 2}
 PASA_ATTN_FORCE_SIMT = 1
+PASA_ATTN_STATS_ONLY = 2
+PASA_ATTN_REUSE_STATS = 4
 
 # every symbol include/pasa.h declares (tests check the library exports them all)
 EXPORTS = [

@@ -171,6 +171,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->count = reinterpret_cast<int32_t*>(w + L.off_count);
     r->mask = reinterpret_cast<uint32_t*>(w + L.off_mask);
     r->route_dtype = -1;
+    r->stats_dtype = -1;
     *out = r;
     return PASA_OK;
 }
@@ -228,7 +229,10 @@ pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h
     cudaError_t e = pasa::launch_route(*q, *k, budget, seed, step, route, (cudaStream_t)stream,
                                        &launches);
     g_launches = launches;
-    if (e == cudaSuccess) route->route_dtype = q->dtype;
+    if (e == cudaSuccess) {
+        route->route_dtype = q->dtype;
+        route->stats_dtype = -1;   // Kbar changed: the next pasa_attn must recompute the stats
+    }
     return cuda_status(e, "pasa_route launch");
 }
 
@@ -250,8 +254,15 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route)");
     int launches = 0;
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = pasa::launch_kv_stats(*k, *v, route, s, &launches);
-    if (e != cudaSuccess) { g_launches = launches; return cuda_status(e, "kv_stats launch"); }
+    if (!(flags & PASA_ATTN_REUSE_STATS)) {
+        cudaError_t e0 = pasa::launch_kv_stats(*k, *v, route, s, &launches);
+        if (e0 != cudaSuccess) { g_launches = launches; return cuda_status(e0, "kv_stats launch"); }
+        route->stats_dtype = q->dtype;
+    } else if (route->stats_dtype != q->dtype) {
+        return fail(PASA_EINVAL, "PASA_ATTN_REUSE_STATS without a matching STATS_ONLY call");
+    }
+    if (flags & PASA_ATTN_STATS_ONLY) { g_launches = launches; return PASA_OK; }
+    cudaError_t e = cudaSuccess;
     // The tensor-core kernel covers bf16 I/O with Bq = 128 and G % 32 == 0 (or one
     // global group); fp32 I/O, Bq = 64 and finer groups run the CUDA-core kernel
     // (documented in include/pasa.h and DESIGN.md §7).

@@ -36,6 +36,7 @@ struct pasa_route_s {
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]
     int32_t route_dtype;             // dtype of the q/k the route was last built from (-1 = none)
+    int32_t stats_dtype;             // dtype of the last kv_stats pass (-1 = none)
 };
 
 namespace pasa {

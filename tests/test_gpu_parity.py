@@ -183,7 +183,9 @@ def test_route_fp32_and_head_partition(pasa):
     cfgp = pasa.RouteCfg(Bq=128, beta=0.3, H_total=4, head_offset=2)
     qp, kp = q[:, :, 2:].contiguous(), k[:, :, 2:].contiguous()
     _, part, _ = check_route(pasa, qp, kp, cfgp, 0.2)
-    assert np.array_equal(full["idx"][2:], part["idx"])
+    kk = full["k"]
+    assert part["k"] == kk
+    assert np.array_equal(full["idx"][2:, :, :kk], part["idx"][:, :, :kk])
     assert np.array_equal(full["mask"][2:], part["mask"])
 
 
