@@ -38,11 +38,14 @@ UNIT = "TFLOP/s-equiv"
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="pasa", choices=["pasa", "reference"])
     ap.add_argument("--config", default="wan14b_720p")
     ap.add_argument("--step-t", type=int, default=25, help="denoising step index t")
+    ap.add_argument("--budget", default="table", choices=["table", "online"],
+                    help="table: rho_t = rho (the 85%%-sparsity config, k = 177 at Wan-14B); "
+                         "online: rho_t from the three-phase trajectory at step t")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-qblocks", type=int, default=48, help="oracle sample size")
@@ -79,7 +82,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -252,9 +255,11 @@ def run_pasa(args):
     stream = torch.cuda.current_stream()
     launches = [0]
 
+    table = [cfg["rho"]] * 50 if args.budget == "table" else None
+
     def step(ev=None):
         budget(x_t, x_tm1, x_tm2, T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
-               h_t=1 / 50, h_tm1=1 / 50)
+               h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
         launches[0] += P.last_launch_count()
         if ev is not None:
             ev[0].record(stream)
@@ -327,7 +332,7 @@ def run_pasa(args):
             for d, hsrc in zip((dq, dk, dv, *dx), (hq, hk, hv, *hx)):
                 d.copy_(hsrc, non_blocking=True)
             budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
-                   h_t=1 / 50, h_tm1=1 / 50)
+                   h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
             route(dq, dk, budget, seed, t_step)
             P.attn(dq, dk, dv, route, out)
             hout.copy_(out, non_blocking=True)
@@ -386,7 +391,8 @@ def run_pasa(args):
         "config": {
             "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
             "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
-            "step_t": t_step, "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
+            "step_t": t_step, "budget": args.budget, "l1": rec["l1"], "alpha": rec["alpha"],
+            "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
             "parallelism": f"head-partition x{world}",

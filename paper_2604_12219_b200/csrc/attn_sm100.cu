@@ -132,21 +132,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         // tail of the op list: centroid chunks with a dropped block, then the
         // first-order op of every group that ends inside the chunk (G % 32 == 0
         // or one global group: every 32-block half-chunk lies in one group)
+        // word-level: word w of the mask covers blocks [32w, 32w+32), inside one group
         int n = cnt;
         if (p.comp != PASA_COMP_NONE && cnt < NK) {
-            auto dropped = [&](int64_t j) { return ((ctl.mask[j >> 5] >> (j & 31)) & 1u) == 0u; };
+            const int W = (int)p.W;
+            auto dropped_word = [&](int w) {
+                const int64_t rem = NK - 32 * (int64_t)w;
+                const uint32_t inb = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+                return (~ctl.mask[w] & inb) != 0u;
+            };
+            const int64_t G = p.G;
+            int64_t g = 0;                              // next group to close
             for (int c = 0; c < nchunks; ++c) {
-                const int64_t j0 = 64 * (int64_t)c, j1 = min(j0 + 64, NK);
-                bool any = false;
-                for (int64_t j = j0; j < j1 && !any; ++j) any = dropped(j);
-                if (any) ctl.ops[n++] = op_make(OP_C, c);
+                if (dropped_word(2 * c) || (2 * c + 1 < W && dropped_word(2 * c + 1)))
+                    ctl.ops[n++] = op_make(OP_C, c);
                 if (p.comp == PASA_COMP_GROUPED) {
-                    for (int64_t g = j0 / p.G; g <= (j1 - 1) / p.G; ++g) {
-                        const int64_t ge = min((g + 1) * (int64_t)p.G, NK) - 1;  // last block
-                        if (ge < j0 || ge >= j1) continue;
-                        bool anyg = false;
-                        for (int64_t j = g * p.G; j <= ge && !anyg; ++j) anyg = dropped(j);
-                        if (anyg) ctl.ops[n++] = op_make(OP_F, (int32_t)g);
+                    const int64_t chunk_end = min(64 * (int64_t)(c + 1), NK);
+                    for (; g * G < NK && min((g + 1) * G, NK) <= chunk_end; ++g) {
+                        const int w0 = (int)((g * G) >> 5);
+                        const int w1 = (int)((min((g + 1) * G, NK) + 31) >> 5);
+                        bool any = false;
+                        for (int w = w0; w < w1 && !any; ++w) any = dropped_word(w);
+                        if (any) ctl.ops[n++] = op_make(OP_F, (int32_t)g);
                     }
                 }
             }
@@ -169,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                             (int)(i * kBQ), (int)h, (int)b);
             for (int n = 0; n < nops; ++n) {
                 const int s = n & 1;
-                mbar_wait(&ctl.k_empty[s], ((n >> 1) & 1) ^ 1);
+                mbar_wait_sleep(&ctl.k_empty[s], ((n >> 1) & 1) ^ 1);
                 uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
@@ -196,7 +203,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) {
             for (int n = 0; n < nops; ++n) {
                 const int s = n & 1;
-                mbar_wait(&ctl.v_empty[s], ((n >> 1) & 1) ^ 1);
+                mbar_wait_sleep(&ctl.v_empty[s], ((n >> 1) & 1) ^ 1);
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
@@ -232,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t v_base = smem_u32(smem + G_::OFF_V);
         auto issue_qk = [&](int n) {
             const int s = n & 1;
-            mbar_wait(&ctl.k_full[s], (n >> 1) & 1);
+            mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t d = tbase + kColS + 64 * s;
@@ -249,15 +256,15 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             __syncwarp();
         };
-        mbar_wait(&ctl.q_full, 0);
+        mbar_wait_sleep(&ctl.q_full, 0);
         tc_fence_after();
         if (nops > 0) issue_qk(0);
         for (int n = 0; n < nops; ++n) {
             const int s = n & 1;
             if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
-            mbar_wait(&ctl.p_full[s], (n >> 1) & 1);
+            mbar_wait_sleep(&ctl.p_full[s], (n >> 1) & 1);
             tc_fence_after();
-            mbar_wait(&ctl.v_full[s], (n >> 1) & 1);
+            mbar_wait_sleep(&ctl.v_full[s], (n >> 1) & 1);
             tc_fence_after();
             const int32_t op = ctl.ops[n];
             if (op_type(op) != OP_F) {
@@ -273,7 +280,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     mma_commit(&ctl.pv_done);
                 }
             } else {
-                mbar_wait(&ctl.k_full[s], (n >> 1) & 1);
+                mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
                 tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
@@ -300,13 +307,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         float A_cur = 0.f, A_done = 0.f;
         int64_t g_cur = -1, g_done = -1;
         int pv_seen = -1;          // pv_done phases consumed (ops whose MMA completed)
-        int sc[2] = {0, 0};        // S-type ops seen per buffer (s_full parity)
+        int sc0 = 0, sc1 = 0;      // S-type ops seen per buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
+        const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
         auto consume_pv = [&](int upto) {
             while (pv_seen < upto) {
                 ++pv_seen;
-                mbar_wait(&ctl.pv_done, pv_seen & 1);
+                mbar_wait_sleep(&ctl.pv_done, pv_seen & 1);
             }
         };
         for (int n = 0; n < nops; ++n) {
@@ -315,8 +323,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int type = op_type(op), v = op_val(op);
             const uint32_t t_buf = tbase + lane_off + kColS + 64 * s;
             if (type != OP_F) {
-                mbar_wait(&ctl.s_full[s], sc[s] & 1);
-                sc[s]++;
+                const int par = (s ? sc1 : sc0) & 1;
+                if (s) ++sc1; else ++sc0;
+                mbar_wait_sleep(&ctl.s_full[s], par);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
                 tmem_ld32(t_buf, sa);
@@ -337,18 +346,21 @@ __global__ void __launch_bounds__(kThreads, 2)
                     valid = ~kept & inb;
                     if (rem <= 64) { clast = (int)(rem - 1); wlast = (float)nlast_len; }
                 }
-                float mx = -INFINITY;
+                if (valid != ~0ull) {   // masked columns -> -inf (ragged block, kept blocks)
 #pragma unroll
-                for (int c = 0; c < 32; ++c) {
-                    const float x0 = ((valid >> c) & 1ull) ? __uint_as_float(sa[c]) * p.scale_log2
-                                                           : -INFINITY;
-                    const float x1 = ((valid >> (c + 32)) & 1ull)
-                                         ? __uint_as_float(sb[c]) * p.scale_log2 : -INFINITY;
-                    sa[c] = __float_as_uint(x0);
-                    sb[c] = __float_as_uint(x1);
-                    mx = fmaxf(mx, fmaxf(x0, x1));
+                    for (int c = 0; c < 32; ++c) {
+                        if (!((valid >> c) & 1ull)) sa[c] = 0xff800000u;
+                        if (!((valid >> (c + 32)) & 1ull)) sb[c] = 0xff800000u;
+                    }
                 }
-                // logit of the ragged last block (C ops), before sa/sb are overwritten
+                float mr0 = -INFINITY, mr1 = -INFINITY;   // raw row max (scale > 0 commutes)
+#pragma unroll
+                for (int c = 0; c < 32; c += 2) {
+                    mr0 = fmax3(mr0, __uint_as_float(sa[c]), __uint_as_float(sa[c + 1]));
+                    mr1 = fmax3(mr1, __uint_as_float(sb[c]), __uint_as_float(sb[c + 1]));
+                }
+                const float mx = fmaxf(mr0, mr1) * cs;
+                // raw logit of the ragged last block (C ops)
                 float xlast = -INFINITY;
                 if (clast >= 0) {
 #pragma unroll
@@ -381,12 +393,13 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 float h0 = 0.f, h1 = 0.f;
                 uint32_t pk[32];
+                const float negm = -m;
 #pragma unroll
                 for (int c = 0; c < 16; ++c) {
-                    const float p0 = ex2(__uint_as_float(sa[2 * c]) - m);
-                    const float p1 = ex2(__uint_as_float(sa[2 * c + 1]) - m);
-                    const float p2 = ex2(__uint_as_float(sb[2 * c]) - m);
-                    const float p3 = ex2(__uint_as_float(sb[2 * c + 1]) - m);
+                    const float p0 = ex2(fmaf(__uint_as_float(sa[2 * c]), cs, negm));
+                    const float p1 = ex2(fmaf(__uint_as_float(sa[2 * c + 1]), cs, negm));
+                    const float p2 = ex2(fmaf(__uint_as_float(sb[2 * c]), cs, negm));
+                    const float p3 = ex2(fmaf(__uint_as_float(sb[2 * c + 1]), cs, negm));
                     h0 += p0 + p1;
                     h1 += p2 + p3;
                     pk[c] = pack_bf16(p0, p1);
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     l += h0 + h1;
                 } else {
                     // denominator: n_j * p_j; every dropped block has 64 tokens except the last
-                    const float pl = clast >= 0 ? ex2(xlast - m) : 0.f;
+                    const float pl = clast >= 0 ? ex2(fmaf(xlast, cs, negm)) : 0.f;
                     l += 64.f * (h0 + h1) - (64.f - wlast) * pl;
                     // group sums A_{t,g} (each 32-block half lies in one group)
                     const int64_t j0 = 64 * (int64_t)v;
@@ -413,7 +426,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_wait_st();
             } else {
                 // F(g): write Aq = bf16(s * A_{t,g} * q_t) into the TMEM A buffer
+                // (packed bf16x2 multiply: w is rounded to bf16 once, R-21)
                 const float w = p.s * (v == g_done ? A_done : A_cur);
+                const uint32_t w2 = pack_bf16(w, w);
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {
                     uint32_t aq[32];
@@ -421,13 +436,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     for (int c = 0; c < 8; ++c) {
                         const uint4 u = *reinterpret_cast<const uint4*>(
                             qrow + a * G_::QBOX + r * 128 + ((c ^ (r & 7)) << 4));
-                        const uint32_t uw[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float lo = __uint_as_float(uw[e] << 16);
-                            const float hi = __uint_as_float(uw[e] & 0xFFFF0000u);
-                            aq[c * 4 + e] = pack_bf16(w * lo, w * hi);
-                        }
+                        aq[c * 4 + 0] = hmul2_bf16(u.x, w2);
+                        aq[c * 4 + 1] = hmul2_bf16(u.y, w2);
+                        aq[c * 4 + 2] = hmul2_bf16(u.z, w2);
+                        aq[c * 4 + 3] = hmul2_bf16(u.w, w2);
                     }
                     tmem_st32(t_buf + 32 * a, aq);
                 }
