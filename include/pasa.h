@@ -177,6 +177,9 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
 #define PASA_ATTN_FORCE_SIMT 1u
 #define PASA_ATTN_STATS_ONLY 2u
 #define PASA_ATTN_REUSE_STATS 4u
+/*   PASA_ATTN_PAIRED       use the paired-block tensor-core variant (one CTA per SM, kept
+ *                          blocks processed two at a time; same results up to rounding) */
+#define PASA_ATTN_PAIRED 8u
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 
@@ -195,6 +198,15 @@ pasa_status pasa_route_read(pasa_route_h route, int32_t* k, int32_t* idx, int32_
 pasa_status pasa_route_pooled_read(pasa_route_h route, double* qbar, double* kbar, void* stream);
 /* Geometry of a handle: dims[0..6] = {B, S, H, D, N_Q, N_K, N_G}. */
 pasa_status pasa_route_dims(pasa_route_h route, int64_t dims[7]);
+/* Diagnostics: make the next tensor-core attention launches record a clock64()
+ * timeline of CTA (x, y) into dev_buf (DEVICE, 13 x 4096 uint64: producer, MMA
+ * and softmax events per op); NULL disables.  Returns the element count. */
+int pasa_debug_trace(void* dev_buf, int x, int y);
+/* Diagnostics: performance ablations of the tensor-core attention kernel (1 = the
+ * softmax warps skip their arithmetic, 2 = the producers skip the TMA loads).
+ * Results are meaningless while set; 0 restores normal operation.  Returns the
+ * previous flags. */
+int pasa_debug_flags(int flags);
 /* Number of kernel launches the last pasa_budget / pasa_route / pasa_attn
  * call on this thread issued (bench accounting). */
 int32_t pasa_last_launch_count(void);

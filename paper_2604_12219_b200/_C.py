@@ -22,6 +22,7 @@ COMP = {"grouped": 0, "zeroth": 1, "none": 2}
 PASA_ATTN_FORCE_SIMT = 1
 PASA_ATTN_STATS_ONLY = 2
 PASA_ATTN_REUSE_STATS = 4
+PASA_ATTN_PAIRED = 8
 
 # every symbol include/pasa.h declares (tests check the library exports them all)
 EXPORTS = [
@@ -29,7 +30,7 @@ EXPORTS = [
     "pasa_route_init", "pasa_budget_fini", "pasa_route_fini", "pasa_budget", "pasa_route",
     "pasa_attn", "pasa_attn_ex", "pasa_layer_seed", "pasa_budget_read", "pasa_route_read",
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
-    "pasa_version",
+    "pasa_version", "pasa_debug_trace", "pasa_debug_flags",
 ]
 
 
@@ -108,6 +109,10 @@ def lib():
     L.pasa_last_error.argtypes = []
     L.pasa_version.restype = ctypes.c_char_p
     L.pasa_version.argtypes = []
+    L.pasa_debug_trace.restype = ctypes.c_int
+    L.pasa_debug_trace.argtypes = [P, ctypes.c_int, ctypes.c_int]
+    L.pasa_debug_flags.restype = ctypes.c_int
+    L.pasa_debug_flags.argtypes = [ctypes.c_int]
     for name in ("pasa_budget_init", "pasa_route_init", "pasa_budget", "pasa_route",
                  "pasa_attn", "pasa_attn_ex", "pasa_budget_read", "pasa_route_read",
                  "pasa_route_pooled_read", "pasa_route_dims"):

@@ -267,14 +267,16 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     // global group); fp32 I/O, Bq = 64 and finer groups run the CUDA-core kernel
     // (documented in include/pasa.h and DESIGN.md §7).
     const pasa_route_cfg& c = route->cfg;
-    const bool fine_groups = c.comp == PASA_COMP_GROUPED && c.G % 32 != 0 && c.G < route->NK;
+    const bool fine_groups = c.comp == PASA_COMP_GROUPED && !pasa::sm100_supports_group(c.G, route->NK);
     const bool simt = q->dtype == PASA_F32 || (flags & PASA_ATTN_FORCE_SIMT) || c.Bq != 128 ||
                       fine_groups;
     if (simt) {
         e = pasa::launch_attn_simt(*q, *k, *v, route, *out, s, &launches);
     } else {
         char why[256] = {0};
-        e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        e = (flags & PASA_ATTN_PAIRED)
+                ? pasa::launch_attn_sm100_pair(*q, *k, *v, route, *out, s, &launches, why, sizeof(why))
+                : pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
         if (e == cudaErrorNotSupported) {
             g_launches = launches;
             return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);

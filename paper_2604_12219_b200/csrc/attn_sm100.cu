@@ -69,12 +69,25 @@ struct Params {
     const uint32_t* mask;
     __nv_bfloat16* out;
     int64_t osB, osS, osH;
+    unsigned long long* trace;   // diagnostics: clock64 timeline of one CTA, or nullptr
+    int32_t trace_x, trace_y;
+    int32_t dbg;                 // diagnostics ablations (see pasa_debug_flags)
 };
+
+// timeline events (pasa_debug_trace); slot = event * kTraceN + index
+constexpr int kTraceN = 4096;
+enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK, TR_SA_ARR,
+       TR_SB_W, TR_SB_OK, TR_SB_ARR, TR_MMA_QKW, TR_KPROD_W, TR_SA_LD, TR_SA_MAX, TR_SA_EXP,
+       TR_SA_ST, TR_NEV };
+#define PASA_TR(ev, ix)                                                               \
+    do {                                                                              \
+        if (tracing && (ix) < kTraceN) p.trace[(ev) * kTraceN + (ix)] = clock64();    \
+    } while (0)
 
 struct Ctl {
     uint64_t q_full;
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_full[2], pv_done;
+    uint64_t s_full[2], p_full[2], pv_done[2];   // pv_done[b]: the O-MMA of an op on buffer b done
     uint32_t tmem_base;
     int32_t nops;
     uint32_t mask[64];
@@ -96,6 +109,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     __shared__ Ctl ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool tracing = p.trace != nullptr && (int)blockIdx.x == p.trace_x &&
+                         (int)blockIdx.y == p.trace_y;
     const int64_t i = blockIdx.x, bh = blockIdx.y;
     const int64_t b = bh / p.H, h = bh % p.H;
     const int64_t row = bh * p.NQ + i;
@@ -116,7 +131,8 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(&ctl.s_full[s], 1);
             mbar_init(&ctl.p_full[s], 128);
         }
-        mbar_init(&ctl.pv_done, 1);
+        mbar_init(&ctl.pv_done[0], 1);
+        mbar_init(&ctl.pv_done[1], 1);
         fence_barrier_init();
     }
     if (warp == 1) {
@@ -237,22 +253,26 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t q_base = smem_u32(smem + G_::OFF_Q);
         const uint32_t k_base = smem_u32(smem + G_::OFF_K);
         const uint32_t v_base = smem_u32(smem + G_::OFF_V);
+        // descriptors: the 14-bit start-address field is advanced arithmetically
+        const uint64_t dq0 = umma_desc_sw128(q_base, 16, 1024);
+        const uint64_t dk0 = umma_desc_sw128(k_base, 16, 1024);
+        const uint64_t dv0 = umma_desc_sw128(v_base, G_::KVBOX, 1024);
         auto issue_qk = [&](int n) {
             const int s = n & 1;
+            if (lane == 0) PASA_TR(TR_MMA_QKW, n);
             mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t d = tbase + kColS + 64 * s;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t off = (kk >> 2) * 0 + (kk & 3) * 32;
-                    const uint64_t ad = umma_desc_sw128(q_base + (kk >> 2) * G_::QBOX + off, 16, 1024);
-                    const uint64_t bd =
-                        umma_desc_sw128(k_base + s * G_::SLOT + (kk >> 2) * G_::KVBOX + off, 16, 1024);
-                    mma_ss(d, ad, bd, kIdQK, kk > 0);
+                    const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
+                    const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
+                    mma_ss(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
                 }
                 mma_commit(&ctl.s_full[s]);
                 mma_commit(&ctl.k_empty[s]);
+                PASA_TR(TR_MMA_QK, n);
             }
             __syncwarp();
         };
@@ -262,22 +282,22 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int n = 0; n < nops; ++n) {
             const int s = n & 1;
             if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
-            mbar_wait_sleep(&ctl.p_full[s], (n >> 1) & 1);
-            tc_fence_after();
             mbar_wait_sleep(&ctl.v_full[s], (n >> 1) & 1);
+            if (lane == 0) PASA_TR(TR_MMA_V, n);
+            mbar_wait_sleep(&ctl.p_full[s], (n >> 1) & 1);
+            if (lane == 0) PASA_TR(TR_MMA_P, n);
             tc_fence_after();
             const int32_t op = ctl.ops[n];
             if (op_type(op) != OP_F) {
                 if (lane == 0) {
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint64_t bd =
-                            umma_desc_sw128(v_base + s * G_::SLOT + kk * 16 * 128, G_::KVBOX, 1024);
-                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdPV,
+                        const uint32_t offv = (s * G_::SLOT + kk * 16 * 128) >> 4;
+                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, dv0 + offv, kIdPV,
                                (n > 0 || kk > 0) ? 1u : 0u);
                     }
                     mma_commit(&ctl.v_empty[s]);
-                    mma_commit(&ctl.pv_done);
+                    mma_commit(&ctl.pv_done[s]);
                 }
             } else {
                 mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
@@ -292,7 +312,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     mma_commit(&ctl.k_empty[s]);
                     mma_commit(&ctl.v_empty[s]);
-                    mma_commit(&ctl.pv_done);
+                    mma_commit(&ctl.pv_done[s]);
                 }
             }
             __syncwarp();
@@ -306,15 +326,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
         int64_t g_cur = -1, g_done = -1;
-        int pv_seen = -1;          // pv_done phases consumed (ops whose MMA completed)
+        // pv_done[b] completes once per op on buffer b (ops b, b+2, ...); seen* = last op whose
+        // completion was consumed.  Before releasing P of op n, op n-2 is consumed, so a
+        // buffer's barrier is never two phases ahead of its consumer.
+        int seen0 = -2, seen1 = -1;
         int sc0 = 0, sc1 = 0;      // S-type ops seen per buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
         const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
-        auto consume_pv = [&](int upto) {
-            while (pv_seen < upto) {
-                ++pv_seen;
-                mbar_wait_sleep(&ctl.pv_done, pv_seen & 1);
+        auto consume_op = [&](int op) {   // wait until the O-MMA of op `op` has completed
+            if (op < 0) return;
+            if (op & 1) {
+                while (seen1 < op) { seen1 += 2; mbar_wait_sleep(&ctl.pv_done[1], (seen1 >> 1) & 1); }
+            } else {
+                while (seen0 < op) { seen0 += 2; mbar_wait_sleep(&ctl.pv_done[0], (seen0 >> 1) & 1); }
             }
         };
         for (int n = 0; n < nops; ++n) {
@@ -325,7 +350,9 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (type != OP_F) {
                 const int par = (s ? sc1 : sc0) & 1;
                 if (s) ++sc1; else ++sc0;
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_W, n);
                 mbar_wait_sleep(&ctl.s_full[s], par);
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
                 tmem_ld32(t_buf, sa);
@@ -379,7 +406,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                     A_cur *= corr;
                 }
                 if (__any_sync(0xffffffffu, resc)) {
-                    consume_pv(n - 1);
+                    consume_op(n - 2);
+                    consume_op(n - 1);
                     tc_fence_after();
 #pragma unroll 1
                     for (int c0 = 0; c0 < D; c0 += 32) {
@@ -429,6 +457,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 // (packed bf16x2 multiply: w is rounded to bf16 once, R-21)
                 const float w = p.s * (v == g_done ? A_done : A_cur);
                 const uint32_t w2 = pack_bf16(w, w);
+                consume_op(n - 2);     // the buffer's previous reader (op n-2) has finished
+                tc_fence_after();
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {
                     uint32_t aq[32];
@@ -445,12 +475,14 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 tmem_wait_st();
             }
-            consume_pv(n - 1);
+            consume_op(n - 2);
             tc_fence_before();
             mbar_arrive(&ctl.p_full[s]);
+            if (warp == 4 && lane == 0) PASA_TR(TR_SA_ARR, n);
         }
         // ---- epilogue: O / l -> bf16 -> global ----
-        consume_pv(nops - 1);
+        consume_op(nops - 2);
+        consume_op(nops - 1);
         tc_fence_after();
         const int64_t t = i * kBQ + r;
         const float inv = 1.f / l;
@@ -480,45 +512,6 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------- host --
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-    static EncodeTiledFn fn = nullptr;
-    if (!fn) {
-        void* ptr = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<EncodeTiledFn>(ptr);
-    }
-    return fn;
-}
-
-bool make_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
-              const uint64_t* strides_bytes, const uint32_t* box, char* why, size_t why_len) {
-    EncodeTiledFn fn = encode_fn();
-    if (!fn) {
-        snprintf(why, why_len, "cuTensorMapEncodeTiled unavailable");
-        return false;
-    }
-    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult rc = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base),
-                     reinterpret_cast<const cuuint64_t*>(dims),
-                     reinterpret_cast<const cuuint64_t*>(strides_bytes),
-                     reinterpret_cast<const cuuint32_t*>(box), estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (rc != CUDA_SUCCESS) {
-        snprintf(why, why_len, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
-        return false;
-    }
-    return true;
-}
-
 template <int D>
 cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                      pasa_route_s* r, const pasa_tensor& out, cudaStream_t st, char* why,
@@ -528,7 +521,7 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
         uint64_t dims[4] = {(uint64_t)t.D, (uint64_t)t.S, (uint64_t)t.H, (uint64_t)t.B};
         uint64_t str[3] = {(uint64_t)t.sS * 2, (uint64_t)t.sH * 2, (uint64_t)t.sB * 2};
         uint32_t box[4] = {64, rows, 1, 1};
-        return make_map(m, t.data, 4, dims, str, box, why, why_len);
+        return make_tensor_map(m, t.data, 4, dims, str, box, why, why_len);
     };
     if (!act(&mQ, q, kBQ) || !act(&mK, k, kBK) || !act(&mV, v, kBK))
         return cudaErrorNotSupported;
@@ -536,15 +529,15 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
         uint64_t dims[3] = {(uint64_t)D, (uint64_t)r->NK, (uint64_t)r->BH};
         uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)r->NK * D * 2};
         uint32_t box[3] = {64, 64, 1};
-        if (!make_map(&mKb, r->kbar_lp, 3, dims, str, box, why, why_len) ||
-            !make_map(&mVs, r->vsum_lp, 3, dims, str, box, why, why_len))
+        if (!make_tensor_map(&mKb, r->kbar_lp, 3, dims, str, box, why, why_len) ||
+            !make_tensor_map(&mVs, r->vsum_lp, 3, dims, str, box, why, why_len))
             return cudaErrorNotSupported;
     }
     {
         uint64_t dims[3] = {(uint64_t)D, (uint64_t)r->NG * D, (uint64_t)r->BH};
         uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)r->NG * D * D * 2};
         uint32_t box[3] = {64, (uint32_t)D, 1};
-        if (!make_map(&mHt, r->ht, 3, dims, str, box, why, why_len)) return cudaErrorNotSupported;
+        if (!make_tensor_map(&mHt, r->ht, 3, dims, str, box, why, why_len)) return cudaErrorNotSupported;
     }
     Params prm;
     prm.S = r->S; prm.H = r->H; prm.NQ = r->NQ; prm.NK = r->NK; prm.NG = r->NG; prm.W = r->W;
@@ -555,6 +548,10 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     prm.idx = r->idx; prm.count = r->count; prm.mask = r->mask;
     prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
     prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
+    prm.trace = g_trace_buf;
+    prm.trace_x = g_trace_x;
+    prm.trace_y = g_trace_y;
+    prm.dbg = g_dbg;
     // request >= 100 KB so at most two CTAs share an SM (2 x 256 TMEM columns)
     size_t smem = (size_t)Geo<D>::BYTES + 1024;
     if (smem < 100 * 1024) smem = 100 * 1024;

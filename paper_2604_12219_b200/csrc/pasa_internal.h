@@ -1,6 +1,7 @@
 // pasa_internal.h -- host-side handle layout and kernel launchers of libpasa.so.
 // Product code: nothing here includes or calls anything under oracle/.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -58,9 +59,28 @@ cudaError_t launch_attn_simt(const pasa_tensor& q, const pasa_tensor& k, const p
                              pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                              int* launches);
 
+// group sizes the tensor-core kernel's group-sum bookkeeping covers: every 32-block
+// mask word inside one group, and at most two groups per 64-block half-chunk
+inline bool sm100_supports_group(int64_t G, int64_t NK) {
+    return G == 32 || G == 64 || G % 128 == 0 || G >= NK;
+}
+
 // returns cudaErrorNotSupported if the configuration is outside the kernel's domain
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                               int* launches, char* why, size_t why_len);
+// variant: one CTA per SM, kept blocks processed in pairs (N = 128 QK^T), two
+// independent softmax warpgroups (PASA_ATTN_PAIRED)
+cudaError_t launch_attn_sm100_pair(const pasa_tensor& q, const pasa_tensor& k,
+                                   const pasa_tensor& v, pasa_route_s* r, const pasa_tensor& out,
+                                   cudaStream_t st, int* launches, char* why, size_t why_len);
+
+// tmap.cpp: TMA tensor-map encoding (bf16, 128-byte swizzle, zero OOB fill) and the
+// diagnostics state set by pasa_debug_trace / pasa_debug_flags
+bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                     const uint64_t* strides_bytes, const uint32_t* box, char* why,
+                     size_t why_len);
+extern unsigned long long* g_trace_buf;
+extern int g_trace_x, g_trace_y, g_dbg;
 
 }  // namespace pasa

@@ -65,6 +65,11 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity,
     while (!mbar_try_wait_sleep(bar, parity, ns)) {
     }
 }
+// critical-path wait: plain polling (spin) or suspend-hinted
+__device__ __forceinline__ void mbar_wait_c(uint64_t* bar, uint32_t parity, bool spin) {
+    if (spin) mbar_wait(bar, parity);
+    else mbar_wait_sleep(bar, parity);
+}
 
 // -------------------------------------------------------------------- TMA --
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* m) {
@@ -169,6 +174,20 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
+        : "memory");
+}
+// named barrier over `n` threads (multiple of 32)
+__device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 // ------------------------------------------------------------ descriptors --
 // UMMA shared-memory descriptor, SWIZZLE_128B, Blackwell version bits = 1.
 // K-major (rows of 128 B, 8-row groups 1024 B apart):  lbo = 16 B (unused), sbo = 1024 B.
@@ -198,6 +217,20 @@ __device__ __forceinline__ float ex2(float x) {
     float y;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+// 2^x on the FMA/ALU pipes only (no XU conversions): x = j + f with j = rint(x)
+// taken from the mantissa of x + 1.5*2^23, f in [-1/2, 1/2], 2^f by a degree-3
+// minimax polynomial (max relative error 1.0e-4), 2^j added to the exponent field.
+// x is clamped at -126 (result ~1.2e-38 instead of 0 for -inf inputs).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.0f;                       // 1.5 * 2^23: rounds x to an integer
+    const int ji = __float_as_int(t) - 0x4B400000;          // that integer
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(0.05500868998260835f, f, 0.2422106313698579f);
+    p = fmaf(p, f, 0.6932829170291438f);
+    p = fmaf(p, f, 1.0f);
+    return __int_as_float(__float_as_int(p) + (ji << 23));
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float r;

@@ -1,0 +1,75 @@
+// tmap.cpp -- host helpers shared by the tensor-core attention kernels: TMA tensor
+// map encoding (driver entry point, no libcuda link) and the diagnostics hooks
+// (pasa_debug_trace / pasa_debug_flags).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "pasa_internal.h"
+
+namespace pasa {
+
+unsigned long long* g_trace_buf = nullptr;
+int g_trace_x = 0, g_trace_y = 0;
+int g_dbg = 0;
+
+namespace {
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+}  // namespace
+
+bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
+                     const uint64_t* strides_bytes, const uint32_t* box, char* why,
+                     size_t why_len) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) {
+        snprintf(why, why_len, "cuTensorMapEncodeTiled unavailable");
+        return false;
+    }
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    CUresult rc = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base),
+                     reinterpret_cast<const cuuint64_t*>(dims),
+                     reinterpret_cast<const cuuint64_t*>(strides_bytes),
+                     reinterpret_cast<const cuuint32_t*>(box), estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (rc != CUDA_SUCCESS) {
+        snprintf(why, why_len, "cuTensorMapEncodeTiled failed (%d)", (int)rc);
+        return false;
+    }
+    return true;
+}
+
+}  // namespace pasa
+
+extern "C" int pasa_debug_flags(int flags) {
+    // diagnostics only: performance ablations (results are wrong while set)
+    const int old = pasa::g_dbg;
+    pasa::g_dbg = flags;
+    return old;
+}
+
+extern "C" int pasa_debug_trace(void* dev_buf, int x, int y) {
+    // diagnostics only: the next tensor-core attention launches record the clock64
+    // timeline of CTA (x, y) into dev_buf[17][4096] (uint64); dev_buf = NULL disables.
+    pasa::g_trace_buf = reinterpret_cast<unsigned long long*>(dev_buf);
+    pasa::g_trace_x = x;
+    pasa::g_trace_y = y;
+    return 17 * 4096;
+}

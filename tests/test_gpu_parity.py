@@ -204,6 +204,10 @@ ATTN_CASES = [
     ("tc_d64_4100_none", 1, 4100, 2, 64, 128, 32, "none", 0.15, torch.bfloat16, "iid"),
     ("fp32_d128_4100", 1, 4100, 1, 128, 128, 32, "grouped", 0.15, torch.float32, "video"),
     ("tc_d128_g8_simt", 1, 4100, 1, 128, 128, 8, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d128_g96_simt", 1, 8200, 1, 128, 128, 96, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d128_20000_g128", 1, 20000, 1, 128, 128, 128, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d64_20000_g64", 1, 20000, 1, 64, 128, 64, "grouped", 0.2, torch.bfloat16, "video"),
+    ("tc_d128_odd_k", 1, 4100, 2, 128, 128, 32, "grouped", 0.11, torch.bfloat16, "iid"),
 ]
 
 
