@@ -196,6 +196,11 @@ pasa_status pasa_route_read(pasa_route_h route, int32_t* k, int32_t* idx, int32_
                             uint32_t* mask, void* stream);
 /* HOST outputs (may be NULL): qbar [B*H][N_Q][D], kbar [B*H][N_K][D] fp64. */
 pasa_status pasa_route_pooled_read(pasa_route_h route, double* qbar, double* kbar, void* stream);
+/* HOST outputs (may be NULL) of the last pasa_attn statistics pass, in the I/O dtype
+ * (bf16 or fp32): kbar [B*H][N_K][D], vsum [B*H][N_K][D], ht [B*H][N_G][D][D]
+ * (ht[.][g][n][k] = Hbar^(g)[k][n]).  Synchronises `stream`. */
+pasa_status pasa_attn_stats_read(pasa_route_h route, void* kbar, void* vsum, void* ht,
+                                 void* stream);
 /* Geometry of a handle: dims[0..6] = {B, S, H, D, N_Q, N_K, N_G}. */
 pasa_status pasa_route_dims(pasa_route_h route, int64_t dims[7]);
 /* Diagnostics: make the next tensor-core attention launches record a clock64()

@@ -30,7 +30,7 @@ EXPORTS = [
     "pasa_route_init", "pasa_budget_fini", "pasa_route_fini", "pasa_budget", "pasa_route",
     "pasa_attn", "pasa_attn_ex", "pasa_layer_seed", "pasa_budget_read", "pasa_route_read",
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
-    "pasa_version", "pasa_debug_trace", "pasa_debug_flags",
+    "pasa_version", "pasa_debug_trace", "pasa_debug_flags", "pasa_attn_stats_read",
 ]
 
 
@@ -103,6 +103,8 @@ def lib():
     L.pasa_route_read.argtypes = [P, P, P, P, P, P]
     L.pasa_route_pooled_read.argtypes = [P, P, P, P]
     L.pasa_route_dims.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
+    L.pasa_attn_stats_read.argtypes = [P, P, P, P, P]
+    L.pasa_attn_stats_read.restype = ctypes.c_int
     L.pasa_last_launch_count.restype = I32
     L.pasa_last_launch_count.argtypes = []
     L.pasa_last_error.restype = ctypes.c_char_p

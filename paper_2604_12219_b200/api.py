@@ -165,6 +165,20 @@ class Route:
                                           _stream_ptr(stream)), "pasa_route_read")
         return dict(k=int(k[0]), idx=idx, count=cnt, mask=mask)
 
+    def stats(self, dtype=torch.bfloat16, stream=None):
+        """Statistics of the last pasa_attn: (kbar, vsum, ht) as float64 numpy arrays,
+        ht[bh, g, n, k] = Hbar^(g)[k][n]."""
+        B, S, H, D = self.shape
+        t = torch.empty
+        kb = t((B * H, self.NK, D), dtype=dtype)
+        vs = t((B * H, self.NK, D), dtype=dtype)
+        ht = t((B * H, self.NG, D, D), dtype=dtype)
+        _C.check(_C.lib().pasa_attn_stats_read(self.handle, ctypes.c_void_p(kb.data_ptr()),
+                                               ctypes.c_void_p(vs.data_ptr()),
+                                               ctypes.c_void_p(ht.data_ptr()),
+                                               _stream_ptr(stream)), "pasa_attn_stats_read")
+        return (kb.double().numpy(), vs.double().numpy(), ht.double().numpy())
+
     def pooled(self, stream=None):
         B, S, H, D = self.shape
         qb = np.zeros((B * H, self.NQ, D))

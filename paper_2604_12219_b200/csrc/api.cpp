@@ -334,6 +334,21 @@ pasa_status pasa_route_pooled_read(pasa_route_h r, double* qbar, double* kbar, v
     return cuda_status(e, "pasa_route_pooled_read");
 }
 
+pasa_status pasa_attn_stats_read(pasa_route_h r, void* kbar, void* vsum, void* ht, void* stream) {
+    if (!r) return fail(PASA_EINVAL, "NULL route");
+    if (r->stats_dtype < 0) return fail(PASA_EINVAL, "no statistics pass has run on this route");
+    const size_t es = r->stats_dtype == PASA_F32 ? 4 : 2;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (kbar) e = cudaMemcpyAsync(kbar, r->kbar_lp, es * r->BH * r->NK * r->D, cudaMemcpyDeviceToHost, s);
+    if (vsum && e == cudaSuccess)
+        e = cudaMemcpyAsync(vsum, r->vsum_lp, es * r->BH * r->NK * r->D, cudaMemcpyDeviceToHost, s);
+    if (ht && e == cudaSuccess)
+        e = cudaMemcpyAsync(ht, r->ht, es * r->BH * r->NG * r->D * r->D, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e, "pasa_attn_stats_read");
+}
+
 pasa_status pasa_route_dims(pasa_route_h r, int64_t dims[7]) {
     if (!r || !dims) return fail(PASA_EINVAL, "NULL argument");
     dims[0] = r->B; dims[1] = r->S; dims[2] = r->H; dims[3] = r->D;

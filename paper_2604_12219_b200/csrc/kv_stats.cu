@@ -198,6 +198,8 @@ cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_rou
     a.vsB = v.sB; a.vsS = v.sS; a.vsH = v.sH;
     a.S = r->S; a.H = r->H; a.NK = r->NK; a.NG = r->NG; a.G = r->cfg.G;
     a.kbar = r->kbar; a.kbar_lp = r->kbar_lp; a.vsum_lp = r->vsum_lp; a.ht = r->ht;
+    if (k.dtype == PASA_BF16 && kv_stats_sm100_supported(r) && !(g_dbg & 16))
+        return launch_kv_stats_sm100(k, v, r, st, launches);
     dim3 grid((unsigned)r->NG, (unsigned)r->BH);
     if (k.dtype == PASA_BF16) {
         if (r->D == 128) stats_bf16_kernel<128><<<grid, 256, 0, st>>>(a);

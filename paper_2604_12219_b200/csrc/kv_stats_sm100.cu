@@ -1,0 +1,246 @@
+// kv_stats_sm100.cu -- the K/V block statistics of pasa_attn on the Blackwell tensor
+// cores (d = 128, bf16): Kbar_j (bf16 copy of the route's fp64 block means), Vsum_j,
+// and the grouped first-order statistic
+//   Hbar^(g) = (1/|G_g|) sum_{j in G_g} sum_n (K_{j,n} - Kbar_j)^T V_{j,n}
+//            = (1/|G_g|) [ sum_{n in G_g} K_n^T V_n  -  sum_{j in G_g} Kbar_j^T Vsum_j ]
+// (Eq. 5 + App. B).  The first term is one contraction over all
+// of the group's tokens, run on tcgen05 straight from TMA-loaded K / V tiles (both
+// operands MN-major: Ht[n][k] = sum_t V[t][n] K[t][k]); the second (the exact centring
+// correction, rank 1 per block) is accumulated in fp32 on CUDA cores.  Per-block H_j is
+// never materialised.  One CTA per (head, group), 4-stage TMA ring, HBM
+// bound: 2 S d * 2 bytes per head.
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstdio>
+
+#include "pasa_internal.h"
+#include "sm100_ptx.cuh"
+
+namespace pasa {
+namespace {
+
+using namespace ptx;
+
+constexpr int D = 128;
+constexpr int kBk = 64;
+constexpr int kStages = 4;
+constexpr int kTile = kBk * D * 2;          // 16 KB: one K or V block tile
+constexpr int kBox = kBk * 128;             // 8 KB: 64 tokens x 64 dims (128-byte rows)
+constexpr int kMaxG = 64;                   // blocks per group handled by one CTA's smem
+constexpr int kThreads = 256;               // warp 0 TMA, warp 1 MMA, warps 4-7 math
+
+struct Args {
+    int64_t H, NK, NG, S;
+    int32_t G;
+    const double* kbar;       // [BH][NK][D] fp64 (route)
+    __nv_bfloat16* kbar_lp;   // [BH][NK][D]
+    __nv_bfloat16* vsum_lp;   // [BH][NK][D]
+    __nv_bfloat16* ht;        // [BH][NG][D][D]
+};
+
+struct Ctl {
+    uint64_t full[kStages], empty[kStages], acc_full;
+    uint32_t tmem_base;
+};
+struct Scratch {              // dynamic smem after the TMA stages
+    float vsum[kMaxG][D];     // fp32 Vsum_j of the group's blocks
+    float kb[kMaxG][D];       // fp32 Kbar_j
+    float part[4][D];         // per-warp partial column sums
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    kv_stats_sm100_kernel(const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                               ~uintptr_t(1023));
+    __shared__ Ctl ctl;
+    Scratch& sc = *reinterpret_cast<Scratch*>(smem + kStages * 2 * kTile);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t g = blockIdx.x, bh = blockIdx.y;
+    const int64_t b = bh / a.H, h = bh % a.H;
+    const int64_t j0 = g * a.G;
+    const int nb = (int)min((int64_t)a.G, a.NK - j0);   // blocks in this group
+
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&ctl.full[s], 1);
+            mbar_init(&ctl.empty[s], 2);     // MMA commit + the math warpgroup
+        }
+        mbar_init(&ctl.acc_full, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) {
+        tmem_alloc(&ctl.tmem_base, 128);
+        tmem_relinquish();
+    }
+    // fp32 Kbar of the group (and its bf16 copy for the attention kernel)
+    for (int e = tid; e < nb * D; e += kThreads) {
+        const int jj = e / D, d = e % D;
+        const double kv = a.kbar[(bh * a.NK + j0 + jj) * D + d];
+        sc.kb[jj][d] = (float)kv;
+        a.kbar_lp[(bh * a.NK + j0 + jj) * D + d] = __float2bfloat16_rn((float)kv);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tbase = ctl.tmem_base;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int jj = 0; jj < nb; ++jj) {
+                const int s = jj % kStages;
+                mbar_wait_sleep(&ctl.empty[s], ((jj / kStages) & 1) ^ 1);
+                uint8_t* st = smem + s * 2 * kTile;
+                mbar_arrive_expect_tx(&ctl.full[s], 2 * kTile);
+                const int tok = (int)((j0 + jj) * kBk);
+#pragma unroll
+                for (int bx = 0; bx < 2; ++bx) {
+                    tma_load_4d(st + bx * kBox, &tmK, &ctl.full[s], 64 * bx, tok, (int)h, (int)b);
+                    tma_load_4d(st + kTile + bx * kBox, &tmV, &ctl.full[s], 64 * bx, tok, (int)h,
+                                (int)b);
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // Ht[n][k] += sum_t V[t][n] K[t][k]:  A = V^T (M = n, MN-major), B = K (N = k, MN-major)
+        constexpr uint32_t kId = idesc_bf16_f32(128, 128, 1, 1);
+        const uint64_t d0 = umma_desc_sw128(smem_u32(smem), kBox, 1024);
+        for (int jj = 0; jj < nb; ++jj) {
+            const int s = jj % kStages;
+            mbar_wait_sleep(&ctl.full[s], (jj / kStages) & 1);
+            tc_fence_after();
+            if (lane == 0) {
+#pragma unroll
+                for (int kk = 0; kk < kBk / 16; ++kk) {
+                    const uint32_t offk = ((uint32_t)s * 2 * kTile + kk * 2048) >> 4;
+                    const uint32_t offv = ((uint32_t)s * 2 * kTile + kTile + kk * 2048) >> 4;
+                    mma_ss(tbase, d0 + offv, d0 + offk, kId, (jj > 0 || kk > 0) ? 1u : 0u);
+                }
+                mma_commit(&ctl.empty[s]);
+                if (jj == nb - 1) mma_commit(&ctl.acc_full);
+            }
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // Vsum_j: thread t sums 8 consecutive dims (one 16-byte chunk) over 8 of the 64 rows
+        const int mt = tid - 128;               // 0..127
+        const int chunk = mt & 15;              // dims 8*chunk .. +7
+        const int rg = mt >> 4;                 // rows rg*8 .. rg*8+7
+        const int bx = chunk >> 3, c16 = chunk & 7;
+        for (int jj = 0; jj < nb; ++jj) {
+            const int s = jj % kStages;
+            mbar_wait_sleep(&ctl.full[s], (jj / kStages) & 1);
+            const uint8_t* vt = smem + s * 2 * kTile + kTile + bx * kBox;
+            float acc[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+#pragma unroll
+            for (int rr = 0; rr < 8; ++rr) {
+                const int t = rg * 8 + rr;
+                const uint4 u = *reinterpret_cast<const uint4*>(vt + t * 128 + ((c16 ^ (t & 7)) << 4));
+                const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(v2[e]);
+                    acc[2 * e] += f.x;
+                    acc[2 * e + 1] += f.y;
+                }
+            }
+            // reduce the 8 row groups: shuffle within the warp (2 row groups per warp), then smem
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], 16);
+            if (lane < 16) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) sc.part[warp - 4][chunk * 8 + e] = acc[e];
+            }
+            bar_sync(1, 128);
+            if (mt == 0) mbar_arrive(&ctl.empty[s]);   // this warpgroup is done with the stage
+            {
+                const int d = mt;                      // 128 threads <-> 128 dims
+                const float vs = sc.part[0][d] + sc.part[1][d] + sc.part[2][d] + sc.part[3][d];
+                sc.vsum[jj][d] = vs;
+                a.vsum_lp[(bh * a.NK + j0 + jj) * D + d] = __float2bfloat16_rn(vs);
+            }
+            bar_sync(1, 128);
+        }
+        // epilogue: thread n owns row n of Ht (TMEM lane n)
+        mbar_wait_sleep(&ctl.acc_full, 0);
+        tc_fence_after();
+        const int n = mt;
+        const uint32_t t_row = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+        const float inv = 1.f / (float)nb;
+        __nv_bfloat16* out = a.ht + ((bh * a.NG + g) * D + n) * D;
+#pragma unroll 1
+        for (int c0 = 0; c0 < D; c0 += 32) {
+            uint32_t raw[32];
+            tmem_ld32(t_row + c0, raw);
+            tmem_wait_ld();
+            float acc[32];
+#pragma unroll
+            for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(raw[c]);
+            // exact centring: subtract sum_j Vsum_j[n] Kbar_j[k]
+            for (int jj = 0; jj < nb; ++jj) {
+                const float vs = sc.vsum[jj][n];
+                const float4* kb4 = reinterpret_cast<const float4*>(&sc.kb[jj][c0]);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float4 kv = kb4[c];
+                    acc[4 * c + 0] = fmaf(-vs, kv.x, acc[4 * c + 0]);
+                    acc[4 * c + 1] = fmaf(-vs, kv.y, acc[4 * c + 1]);
+                    acc[4 * c + 2] = fmaf(-vs, kv.z, acc[4 * c + 2]);
+                    acc[4 * c + 3] = fmaf(-vs, kv.w, acc[4 * c + 3]);
+                }
+            }
+            uint4 pk[4];
+            uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) pw[c] = pack_bf16(acc[2 * c] * inv, acc[2 * c + 1] * inv);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(out + c0)[q] = pk[q];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tbase, 128);
+    }
+}
+
+}  // namespace
+
+bool kv_stats_sm100_supported(const pasa_route_s* r) {
+    return r->D == 128 && r->cfg.G <= kMaxG;
+}
+
+cudaError_t launch_kv_stats_sm100(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
+                                  cudaStream_t st, int* launches) {
+    char why[128];
+    CUtensorMap mK, mV;
+    auto act = [&](CUtensorMap* m, const pasa_tensor& t) {
+        uint64_t dims[4] = {(uint64_t)t.D, (uint64_t)t.S, (uint64_t)t.H, (uint64_t)t.B};
+        uint64_t str[3] = {(uint64_t)t.sS * 2, (uint64_t)t.sH * 2, (uint64_t)t.sB * 2};
+        uint32_t box[4] = {64, (uint32_t)kBk, 1, 1};
+        return make_tensor_map(m, t.data, 4, dims, str, box, why, sizeof(why));
+    };
+    if (!act(&mK, k) || !act(&mV, v)) return cudaErrorInvalidValue;
+    Args a;
+    a.H = r->H; a.NK = r->NK; a.NG = r->NG; a.S = r->S; a.G = r->cfg.G;
+    a.kbar = r->kbar;
+    a.kbar_lp = reinterpret_cast<__nv_bfloat16*>(r->kbar_lp);
+    a.vsum_lp = reinterpret_cast<__nv_bfloat16*>(r->vsum_lp);
+    a.ht = reinterpret_cast<__nv_bfloat16*>(r->ht);
+    const size_t smem = (size_t)kStages * 2 * kTile + sizeof(Scratch) + 1024;
+    cudaError_t e = cudaFuncSetAttribute(kv_stats_sm100_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)r->NG, (unsigned)r->BH);
+    kv_stats_sm100_kernel<<<grid, kThreads, smem, st>>>(mK, mV, a);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace pasa

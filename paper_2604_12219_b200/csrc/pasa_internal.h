@@ -54,6 +54,10 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
 
 cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                             cudaStream_t st, int* launches);
+// tensor-core statistics pass (d = 128, bf16, G <= 64); launch_kv_stats dispatches to it
+bool kv_stats_sm100_supported(const pasa_route_s* r);
+cudaError_t launch_kv_stats_sm100(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
+                                  cudaStream_t st, int* launches);
 
 cudaError_t launch_attn_simt(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                              pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
