@@ -37,7 +37,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
-    size_t off_hdr, off_qbar, off_kbar, off_scores, off_kbar_lp, off_vsum, off_ht, off_idx,
+    size_t off_hdr, off_qbar, off_kbar, off_scores, off_sigma, off_kbar_lp, off_vsum, off_ht, off_idx,
         off_count, off_mask, total;
 };
 
@@ -72,6 +72,7 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_qbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NQ * D);
     L.off_kbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NK * D);
     L.off_scores = o;   o = align_up(o + sizeof(double) * L.BH * L.NQ * L.NK);
+    L.off_sigma = o;    o = align_up(o + sizeof(double) * L.BH * L.NQ);
     L.off_kbar_lp = o;  o = align_up(o + 4 * L.BH * L.NK * D);
     L.off_vsum = o;     o = align_up(o + 4 * L.BH * L.NK * D);
     L.off_ht = o;       o = align_up(o + 4 * L.BH * L.NG * D * D);
@@ -164,6 +165,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
     r->kbar = reinterpret_cast<double*>(w + L.off_kbar);
     r->scores = reinterpret_cast<double*>(w + L.off_scores);
+    r->sigma = reinterpret_cast<double*>(w + L.off_sigma);
     r->kbar_lp = w + L.off_kbar_lp;
     r->vsum_lp = w + L.off_vsum;
     r->ht = w + L.off_ht;

@@ -30,6 +30,7 @@ struct pasa_route_s {
     double* qbar;                    // [BH][NQ][D]
     double* kbar;                    // [BH][NK][D]
     double* scores;                  // [BH][NQ][NK] scratch (r, fp64)
+    double* sigma;                   // [BH][NQ] row standard deviations (scratch)
     void* kbar_lp;                   // [BH][NK][D]   bf16 or fp32 (4 B/elem capacity)
     void* vsum_lp;                   // [BH][NK][D]
     void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)

@@ -155,12 +155,75 @@ __global__ void __launch_bounds__(256) scores_kernel(const double* __restrict__ 
 }
 
 // ---------------------------------------------------------------------------
-// a4 + a5: per (head, query block) row: sigma_i, Gumbel bias, top-k by
-// (score desc, j asc) via an 8-pass MSB radix select on orderable 64-bit keys,
-// then an ascending compaction into idx / count / mask.
+// a4 (row statistics): sigma_i, the population std of score row i (R3).  The
+// sums run sequentially in ascending j exactly as in the oracle (bit-exact), one
+// thread per row; 128 rows per CTA are staged through shared memory in column
+// chunks so the loads are coalesced and 128 sequential chains run concurrently.
 // ---------------------------------------------------------------------------
-constexpr int kSelThreads = 256;
-constexpr int kMaxNK = 2048;   // smem capacity of the select kernel (S <= 131,072 at Bk = 64)
+constexpr int kRsRows = 64, kRsCols = 32;
+
+__global__ void __launch_bounds__(kRsRows * 2) rowstats_kernel(const double* __restrict__ r,
+                                                               int64_t rows, int64_t NK,
+                                                               double* __restrict__ sigma) {
+    // 128 threads stage a [64 rows x 64 cols] chunk (register prefetch of the next
+    // chunk overlaps the sequential sums of the current one); threads 0..63 own a row.
+    __shared__ double tile[2][kRsRows][kRsCols + 1];
+    const int tid = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.x * kRsRows;
+    const int nrows = (int)min((int64_t)kRsRows, rows - r0);
+    const int nchunk = (int)((NK + kRsCols - 1) / kRsCols);
+    constexpr int kPer = kRsRows * kRsCols / (kRsRows * 2);   // 32 loads per thread per chunk
+    double buf[kPer];
+    auto fetch = [&](int c) {
+        const int64_t c0 = (int64_t)c * kRsCols;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = tid + u * (kRsRows * 2);
+            const int rr = e / kRsCols, cc = e % kRsCols;
+            buf[u] = (rr < nrows && c0 + cc < NK) ? __ldg(r + (r0 + rr) * NK + c0 + cc) : 0.0;
+        }
+    };
+    auto stash = [&](int slot) {
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int e = tid + u * (kRsRows * 2);
+            tile[slot][e / kRsCols][e % kRsCols] = buf[u];
+        }
+    };
+    double sum = 0.0, mu = 0.0, acc = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        fetch(0);
+        for (int c = 0; c < nchunk; ++c) {
+            const int slot = c & 1;
+            stash(slot);
+            __syncthreads();
+            if (c + 1 < nchunk) fetch(c + 1);
+            const int nc = (int)min((int64_t)kRsCols, NK - (int64_t)c * kRsCols);
+            if (tid < nrows) {
+                if (pass == 0) {
+                    for (int cc = 0; cc < nc; ++cc) sum = __dadd_rn(sum, tile[slot][tid][cc]);
+                } else {
+                    for (int cc = 0; cc < nc; ++cc) {
+                        const double dl = __dsub_rn(tile[slot][tid][cc], mu);
+                        acc = __fma_rn(dl, dl, acc);
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        if (pass == 0) mu = __ddiv_rn(sum, (double)NK);
+    }
+    if (tid < nrows) sigma[r0 + tid] = __dsqrt_rn(__ddiv_rn(acc, (double)NK));
+}
+
+// ---------------------------------------------------------------------------
+// a4 + a5: one warp per (head, query block) row.  Element j = 32 m + lane lives in
+// register m of lane `lane`.  Gumbel bias, then the k-th largest orderable key T is
+// found bit by bit (T = the largest value with #{key >= T} >= k), ties at T go to
+// the smallest j (R-13), and the ballot of each 32-block chunk is directly the
+// route's mask word; the ascending index list follows from ballot prefix counts.
+// ---------------------------------------------------------------------------
+constexpr int kSelWarps = 4;
 
 __device__ __forceinline__ uint64_t orderable(double x) {
     x = __dadd_rn(x, 0.0);  // -0.0 -> +0.0: the oracle's double compare treats them as equal
@@ -178,8 +241,9 @@ __device__ __forceinline__ int device_k(const BudgetRec* rec, int64_t NK) {
 
 struct SelArgs {
     const double* r;          // [BH][NQ][NK]
+    const double* sigma;      // [BH][NQ]
     const BudgetRec* rec;
-    int64_t NQ, NK, W, H, H_total, head_offset;
+    int64_t rows, NQ, NK, W, H, H_total, head_offset;
     double beta;
     uint32_t key0, key1;      // Philox key = (lo32 seed, hi32 seed)
     uint32_t step;
@@ -189,172 +253,88 @@ struct SelArgs {
     int32_t* hdr;
 };
 
-__global__ void __launch_bounds__(kSelThreads) select_kernel(SelArgs a) {
-    __shared__ uint64_t keys[kMaxNK];
-    __shared__ double sr[kMaxNK];
-    __shared__ uint32_t hist[256];
-    __shared__ uint8_t flag[kMaxNK];
-    __shared__ double s_sigma;
-    __shared__ uint64_t s_prefix;
-    __shared__ int s_remaining;
-    __shared__ int warp_tot[kSelThreads / 32][2];
-
-    const int64_t row = blockIdx.x;            // bh * NQ + i
+template <int MAXM>
+__global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);   // bh * NQ + i
+    if (row >= a.rows) return;
     const int64_t bh = row / a.NQ, i = row % a.NQ;
-    const int64_t NK = a.NK;
-    const int tid = threadIdx.x;
+    const int NK = (int)a.NK;
+    const int M = (NK + 31) >> 5;
     const int k = device_k(a.rec, NK);
-    if (row == 0 && tid == 0) a.hdr[0] = k;
-
+    if (row == 0 && lane == 0) a.hdr[0] = k;
     int32_t* orow = a.idx + row * NK;
     uint32_t* mrow = a.mask + row * a.W;
     if (k >= NK) {  // dense step / full budget: every block exact
-        for (int64_t j = tid; j < NK; j += kSelThreads) orow[j] = (int32_t)j;
-        for (int64_t w = tid; w < a.W; w += kSelThreads) {
-            int64_t rem = NK - 32 * w;
+        for (int j = lane; j < NK; j += 32) orow[j] = j;
+        for (int w = lane; w < M; w += 32) {
+            const int rem = NK - 32 * w;
             mrow[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
         }
-        if (tid == 0) a.count[row] = (int32_t)NK;
+        if (lane == 0) a.count[row] = NK;
         return;
     }
-
     const double* rr = a.r + row * NK;
-    for (int64_t j = tid; j < NK; j += kSelThreads) sr[j] = rr[j];
-    __syncthreads();
-
-    if (a.beta != 0.0) {
-        // R3: sequential mean and fma-chain variance (one thread; exact order)
-        if (tid == 0) {
-            double sum = 0.0;
-            for (int64_t j = 0; j < NK; ++j) sum = __dadd_rn(sum, sr[j]);
-            double mu = __ddiv_rn(sum, (double)NK);
-            double acc = 0.0;
-            for (int64_t j = 0; j < NK; ++j) {
-                double dl = __dsub_rn(sr[j], mu);
-                acc = __fma_rn(dl, dl, acc);
+    uint64_t key[MAXM];
+    const bool biased = a.beta != 0.0;
+    const double bi = biased ? __dmul_rn(a.beta, a.sigma[row]) : 0.0;
+    const uint32_t gh = (uint32_t)((bh / a.H) * a.H_total + a.head_offset + (bh % a.H));
+    uint64_t kand = ~0ull, kor = 0ull;
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) {
+        const int j = 32 * m + lane;
+        key[m] = 0ull;                       // absent elements sort last (below every key)
+        if (m < M && j < NK) {
+            double x = __ldg(rr + j);
+            if (biased) {   // R4/R5: rt = r + (beta * sigma_i) * g, two rounded operations
+                const uint32_t x0 = philox4x32_10_x0((uint32_t)j, (uint32_t)i, gh, a.step, a.key0,
+                                                     a.key1);
+                const double u = __dmul_rn(__dadd_rn((double)x0, 0.5), 2.3283064365386963e-10);
+                x = __dadd_rn(x, __dmul_rn(bi, -log(-log(u))));
             }
-            s_sigma = __dsqrt_rn(__ddiv_rn(acc, (double)NK));
+            key[m] = orderable(x);
+            kand &= key[m];
+            kor |= key[m];
         }
-        // meanwhile: the Gumbel draws (R-11/R-12), kept in keys[] as doubles
-        const uint32_t gh = (uint32_t)((bh / a.H) * a.H_total + a.head_offset + (bh % a.H));
-        for (int64_t j = tid; j < NK; j += kSelThreads) {
-            uint32_t x0 = philox4x32_10_x0((uint32_t)j, (uint32_t)i, gh, a.step, a.key0, a.key1);
-            double u = __dmul_rn(__dadd_rn((double)x0, 0.5), 2.3283064365386963e-10);
-            double g = -log(-log(u));
-            keys[j] = (uint64_t)__double_as_longlong(g);
-        }
-        __syncthreads();
-        const double bi = __dmul_rn(a.beta, s_sigma);
-        for (int64_t j = tid; j < NK; j += kSelThreads) {
-            double g = __longlong_as_double((long long)keys[j]);
-            keys[j] = orderable(__dadd_rn(sr[j], __dmul_rn(bi, g)));   // R5
-        }
-    } else {
-        for (int64_t j = tid; j < NK; j += kSelThreads) keys[j] = orderable(sr[j]);
     }
-    if (tid == 0) { s_prefix = 0; s_remaining = k; }
-    __syncthreads();
-
-    // radix select of the k-th largest key
-    uint64_t pmask = 0;
-    for (int pass = 7; pass >= 0; --pass) {
-        const int shift = pass * 8;
-        for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
-        __syncthreads();
-        const uint64_t prefix = s_prefix;
-        for (int64_t j = tid; j < NK; j += kSelThreads) {
-            uint64_t key = keys[j];
-            if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255], 1u);
-        }
-        __syncthreads();
-        if (tid < 32) {
-            // lane l owns digits 255-8l ... 248-8l (descending)
-            uint32_t loc[8];
-            uint32_t sum = 0;
+    // bits above the highest differing bit are common to every present key
 #pragma unroll
-            for (int u = 0; u < 8; ++u) { loc[u] = hist[255 - 8 * tid - u]; sum += loc[u]; }
-            uint32_t incl = sum;
+    for (int o = 16; o > 0; o >>= 1) {
+        kand &= __shfl_xor_sync(0xffffffffu, kand, o);
+        kor |= __shfl_xor_sync(0xffffffffu, kor, o);
+    }
+    const uint64_t diff = kand ^ kor;
+    uint64_t T = diff ? (kand & ~((2ull << (63 - __clzll(diff))) - 1ull)) : kand;
+    for (int bpos = diff ? 63 - __clzll(diff) : -1; bpos >= 0; --bpos) {
+        const uint64_t cand = T | (1ull << bpos);
+        int c = 0;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += v;
-            }
-            const uint32_t rem = (uint32_t)s_remaining;
-            const uint32_t excl = incl - sum;
-            const bool hit = excl < rem && incl >= rem;
-            const unsigned ball = __ballot_sync(0xffffffffu, hit);
-            const int lane = __ffs(ball) - 1;
-            if (tid == lane) {
-                uint32_t cum = excl;
-                int digit = 0;
+        for (int m = 0; m < MAXM; ++m) c += key[m] >= cand;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= k) T = cand;
+    }
+    int gt = 0;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    if (cum + loc[u] >= rem) { digit = 255 - 8 * tid - u; break; }
-                    cum += loc[u];
-                }
-                s_prefix = prefix | ((uint64_t)digit << shift);
-                s_remaining = (int)(rem - cum);
-            }
+    for (int m = 0; m < MAXM; ++m) gt += key[m] > T;
+    const int need = k - __reduce_add_sync(0xffffffffu, gt);   // keys equal to T to take
+    // walk the chunks in ascending j: ties go to the smallest j; the ballot of a chunk
+    // is its mask word; positions come from prefix counts
+    int taken_eq = 0, pos = 0;
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+    for (int m = 0; m < MAXM; ++m) {
+        if (m < M) {
+            const uint32_t eqb = __ballot_sync(0xffffffffu, key[m] == T);
+            const int eq_rank = taken_eq + __popc(eqb & below);
+            const bool take = key[m] > T || (key[m] == T && eq_rank < need);
+            taken_eq += __popc(eqb);
+            const uint32_t sel = __ballot_sync(0xffffffffu, take);
+            if (take) orow[pos + __popc(sel & below)] = 32 * m + lane;
+            pos += __popc(sel);
+            if (lane == 0) mrow[m] = sel;
         }
-        pmask |= (uint64_t)255 << shift;
-        __syncthreads();
     }
-    const uint64_t T = s_prefix;
-    const int need = s_remaining;   // how many keys equal to T are taken (lowest j first)
-
-    // ascending compaction: thread t owns a contiguous run of j
-    const int64_t per = (NK + kSelThreads - 1) / kSelThreads;
-    const int64_t ja = tid * per, jb = min(ja + per, NK);
-    int n_gt = 0, n_eq = 0;
-    for (int64_t j = ja; j < jb; ++j) {
-        uint64_t key = keys[j];
-        n_gt += key > T;
-        n_eq += key == T;
-    }
-    // exclusive block scans of n_eq (tie rank) -- then decide, then scan selected
-    int lane = tid & 31, wid = tid >> 5;
-    int v = n_eq;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int x = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += x;
-    }
-    if (lane == 31) warp_tot[wid][0] = v;
-    __syncthreads();
-    int base = 0;
-    for (int w = 0; w < wid; ++w) base += warp_tot[w][0];
-    int eq_rank = base + v - n_eq;
-    int n_sel = 0;
-    for (int64_t j = ja; j < jb; ++j) {
-        uint64_t key = keys[j];
-        bool take = key > T || (key == T && eq_rank < need);
-        eq_rank += key == T;
-        flag[j] = take;
-        n_sel += take;
-    }
-    __syncthreads();
-    v = n_sel;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int x = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += x;
-    }
-    if (lane == 31) warp_tot[wid][1] = v;
-    __syncthreads();
-    base = 0;
-    for (int w = 0; w < wid; ++w) base += warp_tot[w][1];
-    int pos = base + v - n_sel;
-    for (int64_t j = ja; j < jb; ++j)
-        if (flag[j]) orow[pos++] = (int32_t)j;
-    for (int64_t w = tid; w < a.W; w += kSelThreads) {
-        uint32_t word = 0;
-        for (int u = 0; u < 32; ++u) {
-            int64_t j = 32 * w + u;
-            if (j < NK && flag[j]) word |= 1u << u;
-        }
-        mrow[w] = word;
-    }
-    if (tid == 0) a.count[row] = k;
+    if (lane == 0) a.count[row] = k;
 }
 
 }  // namespace
@@ -377,10 +357,19 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     dim3 sg((unsigned)((r->NK + kST - 1) / kST), (unsigned)((r->NQ + kST - 1) / kST),
             (unsigned)r->BH);
     scores_kernel<<<sg, 256, 0, st>>>(r->qbar, r->kbar, r->NQ, r->NK, r->D, s, r->scores);
+    *launches += 2;
 
+    const int64_t rows = r->BH * r->NQ;
+    if (r->cfg.beta != 0.0) {
+        rowstats_kernel<<<(unsigned)((rows + kRsRows - 1) / kRsRows), kRsRows * 2, 0, st>>>(
+            r->scores, rows, r->NK, r->sigma);
+        *launches += 1;
+    }
     SelArgs sa;
     sa.r = r->scores;
+    sa.sigma = r->sigma;
     sa.rec = b->rec;
+    sa.rows = rows;
     sa.NQ = r->NQ; sa.NK = r->NK; sa.W = r->W; sa.H = r->H;
     sa.H_total = r->cfg.H_total; sa.head_offset = r->cfg.head_offset;
     sa.beta = r->cfg.beta;
@@ -388,11 +377,16 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     sa.key1 = (uint32_t)(seed >> 32);
     sa.step = (uint32_t)step;
     sa.idx = r->idx; sa.count = r->count; sa.mask = r->mask; sa.hdr = r->hdr;
-    select_kernel<<<(unsigned)(r->BH * r->NQ), kSelThreads, 0, st>>>(sa);
-    *launches += 3;
+    const unsigned sg2 = (unsigned)((rows + kSelWarps - 1) / kSelWarps);
+    const int M = (int)((r->NK + 31) / 32);
+    if (M <= 8) select_kernel<8><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
+    else if (M <= 20) select_kernel<20><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
+    else if (M <= 40) select_kernel<40><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
+    else select_kernel<64><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
+    *launches += 1;
     return cudaGetLastError();
 }
 
-int route_max_nk() { return kMaxNK; }
+int route_max_nk() { return 2048; }
 
 }  // namespace pasa
