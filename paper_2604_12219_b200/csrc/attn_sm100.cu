@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __shared__ Ctl ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const bool spin = (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
     const bool tracing = p.trace != nullptr && (int)blockIdx.x == p.trace_x &&
                          (int)blockIdx.y == p.trace_y;
     const int64_t i = blockIdx.x, bh = blockIdx.y;
@@ -119,8 +120,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int nchunks = (int)((NK + 63) / 64);
 
     // ---------------- setup: op list, mask row, barriers, TMEM ----------------
-    for (int w = tid; w < p.W; w += kThreads) ctl.mask[w] = p.mask[row * p.W + w];
-    for (int q = tid; q < cnt; q += kThreads) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
+    for (int w = tid; w < p.W; w += blockDim.x) ctl.mask[w] = p.mask[row * p.W + w];
+    for (int q = tid; q < cnt; q += blockDim.x) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
     if (tid == 0) {
         mbar_init(&ctl.q_full, 1);
         for (int s = 0; s < 2; ++s) {
@@ -196,7 +197,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
-                if (op_type(op) == OP_F) {
+                if (p.dbg & 2) {
+                    mbar_arrive(&ctl.k_full[s]);
+                } else if (op_type(op) == OP_F) {
                     mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
                     tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
                 } else {
@@ -223,7 +226,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
-                if (op_type(op) == OP_F) {
+                if (p.dbg & 2) {
+                    mbar_arrive(&ctl.v_full[s]);
+                } else if (op_type(op) == OP_F) {
                     if (G_::NBOX == 2) {
                         mbar_arrive_expect_tx(&ctl.v_full[s], G_::HTBOX);
                         tma_load_3d(dst, &tmHt, &ctl.v_full[s], 64, v * D, (int)bh);
@@ -260,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         auto issue_qk = [&](int n) {
             const int s = n & 1;
             if (lane == 0) PASA_TR(TR_MMA_QKW, n);
-            mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
+            mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
             tc_fence_after();
             if (lane == 0) {
                 const uint32_t d = tbase + kColS + 64 * s;
@@ -282,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int n = 0; n < nops; ++n) {
             const int s = n & 1;
             if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
-            mbar_wait_sleep(&ctl.v_full[s], (n >> 1) & 1);
+            mbar_wait_c(&ctl.v_full[s], (n >> 1) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_V, n);
-            mbar_wait_sleep(&ctl.p_full[s], (n >> 1) & 1);
+            mbar_wait_c(&ctl.p_full[s], (n >> 1) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_P, n);
             tc_fence_after();
             const int32_t op = ctl.ops[n];
@@ -298,9 +303,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                     mma_commit(&ctl.v_empty[s]);
                     mma_commit(&ctl.pv_done[s]);
+                    PASA_TR(TR_KPROD_W, n);
                 }
             } else {
-                mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
+                mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
                 tc_fence_after();
                 if (lane == 0) {
 #pragma unroll
@@ -347,17 +353,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int32_t op = ctl.ops[n];
             const int type = op_type(op), v = op_val(op);
             const uint32_t t_buf = tbase + lane_off + kColS + 64 * s;
-            if (type != OP_F) {
+            if (type != OP_F && (p.dbg & 1)) {
+                // diagnostics: skip the softmax arithmetic
+                const int par = (s ? sc1 : sc0) & 1;
+                if (s) ++sc1; else ++sc0;
+                mbar_wait_sleep(&ctl.s_full[s], par);
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
+            } else if (type != OP_F) {
                 const int par = (s ? sc1 : sc0) & 1;
                 if (s) ++sc1; else ++sc0;
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_W, n);
-                mbar_wait_sleep(&ctl.s_full[s], par);
+                mbar_wait_c(&ctl.s_full[s], par, spin);
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
                 tmem_ld32(t_buf, sa);
                 tmem_ld32(t_buf + 32, sb);
                 tmem_wait_ld();
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_LD, n);
                 // valid columns and denominator weights
                 uint64_t valid;
                 float wlast = 1.f;     // token count of block n_last (C ops)
@@ -380,13 +393,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                         if (!((valid >> (c + 32)) & 1ull)) sb[c] = 0xff800000u;
                     }
                 }
-                float mr0 = -INFINITY, mr1 = -INFINITY;   // raw row max (scale > 0 commutes)
+                // raw row max (scale > 0 commutes), four independent chains
+                float mr0 = -INFINITY, mr1 = -INFINITY, mr2 = -INFINITY, mr3 = -INFINITY;
 #pragma unroll
-                for (int c = 0; c < 32; c += 2) {
+                for (int c = 0; c < 16; c += 2) {
                     mr0 = fmax3(mr0, __uint_as_float(sa[c]), __uint_as_float(sa[c + 1]));
                     mr1 = fmax3(mr1, __uint_as_float(sb[c]), __uint_as_float(sb[c + 1]));
+                    mr2 = fmax3(mr2, __uint_as_float(sa[c + 16]), __uint_as_float(sa[c + 17]));
+                    mr3 = fmax3(mr3, __uint_as_float(sb[c + 16]), __uint_as_float(sb[c + 17]));
                 }
-                const float mx = fmaxf(mr0, mr1) * cs;
+                const float mx = fmaxf(fmax3(mr0, mr1, mr2), mr3) * cs;
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_MAX, n);
                 // raw logit of the ragged last block (C ops)
                 float xlast = -INFINITY;
                 if (clast >= 0) {
@@ -433,6 +450,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     pk[c] = pack_bf16(p0, p1);
                     pk[16 + c] = pack_bf16(p2, p3);
                 }
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_EXP, n);
                 tmem_st32(t_buf, pk);
                 if (type == OP_E) {
                     l += h0 + h1;
@@ -452,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                 }
                 tmem_wait_st();
+                if (warp == 4 && lane == 0) PASA_TR(TR_SA_ST, n);
             } else {
                 // F(g): write Aq = bf16(s * A_{t,g} * q_t) into the TMEM A buffer
                 // (packed bf16x2 multiply: w is rounded to bf16 once, R-21)

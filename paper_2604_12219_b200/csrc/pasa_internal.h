@@ -79,7 +79,6 @@ cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const 
 cudaError_t launch_attn_sm100_pair(const pasa_tensor& q, const pasa_tensor& k,
                                    const pasa_tensor& v, pasa_route_s* r, const pasa_tensor& out,
                                    cudaStream_t st, int* launches, char* why, size_t why_len);
-
 // tmap.cpp: TMA tensor-map encoding (bf16, 128-byte swizzle, zero OOB fill) and the
 // diagnostics state set by pasa_debug_trace / pasa_debug_flags
 bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,

@@ -64,11 +64,18 @@ def test_kv_stats_kernels_agree(pasa):
     assert np.abs(a - b).max() <= 1e-2 * np.abs(b).max()
 
 
+@pytest.mark.parametrize("variant", ["paired", "prefetch"])
 @pytest.mark.parametrize("S,H,D,G,rho", [(4100, 2, 128, 32, 0.15), (4100, 2, 64, 64, 0.2),
-                                         (20000, 1, 128, 128, 0.15), (1000, 2, 128, 1000, 0.11)])
-def test_paired_variant_parity(pasa, S, H, D, G, rho):
+                                         (20000, 1, 128, 128, 0.15), (1000, 2, 128, 1000, 0.11),
+                                         (9000, 2, 128, 32, 0.05), (9000, 1, 64, 4096, 0.3)])
+def test_variant_parity(pasa, S, H, D, G, rho, variant):
     q, k, v = synth.video_qkv(1, (1, 1, S), H, D, seed=9, dtype=torch.bfloat16, device="cuda")
-    route, out = _run(pasa, q, k, v, G, rho=rho, paired=True)
+    from paper_2604_12219_b200 import _C
+    old = _C.lib().pasa_debug_flags(0)
+    try:
+        route, out = _run(pasa, q, k, v, G, rho=rho, paired=variant == "paired")
+    finally:
+        _C.lib().pasa_debug_flags(old)
     got = route.read()
     ref = oracle.attn_with_route(q, k, v, got["idx"], got["count"], Bq=128, Bk=64, G=G)
     err = np.abs(oracle.f64(out) - ref).max() / np.abs(ref).max()

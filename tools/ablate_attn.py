@@ -21,7 +21,8 @@ z = torch.zeros(64, device="cuda")
 bud(z, z, z, T=50, step=25, rho_table=[cfg["rho"]] * 50)
 route(q, k, bud, 1, 25)
 out = P.attn(q, k, v, route, stats_only=True)
-for paired in (False, True):
+for variant in os.environ.get("VARIANTS", "default,paired").split(","):
+    paired = variant == "paired"
     for flags in [int(f) for f in os.environ.get("FLAGS", "0,1,3").split(",")]:
         _C.lib().pasa_debug_flags(flags)
         for _ in range(2):
@@ -32,5 +33,5 @@ for paired in (False, True):
             P.attn(q, k, v, route, out, reuse_stats=True, paired=paired)
         e1.record()
         torch.cuda.synchronize()
-        print(f"paired={paired} flags={flags} attn {e0.elapsed_time(e1) / 5:.3f} ms", flush=True)
+        print(f"{variant} flags={flags} attn {e0.elapsed_time(e1) / 5:.3f} ms", flush=True)
 _C.lib().pasa_debug_flags(0)

@@ -72,9 +72,35 @@ def main():
         lat.append(mq[u] - kp[u])
     print("K issue -> QK start (median)", float(np.median(lat)))
     ld, mxx, ex, st = col("SA_LD"), col("SA_MAX"), col("SA_EXP"), col("SA_ST")
-    print("middle ops 100..110 A (S-type indices): OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR")
-    for i in range(100, 110):
-        print(i, ld[i] - sa_ok[i], mxx[i] - ld[i], ex[i] - mxx[i], st[i] - ex[i], sa_arr[i] - st[i])
+    if len(ld) > 110 and len(col("SB_ARR")) == 0:
+        print("v1 ops 100..120: OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR, ARR->W(next)")
+        for i in range(100, 120):
+            print(i, ld[i] - sa_ok[i], mxx[i] - ld[i], ex[i] - mxx[i], st[i] - ex[i], sa_arr[i] - st[i],
+                  sa_w[i + 1] - sa_arr[i])
+    elif len(ld) > 110:
+        print("middle ops 100..110 A (S-type indices): OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR")
+        for i in range(100, 110):
+            print(i, ld[i] - sa_ok[i], mxx[i] - ld[i], ex[i] - mxx[i], st[i] - ex[i], sa_arr[i] - st[i])
+    # single-tile kernels: per op n, the MMA warp's view
+    if len(col("SB_ARR")) == 0 and len(mp) > 120:
+        print("op: OK-W(s_full wait) ARR-OK(softmax busy) P-ARR(p_full notice) "
+              "QK(n+1)-QKW(n+1)(k wait) V-QK? period")
+        for u in range(100, 120):
+            print(u, sa_ok[u] - sa_w[u], sa_arr[u] - sa_ok[u], mp[u] - sa_arr[u],
+                  (mq[u + 1] - mqw[u + 1]) if u + 1 < len(mq) else -1, mv[u] - mp[u] if u < len(mv) else -1,
+                  sa_arr[u + 1] - sa_arr[u])
+        per = np.diff(sa_arr[50:-50])
+        print("median period", float(np.median(per)), "mean", float(np.mean(per)))
+        pv = col("KPROD_W")
+        if len(pv) > 120:
+            print("MMA warp per op: QKW->QK(n+1) | QK(n+1)->V(n) | V->P(n) | P->PVdone(n) | PVdone->QKW(n+2)")
+            for u in range(100, 120):
+                print(u, mq[u + 1] - mqw[u + 1], mv[u] - mq[u + 1], mp[u] - mv[u], pv[u] - mp[u],
+                      mqw[u + 2] - pv[u])
+        k = min(len(sa_ok), len(sa_w)) - 50
+        print("median softmax busy", float(np.median(sa_arr[50:k] - sa_ok[50:k])),
+              "median s_full wait", float(np.median(sa_ok[50:k] - sa_w[50:k])),
+              "median p_full notice", float(np.median(mp[50:k] - sa_arr[50:k])))
     print("middle window ops 100..110 A: W OK ARR")
     for i in range(100, 110):
         print(i, sa_w[i] if i < len(sa_w) else -1, sa_ok[i] if i < len(sa_ok) else -1,
