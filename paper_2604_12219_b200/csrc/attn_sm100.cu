@@ -81,7 +81,7 @@ enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK,
        TR_SA_ST, TR_NEV };
 #define PASA_TR(ev, ix)                                                               \
     do {                                                                              \
-        if (tracing && (ix) < kTraceN) p.trace[(ev) * kTraceN + (ix)] = clock64();    \
+        if (DIAG && tracing && (ix) < kTraceN) p.trace[(ev) * kTraceN + (ix)] = clock64(); \
     } while (0)
 
 struct Ctl {
@@ -94,7 +94,9 @@ struct Ctl {
     int32_t ops[kMaxOps];
 };
 
-template <int D>
+// DIAG: diagnostics build (trace points, ablation flags, polling waits); the
+// production instantiation compiles all of it out
+template <int D, bool DIAG>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __shared__ Ctl ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool spin = (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
+    const bool spin = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
     const bool tracing = p.trace != nullptr && (int)blockIdx.x == p.trace_x &&
                          (int)blockIdx.y == p.trace_y;
     const int64_t i = blockIdx.x, bh = blockIdx.y;
@@ -197,7 +199,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
-                if (p.dbg & 2) {
+                if (DIAG && (p.dbg & 2)) {
                     mbar_arrive(&ctl.k_full[s]);
                 } else if (op_type(op) == OP_F) {
                     mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
-                if (p.dbg & 2) {
+                if (DIAG && (p.dbg & 2)) {
                     mbar_arrive(&ctl.v_full[s]);
                 } else if (op_type(op) == OP_F) {
                     if (G_::NBOX == 2) {
@@ -353,7 +355,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int32_t op = ctl.ops[n];
             const int type = op_type(op), v = op_val(op);
             const uint32_t t_buf = tbase + lane_off + kColS + 64 * s;
-            if (type != OP_F && (p.dbg & 1)) {
+            if (DIAG && type != OP_F && (p.dbg & 1)) {
                 // diagnostics: skip the softmax arithmetic
                 const int par = (s ? sc1 : sc0) & 1;
                 if (s) ++sc1; else ++sc0;
@@ -574,7 +576,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     // request >= 100 KB so at most two CTAs share an SM (2 x 256 TMEM columns)
     size_t smem = (size_t)Geo<D>::BYTES + 1024;
     if (smem < 100 * 1024) smem = 100 * 1024;
-    auto kern = attn_sm100_kernel<D>;
+    const bool diag = g_dbg != 0 || g_trace_buf != nullptr;
+    auto kern = diag ? attn_sm100_kernel<D, true> : attn_sm100_kernel<D, false>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)r->NQ, (unsigned)r->BH);
