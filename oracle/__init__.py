@@ -61,7 +61,8 @@ def lib():
         L.orc_density_to_k.argtypes = [D, I64]
         L.orc_density_to_k.restype = I64
         L.orc_route.argtypes = [P, P, I64, I64, I64, I64, I32, I32, D, U64, I32, I64, I64, I64,
-                                P, P, P]
+                                P, P, P, P, D]
+        L.orc_heterogeneity.argtypes = [P, P, I64, I64, I32, I32, I32, P]
         L.orc_block_means.argtypes = [P, I64, I64, I32, P]
         L.orc_block_stats.argtypes = [P, P, I64, I64, I32, I32, P, P, P, P]
         L.orc_attn_with_route.argtypes = [P, P, P, I64, I64, I64, I32, I32, I32, I32, P, P, I64, P]
@@ -155,9 +156,10 @@ def block_means(x_head, Bsz: int) -> np.ndarray:
 
 
 def route(q, k, *, Bq=64, Bk=64, beta=0.1, seed=42, step=25, H_total=None, head_offset=0,
-          rho_t=None, kk=None, want_scores=False):
+          rho_t=None, kk=None, want_scores=False, het=None, eps=1e-6):
     """q, k: [B, S, H, D] (torch or numpy).  Returns dict(idx [B*H, N_Q, kk] int32,
-    mask [B*H, N_Q, W] uint32, kk, scores?)."""
+    mask [B*H, N_Q, W] uint32, kk, scores?).  het: optional [B*H, N_K] norms of
+    Eq. 8's prior (see heterogeneity); r_ij += log(het_j + eps)."""
     qa, ka = f64(q), f64(k)
     B, S, H, D = qa.shape
     qh, kh = heads(qa), heads(ka)
@@ -171,11 +173,38 @@ def route(q, k, *, Bq=64, Bk=64, beta=0.1, seed=42, step=25, H_total=None, head_
     scores = np.zeros((B * H, NQ, NK)) if want_scores else None
     lib().orc_route(_ptr(qh), _ptr(kh), B, H, S, D, Bq, Bk, beta, seed, step,
                     H if H_total is None else H_total, head_offset, kk, _ptr(idx), _ptr(mask),
-                    None if scores is None else _ptr(scores))
+                    None if scores is None else _ptr(scores), _het_ptr(het, B * H, NK), eps)
     out = dict(idx=idx, mask=mask, kk=kk)
     if want_scores:
         out["scores"] = scores
     return out
+
+
+_HET_KEEP = []
+
+
+def _het_ptr(het, BH, NK):
+    if het is None:
+        return None
+    h = np.ascontiguousarray(np.asarray(het, dtype=np.float64))
+    if h.shape != (BH, NK):
+        raise ValueError(f"het must be [{BH}, {NK}], got {h.shape}")
+    _HET_KEEP[:] = [h]
+    return _ptr(h)
+
+
+PRIOR = {"global": 1, "group": 2}
+
+
+def heterogeneity(k_head, v_head, *, Bk=64, G=32, mode="global"):
+    """Eq. 8 prior statistic for one head ([S, D] each): het[j] = ||H_j - C||_F,
+    C = global Hbar (mode "global") or the group mean Hbar^(g(j)) ("group")."""
+    k, v = f64(k_head), f64(v_head)
+    S, D = k.shape
+    NK = (S + Bk - 1) // Bk
+    het = np.zeros(NK)
+    lib().orc_heterogeneity(_ptr(k), _ptr(v), S, D, Bk, G, PRIOR[mode], _ptr(het))
+    return het
 
 
 def block_stats(k_head, v_head, *, Bk=64, G=32, want_blocks=False):

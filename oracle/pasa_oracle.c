@@ -180,7 +180,8 @@ static int orc_cmp_i32(const void* pa, const void* pb) {
 void orc_route(const double* q, const double* k, int64_t B, int64_t H, int64_t S, int64_t D,
                int32_t Bq, int32_t Bk, double beta, uint64_t seed, int32_t step,
                int64_t H_total, int64_t head_offset, int64_t kk,
-               int32_t* idx, uint32_t* mask, double* scores) {
+               int32_t* idx, uint32_t* mask, double* scores,
+               const double* het, double eps) {
     int64_t NQ = (S + Bq - 1) / Bq, NK = (S + Bk - 1) / Bk, W = (NK + 31) / 32;
     int64_t BH = B * H;
     if (kk > NK) kk = NK;
@@ -203,6 +204,8 @@ void orc_route(const double* q, const double* k, int64_t B, int64_t H, int64_t S
                 double dot = 0.0;
                 for (int64_t a = 0; a < D; ++a) dot = fma(Qbar[i * D + a], Kbar[j * D + a], dot);
                 r[j] = s * dot;
+                /* Eq. 8 prior: + log(||H_j - C||_F + eps) */
+                if (het) r[j] = r[j] + log(het[bh * NK + j] + eps);
             }
             /* R3: row mean and population standard deviation */
             double sum = 0.0;
@@ -276,6 +279,38 @@ void orc_block_stats(const double* k, const double* v, int64_t S, int64_t D,
         for (int64_t e = 0; e < D * D; ++e) Hg[e] = Hg[e] / (double)(j1 - j0);
         free(Hj);
     }
+}
+
+/* ------------------------------------------------------------------------ */
+/* Heterogeneity prior of Eq. 8.                                              */
+/* ------------------------------------------------------------------------ */
+void orc_heterogeneity(const double* k, const double* v, int64_t S, int64_t D, int32_t Bk,
+                       int32_t G, int32_t mode, double* het) {
+    int64_t NK = (S + Bk - 1) / Bk;
+    int64_t NG = (NK + G - 1) / G;
+    double* Kbar = (double*)malloc(sizeof(double) * NK * D);
+    double* Vsum = (double*)malloc(sizeof(double) * NK * D);
+    double* Hblk = (double*)malloc(sizeof(double) * NK * D * D);
+    double* Hgrp = (double*)malloc(sizeof(double) * NG * D * D);
+    double* Hglob = (double*)malloc(sizeof(double) * D * D);
+    orc_block_stats(k, v, S, D, Bk, G, Kbar, Vsum, Hblk, Hgrp);
+    /* Eq. 6: Hbar = (1/N_B) sum_j H_j, blocks in ascending order */
+    for (int64_t e = 0; e < D * D; ++e) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < NK; ++j) acc += Hblk[j * D * D + e];
+        Hglob[e] = acc / (double)NK;
+    }
+    for (int64_t j = 0; j < NK; ++j) {
+        const double* C = mode == 2 ? Hgrp + (j / G) * D * D : Hglob;
+        const double* Hj = Hblk + j * D * D;
+        double acc = 0.0;
+        for (int64_t e = 0; e < D * D; ++e) {
+            double d = Hj[e] - C[e];
+            acc += d * d;
+        }
+        het[j] = sqrt(acc);
+    }
+    free(Kbar); free(Vsum); free(Hblk); free(Hgrp); free(Hglob);
 }
 
 /* ------------------------------------------------------------------------ */

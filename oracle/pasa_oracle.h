@@ -63,7 +63,20 @@ int64_t orc_density_to_k(double rho_t, int64_t n_blocks);
 void orc_route(const double* q, const double* k, int64_t B, int64_t H, int64_t S, int64_t D,
                int32_t Bq, int32_t Bk, double beta, uint64_t seed, int32_t step,
                int64_t H_total, int64_t head_offset, int64_t kk,
-               int32_t* idx, uint32_t* mask, double* scores);
+               int32_t* idx, uint32_t* mask, double* scores,
+               const double* het, double eps);
+/* het (optional, may be NULL): [BH][N_K] heterogeneity norms ||H_j - C||_F of
+ * Eq. 8's prior (orc_heterogeneity); then r_ij = s * dot + log(het_j + eps)
+ * (the softmax of Eq. 8 is rank preserving and dropped, R-8),
+ * and sigma_i is taken over these r_ij. */
+
+/* ---- Eq. 8 heterogeneity prior ---------
+ * For one head: het[j] = ||H_j - C||_F (Frobenius), H_j of Eq. 5,
+ * C = the global mean Hbar of Eq. 6 (mode 1, Eq. 8 literally) or the group
+ * mean Hbar^(g(j)) of App. B (mode 2).  The squared entries are summed row by
+ * row in ascending (a, b) order, then sqrt.  Memory: N_K*D*D doubles. */
+void orc_heterogeneity(const double* k, const double* v, int64_t S, int64_t D, int32_t Bk,
+                       int32_t G, int32_t mode, double* het);
 /* Block means (used by routing and by the statistics). out [N][D]. */
 void orc_block_means(const double* x, int64_t S, int64_t D, int32_t Bsz, double* out);
 
