@@ -48,6 +48,10 @@ def parse():
                          "online: rho_t from the three-phase trajectory at step t")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--prior", default="none", choices=["none", "global", "group"],
+                    help="Eq. 8 heterogeneity prior in routing (SURVEY.md §8f NEXT 1; off in "
+                         "the north-star path)")
     ap.add_argument("--cpu-qblocks", type=int, default=48, help="oracle sample size")
     return ap.parse_args()
 
@@ -248,7 +252,8 @@ def run_pasa(args):
     x_t, x_tm1, x_tm2 = (x.contiguous() for x in tp.latents(t_step))
     lbar = tp.expected_l1_mean()
     rcfg = P.RouteCfg(Bq=cfg["Bq"], Bk=cfg["Bk"], G=cfg["G"], comp="grouped", beta=0.1,
-                      H_total=H, head_offset=off)
+                      H_total=H, head_offset=off, prior=args.prior)
+    use_v = args.prior != "none"
     budget = P.Budget(dev)
     route = P.Route(B, S, Hl, D, rcfg, dev)
     seed = P.layer_seed(42, 0)
@@ -263,7 +268,7 @@ def run_pasa(args):
         launches[0] += P.last_launch_count()
         if ev is not None:
             ev[0].record(stream)
-        route(q, k, budget, seed, t_step)
+        route(q, k, budget, seed, t_step, v=v if use_v else None)
         launches[0] += P.last_launch_count()
         if ev is not None:
             ev[1].record(stream)
@@ -317,6 +322,34 @@ def run_pasa(args):
         t_max = float(tt[0])
         ph = tt[1:].cpu().numpy()
 
+    # ---------------- the same step captured once in a CUDA graph, replayed K times -----
+    graph = None
+    if not args.no_graph:
+        try:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step()
+            g.replay()
+            torch.cuda.synchronize()
+            ga, gb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ga.record()
+            for _ in range(K):
+                g.replay()
+            gb.record()
+            torch.cuda.synchronize()
+            tg = ga.elapsed_time(gb) / K
+            if world > 1:
+                tt = torch.tensor([tg], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                tg = float(tt[0])
+            graph = {"ms_per_step": tg, "value": 4.0 * S * S * D * B * H / (tg * 1e-3) / 1e12,
+                     "unit": UNIT, "note": "budget+route+stats+attn captured once, replayed"}
+        except Exception as exc:  # report, do not hide, a capture failure
+            graph = {"error": f"{type(exc).__name__}: {exc}"[:300]}
+
     # ---------------- e2e through the public API with host buffers --------------
     e2e = None
     if not args.no_e2e:
@@ -333,7 +366,7 @@ def run_pasa(args):
                 d.copy_(hsrc, non_blocking=True)
             budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
                    h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
-            route(dq, dk, budget, seed, t_step)
+            route(dq, dk, budget, seed, t_step, v=dv if use_v else None)
             P.attn(dq, dk, dv, route, out)
             hout.copy_(out, non_blocking=True)
 
@@ -391,7 +424,7 @@ def run_pasa(args):
         "config": {
             "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
             "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
-            "step_t": t_step, "budget": args.budget, "l1": rec["l1"], "alpha": rec["alpha"],
+            "step_t": t_step, "budget": args.budget, "prior": args.prior, "l1": rec["l1"], "alpha": rec["alpha"],
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
@@ -408,6 +441,7 @@ def run_pasa(args):
         "clocks": clk.summary(),
         "gpu_launches": gpu_launches,
         "e2e": e2e,
+        "graph": graph,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)

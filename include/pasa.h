@@ -83,6 +83,12 @@ typedef struct {
 
 typedef enum { PASA_COMP_GROUPED = 0, PASA_COMP_ZEROTH = 1, PASA_COMP_NONE = 2 } pasa_comp;
 
+/* Eq. 8 heterogeneity prior in the routing score (reading R-9,
+ * SURVEY.md §8f NEXT 1): r_ij += log(||H_j - C||_F + eps) with C the global mean
+ * Hbar of Eq. 6 (GLOBAL, Eq. 8 literally) or the group mean Hbar^(g(j)) of
+ * App. B (GROUP).  Needs V at route time: use pasa_route_v. */
+typedef enum { PASA_PRIOR_NONE = 0, PASA_PRIOR_GLOBAL = 1, PASA_PRIOR_GROUP = 2 } pasa_prior;
+
 /* Routing / attention configuration (fixed per route handle). */
 typedef struct {
     int32_t Bq;              /* query block: 64 or 128 (reading R-7)                           */
@@ -92,6 +98,9 @@ typedef struct {
     double beta;             /* bias scale >= 0 (0.1 default; 0 = deterministic top-k, R-10)   */
     int64_t H_total;         /* global head count; Philox is keyed on the global head          */
     int64_t head_offset;     /* this call's buffers hold global heads [off, off + H)           */
+    int32_t prior;           /* pasa_prior (PASA_PRIOR_NONE = the north star's route)          */
+    int32_t _pad;
+    double eps;              /* epsilon of the prior's log (1e-6); > 0 if prior on */
 } pasa_route_cfg;
 
 typedef struct pasa_budget_s* pasa_budget_h;
@@ -149,6 +158,19 @@ pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const 
 pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h budget,
                        uint64_t seed, int32_t step, pasa_route_h route, void* stream);
 
+/* pasa_route with Eq. 8's heterogeneity prior (cfg.prior !=
+ * PASA_PRIOR_NONE): as pasa_route, but before scoring computes per KV block
+ *   H_j = sum_n (K_n - Kbar_j)^T V_n (Eq. 5), het_j = ||H_j - C||_F,
+ * in fp64, and scores r_ij = s * dot(Qbar_i, Kbar_j) + log(het_j + eps); sigma_i
+ * and the bias then follow as in pasa_route.  v: [B,S,H,D] like k.  The workspace
+ * of a prior-enabled handle also holds het, the prior and the fp64 group sums
+ * (pasa_route_workspace_bytes accounts for them).  Errors: as pasa_route, plus
+ * EINVAL if the handle's cfg.prior is NONE.  pasa_route on a prior-enabled
+ * handle returns EINVAL (it has no V). */
+pasa_status pasa_route_v(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                         pasa_budget_h budget, uint64_t seed, int32_t step, pasa_route_h route,
+                         void* stream);
+
 /* pasa_attn -- Eq. 7 with grouped first-order
  * compensation (App. B :494-506), readings R-1..R-5, R-21,
  * R-22:
@@ -203,6 +225,9 @@ pasa_status pasa_attn_stats_read(pasa_route_h route, void* kbar, void* vsum, voi
                                  void* stream);
 /* Geometry of a handle: dims[0..6] = {B, S, H, D, N_Q, N_K, N_G}. */
 pasa_status pasa_route_dims(pasa_route_h route, int64_t dims[7]);
+/* Synchronous: het [B*H][N_K] fp64 = ||H_j - C||_F of the last pasa_route_v
+ * (HOST buffer).  EINVAL if the handle has no prior or it was never computed. */
+pasa_status pasa_route_het_read(pasa_route_h route, double* het, void* stream);
 /* Diagnostics: make the next tensor-core attention launches record a clock64()
  * timeline of CTA (x, y) into dev_buf (DEVICE, 13 x 4096 uint64: producer, MMA
  * and softmax events per op); NULL disables.  Returns the element count. */

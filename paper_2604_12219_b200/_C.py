@@ -22,6 +22,7 @@ COMP = {"grouped": 0, "zeroth": 1, "none": 2}
 PASA_ATTN_FORCE_SIMT = 1
 PASA_ATTN_STATS_ONLY = 2
 PASA_ATTN_REUSE_STATS = 4
+PRIOR = {"none": 0, "global": 1, "group": 2}
 PASA_ATTN_PAIRED = 8
 
 # every symbol include/pasa.h declares (tests check the library exports them all)
@@ -31,6 +32,7 @@ EXPORTS = [
     "pasa_attn", "pasa_attn_ex", "pasa_layer_seed", "pasa_budget_read", "pasa_route_read",
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
     "pasa_version", "pasa_debug_trace", "pasa_debug_flags", "pasa_attn_stats_read",
+    "pasa_route_v", "pasa_route_het_read",
 ]
 
 
@@ -57,7 +59,8 @@ class PasaSchedule(ctypes.Structure):
 class PasaRouteCfg(ctypes.Structure):
     _fields_ = [("Bq", ctypes.c_int32), ("Bk", ctypes.c_int32), ("G", ctypes.c_int32),
                 ("comp", ctypes.c_int32), ("beta", ctypes.c_double),
-                ("H_total", ctypes.c_int64), ("head_offset", ctypes.c_int64)]
+                ("H_total", ctypes.c_int64), ("head_offset", ctypes.c_int64),
+                ("prior", ctypes.c_int32), ("_pad", ctypes.c_int32), ("eps", ctypes.c_double)]
 
 
 class PasaError(RuntimeError):
@@ -95,6 +98,8 @@ def lib():
     L.pasa_route_fini.restype = None
     L.pasa_budget.argtypes = [LT, LT, LT, ctypes.POINTER(PasaSchedule), P, P]
     L.pasa_route.argtypes = [T, T, P, U64, I32, P, P]
+    L.pasa_route_v.argtypes = [T, T, T, P, U64, I32, P, P]
+    L.pasa_route_het_read.argtypes = [P, P, P]
     L.pasa_attn.argtypes = [T, T, T, P, T, P]
     L.pasa_attn_ex.argtypes = [T, T, T, P, T, ctypes.c_uint32, P]
     L.pasa_layer_seed.argtypes = [U64, I32]

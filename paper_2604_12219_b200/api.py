@@ -110,10 +110,13 @@ class RouteCfg:
     beta: float = 0.1
     H_total: Optional[int] = None
     head_offset: int = 0
+    prior: str = "none"          # Eq. 8 heterogeneity prior: "none" | "global" | "group"
+    eps: float = 1e-6
 
     def to_c(self, H: int) -> _C.PasaRouteCfg:
         return _C.PasaRouteCfg(self.Bq, self.Bk, self.G, _C.COMP[self.comp], self.beta,
-                               self.H_total if self.H_total is not None else H, self.head_offset)
+                               self.H_total if self.H_total is not None else H, self.head_offset,
+                               _C.PRIOR[self.prior], 0, self.eps)
 
 
 class Route:
@@ -147,11 +150,26 @@ class Route:
         except Exception:  # pragma: no cover
             pass
 
-    def __call__(self, q, k, budget: Budget, seed: int, step: int, stream=None):
+    def __call__(self, q, k, budget: Budget, seed: int, step: int, v=None, stream=None):
+        """pasa_route, or pasa_route_v when v is given (Eq. 8 prior enabled in cfg)."""
         qd, kd = tensor_desc(q), tensor_desc(k)
-        _C.check(_C.lib().pasa_route(ctypes.byref(qd), ctypes.byref(kd), budget.handle, seed,
-                                     step, self.handle, _stream_ptr(stream)), "pasa_route")
+        if v is None:
+            _C.check(_C.lib().pasa_route(ctypes.byref(qd), ctypes.byref(kd), budget.handle, seed,
+                                         step, self.handle, _stream_ptr(stream)), "pasa_route")
+        else:
+            vd = tensor_desc(v)
+            _C.check(_C.lib().pasa_route_v(ctypes.byref(qd), ctypes.byref(kd), ctypes.byref(vd),
+                                           budget.handle, seed, step, self.handle,
+                                           _stream_ptr(stream)), "pasa_route_v")
         return self
+
+    def het(self, stream=None) -> np.ndarray:
+        """||H_j - C||_F of the last pasa_route_v: float64 [B*H, N_K]."""
+        B, S, H, D = self.shape
+        out = np.zeros((B * H, self.NK))
+        _C.check(_C.lib().pasa_route_het_read(self.handle, ctypes.c_void_p(out.ctypes.data),
+                                              _stream_ptr(stream)), "pasa_route_het_read")
+        return out
 
     def read(self, stream=None) -> dict:
         B, S, H, D = self.shape

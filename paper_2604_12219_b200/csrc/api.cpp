@@ -38,7 +38,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
     size_t off_hdr, off_qbar, off_kbar, off_scores, off_sigma, off_kbar_lp, off_vsum, off_ht, off_idx,
-        off_count, off_mask, total;
+        off_count, off_mask, off_het, off_prior, off_hgs, off_hglob, total;
 };
 
 pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int64_t D) {
@@ -55,6 +55,10 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
     if (c->head_offset < 0 || c->H_total < c->head_offset + H)
         return fail(PASA_EINVAL, "head_offset=%lld H=%lld exceed H_total=%lld",
                     (long long)c->head_offset, (long long)H, (long long)c->H_total);
+    if (c->prior < PASA_PRIOR_NONE || c->prior > PASA_PRIOR_GROUP)
+        return fail(PASA_EINVAL, "prior=%d", c->prior);
+    if (c->prior != PASA_PRIOR_NONE && !(c->eps > 0.0 && std::isfinite(c->eps)))
+        return fail(PASA_EINVAL, "prior eps must be finite and > 0");
     const int64_t NK = (S + c->Bk - 1) / c->Bk;
     if (NK > 2048) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 2048 (S too long)", (long long)NK);
     return PASA_OK;
@@ -79,6 +83,11 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_idx = o;      o = align_up(o + sizeof(int32_t) * L.BH * L.NQ * L.NK);
     L.off_count = o;    o = align_up(o + sizeof(int32_t) * L.BH * L.NQ);
     L.off_mask = o;     o = align_up(o + sizeof(uint32_t) * L.BH * L.NQ * L.W);
+    const bool pr = c->prior != PASA_PRIOR_NONE;   // Eq. 8 prior buffers (fp64)
+    L.off_het = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
+    L.off_prior = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
+    L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NG * D * D : 0));
+    L.off_hglob = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * D * D : 0));
     L.total = o;
     return L;
 }
@@ -172,6 +181,12 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->idx = reinterpret_cast<int32_t*>(w + L.off_idx);
     r->count = reinterpret_cast<int32_t*>(w + L.off_count);
     r->mask = reinterpret_cast<uint32_t*>(w + L.off_mask);
+    const bool pr = cfg->prior != PASA_PRIOR_NONE;
+    r->het = pr ? reinterpret_cast<double*>(w + L.off_het) : nullptr;
+    r->prior = pr ? reinterpret_cast<double*>(w + L.off_prior) : nullptr;
+    r->hgs = pr ? reinterpret_cast<double*>(w + L.off_hgs) : nullptr;
+    r->hglob = pr ? reinterpret_cast<double*>(w + L.off_hglob) : nullptr;
+    r->het_valid = 0;
     r->route_dtype = -1;
     r->stats_dtype = -1;
     *out = r;
@@ -217,8 +232,10 @@ pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const 
     return cuda_status(e, "pasa_budget launch");
 }
 
-pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h budget,
-                       uint64_t seed, int32_t step, pasa_route_h route, void* stream) {
+namespace {
+pasa_status route_common(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                         pasa_budget_h budget, uint64_t seed, int32_t step, pasa_route_h route,
+                         void* stream) {
     g_launches = 0;
     if (!route || !budget) return fail(PASA_EINVAL, "NULL handle");
     pasa_status st;
@@ -227,15 +244,38 @@ pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h
     if (q->dtype != k->dtype) return fail(PASA_EDTYPE, "q and k dtypes differ");
     if ((st = match_route(q, route, "q")) != PASA_OK) return st;
     if ((st = match_route(k, route, "k")) != PASA_OK) return st;
+    if (v) {
+        if ((st = check_tensor(v, "v")) != PASA_OK) return st;
+        if (v->dtype != k->dtype) return fail(PASA_EDTYPE, "v and k dtypes differ");
+        if ((st = match_route(v, route, "v")) != PASA_OK) return st;
+    }
     int launches = 0;
-    cudaError_t e = pasa::launch_route(*q, *k, budget, seed, step, route, (cudaStream_t)stream,
+    cudaError_t e = pasa::launch_route(*q, *k, v, budget, seed, step, route, (cudaStream_t)stream,
                                        &launches);
     g_launches = launches;
     if (e == cudaSuccess) {
         route->route_dtype = q->dtype;
         route->stats_dtype = -1;   // Kbar changed: the next pasa_attn must recompute the stats
+        route->het_valid = v != nullptr;
     }
     return cuda_status(e, "pasa_route launch");
+}
+}  // namespace
+
+pasa_status pasa_route(const pasa_tensor* q, const pasa_tensor* k, pasa_budget_h budget,
+                       uint64_t seed, int32_t step, pasa_route_h route, void* stream) {
+    if (route && route->cfg.prior != PASA_PRIOR_NONE)
+        return fail(PASA_EINVAL, "this route handle has the Eq. 8 prior enabled: use pasa_route_v");
+    return route_common(q, k, nullptr, budget, seed, step, route, stream);
+}
+
+pasa_status pasa_route_v(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
+                         pasa_budget_h budget, uint64_t seed, int32_t step, pasa_route_h route,
+                         void* stream) {
+    if (route && route->cfg.prior == PASA_PRIOR_NONE)
+        return fail(PASA_EINVAL, "pasa_route_v needs a handle with cfg.prior != PASA_PRIOR_NONE");
+    if (!v) return fail(PASA_EINVAL, "v is NULL");
+    return route_common(q, k, v, budget, seed, step, route, stream);
 }
 
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
@@ -349,6 +389,17 @@ pasa_status pasa_attn_stats_read(pasa_route_h r, void* kbar, void* vsum, void* h
         e = cudaMemcpyAsync(ht, r->ht, es * r->BH * r->NG * r->D * r->D, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     return cuda_status(e, "pasa_attn_stats_read");
+}
+
+pasa_status pasa_route_het_read(pasa_route_h r, double* het, void* stream) {
+    if (!r || !het) return fail(PASA_EINVAL, "NULL argument");
+    if (r->cfg.prior == PASA_PRIOR_NONE || !r->het_valid)
+        return fail(PASA_EINVAL, "no heterogeneity prior has been computed on this route");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(het, r->het, sizeof(double) * r->BH * r->NK,
+                                    cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    return cuda_status(e, "pasa_route_het_read");
 }
 
 pasa_status pasa_route_dims(pasa_route_h r, int64_t dims[7]) {

@@ -37,6 +37,11 @@ struct pasa_route_s {
     int32_t* idx;                    // [BH][NQ][NK]
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]
+    double* het;                     // [BH][NK] ||H_j - C||_F (prior-enabled handles only)
+    double* prior;                   // [BH][NK] log(het + eps)
+    double* hgs;                     // [BH][NG][D][D] fp64 group sums / means of H_j
+    double* hglob;                   // [BH][D][D] fp64 global mean Hbar
+    int32_t het_valid;               // a pasa_route_v has filled het
     int32_t route_dtype;             // dtype of the q/k the route was last built from (-1 = none)
     int32_t stats_dtype;             // dtype of the last kv_stats pass (-1 = none)
 };
@@ -49,9 +54,12 @@ cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, in
                           double rho, double l1_mean, double rho_max, int use_table,
                           double table_val, pasa_budget_s* b, cudaStream_t st, int* launches);
 
-cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_budget_s* b,
-                         uint64_t seed, int32_t step, pasa_route_s* r, cudaStream_t st,
-                         int* launches);
+// v != nullptr: Eq. 8 prior (het.cu) between pooling and scoring
+cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
+                         const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
+                         cudaStream_t st, int* launches);
+cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
+                       cudaStream_t st, int* launches);
 
 cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                             cudaStream_t st, int* launches);

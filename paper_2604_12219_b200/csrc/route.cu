@@ -107,6 +107,7 @@ constexpr int kSK = 16;     // D chunk staged in smem
 __global__ void __launch_bounds__(256) scores_kernel(const double* __restrict__ qbar,
                                                      const double* __restrict__ kbar, int64_t NQ,
                                                      int64_t NK, int64_t D, double s,
+                                                     const double* __restrict__ prior,
                                                      double* __restrict__ r) {
     __shared__ double sq[kSK][kST + 1];
     __shared__ double sk[kSK][kST + 1];
@@ -149,7 +150,11 @@ __global__ void __launch_bounds__(256) scores_kernel(const double* __restrict__ 
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             int64_t gj = j0 + tx + 16 * c;
-            if (gj < NK) r[(bh * NQ + gi) * NK + gj] = __dmul_rn(s, acc[a][c]);
+            if (gj < NK) {
+                double x = __dmul_rn(s, acc[a][c]);
+                if (prior) x = __dadd_rn(x, prior[bh * NK + gj]);   // Eq. 8 prior term
+                r[(bh * NQ + gi) * NK + gj] = x;
+            }
         }
     }
 }
@@ -339,9 +344,9 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
 
 }  // namespace
 
-cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_budget_s* b,
-                         uint64_t seed, int32_t step, pasa_route_s* r, cudaStream_t st,
-                         int* launches) {
+cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
+                         const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
+                         cudaStream_t st, int* launches) {
     PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qbar};
     PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, r->kbar};
     int64_t ng = r->D / 8;
@@ -353,10 +358,16 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     else
         pool_kernel<__nv_bfloat16><<<(unsigned)grid, 256, 0, st>>>(qa, ka, q_tasks, total);
 
+    const double* prior = nullptr;
+    if (v) {
+        cudaError_t e = launch_het(k, *v, r, st, launches);
+        if (e != cudaSuccess) return e;
+        prior = r->prior;
+    }
     const double s = 1.0 / sqrt((double)r->D);
     dim3 sg((unsigned)((r->NK + kST - 1) / kST), (unsigned)((r->NQ + kST - 1) / kST),
             (unsigned)r->BH);
-    scores_kernel<<<sg, 256, 0, st>>>(r->qbar, r->kbar, r->NQ, r->NK, r->D, s, r->scores);
+    scores_kernel<<<sg, 256, 0, st>>>(r->qbar, r->kbar, r->NQ, r->NK, r->D, s, prior, r->scores);
     *launches += 2;
 
     const int64_t rows = r->BH * r->NQ;

@@ -70,6 +70,19 @@ def test_route_workspace_validation(L):
     assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 64 * 2049, 4, 128) == 0
 
 
+def test_prior_workspace_validation(L):
+    """Eq. 8 prior (NEXT 1): prior in {0,1,2}, eps > 0; the prior-enabled layout
+    adds het + prior [BH][N_K] and fp64 group sums [BH][N_G][D][D] + Hbar [BH][D][D]."""
+    S, H, D = 4096, 4, 128
+    base = L.pasa_route_workspace_bytes(ctypes.byref(cfg()), 1, S, H, D)
+    withp = L.pasa_route_workspace_bytes(ctypes.byref(cfg(prior=1, eps=1e-6)), 1, S, H, D)
+    NK, NG = S // 64, (S // 64 + 31) // 32
+    assert withp - base >= 8 * (2 * H * NK + H * NG * D * D + H * D * D)
+    for bad in (cfg(prior=3, eps=1e-6), cfg(prior=1, eps=0.0), cfg(prior=2, eps=float("nan"))):
+        assert L.pasa_route_workspace_bytes(ctypes.byref(bad), 1, S, H, D) == 0
+        assert L.pasa_last_error()
+
+
 def test_init_rejects_small_workspace_without_touching_device(L):
     c = cfg()
     n = L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 4096, 4, 128)
