@@ -63,6 +63,8 @@ def lib():
         L.orc_route.argtypes = [P, P, I64, I64, I64, I64, I32, I32, D, U64, I32, I64, I64, I64,
                                 P, P, P, P, D]
         L.orc_heterogeneity.argtypes = [P, P, I64, I64, I32, I32, I32, P]
+        L.orc_calibrate.argtypes = [P, I32, I32, D, D, D, P, P, P, P]
+        L.orc_calibrate.restype = ctypes.c_int
         L.orc_block_means.argtypes = [P, I64, I64, I32, P]
         L.orc_block_stats.argtypes = [P, P, I64, I64, I32, I32, P, P, P, P]
         L.orc_attn_with_route.argtypes = [P, P, P, I64, I64, I64, I32, I32, I32, I32, P, P, I64, P]
@@ -178,6 +180,20 @@ def route(q, k, *, Bq=64, Bk=64, beta=0.1, seed=42, step=25, H_total=None, head_
     if want_scores:
         out["scores"] = scores
     return out
+
+
+def calibrate(curves, *, rho=0.15, dense_frac=0.2, rho_max=1.0):
+    """Offline Eqs. 9-11 from l-curves [N, T] (orc_calibrate).  Returns
+    dict(rho_table, alpha, clipped, l1_mean) or raises ValueError."""
+    c = np.ascontiguousarray(np.atleast_2d(np.asarray(curves, dtype=np.float64)))
+    N, T = c.shape
+    tab, alpha, lbar = np.zeros(T), np.zeros(T), np.zeros(1)
+    clipped = np.zeros(T, dtype=np.int32)
+    rc = lib().orc_calibrate(_ptr(c), N, T, rho, dense_frac, rho_max, _ptr(tab), _ptr(alpha),
+                             _ptr(clipped), _ptr(lbar))
+    if rc != 0:
+        raise ValueError("orc_calibrate rejected the input")
+    return dict(rho_table=tab, alpha=alpha, clipped=clipped.astype(bool), l1_mean=float(lbar[0]))
 
 
 _HET_KEEP = []

@@ -111,6 +111,36 @@ double orc_l1(const double* x_t, const double* x_tm1, const double* x_tm2,
     return n > 0 ? acc / (double)n : 0.0;
 }
 
+int orc_calibrate(const double* curves, int32_t N, int32_t T, double rho, double dense_frac,
+                  double rho_max, double* rho_table, double* alpha, int32_t* clipped,
+                  double* lbar) {
+    if (N < 1 || T < 1) return -1;
+    int32_t D = (int32_t)floor(dense_frac * (double)T + 0.5);
+    int32_t t0 = D > 2 ? D : 2;                     /* first sparse step (R-15) */
+    if (t0 >= T) return -1;
+    double* lavg = (double*)malloc(sizeof(double) * T);
+    for (int32_t t = 0; t < T; ++t) {
+        double acc = 0.0;
+        for (int32_t n = 0; n < N; ++n) acc += curves[(int64_t)n * T + t];
+        lavg[t] = acc / (double)N;                 /* R-19: pointwise mean over trajectories */
+    }
+    double acc = 0.0;
+    for (int32_t t = t0; t < T; ++t) acc += lavg[t];
+    double lb = acc / (double)(T - t0);            /* Eq. 9 */
+    if (!(lb > 0.0) || !isfinite(lb)) { free(lavg); return -1; }
+    for (int32_t t = 0; t < T; ++t) {
+        if (t < t0) { rho_table[t] = 1.0; alpha[t] = 0.0; clipped[t] = 0; continue; }
+        double a = lavg[t] / lb;                   /* Eq. 10 */
+        double r = rho * a;                        /* Eq. 11 */
+        clipped[t] = r > rho_max;
+        rho_table[t] = r > rho_max ? rho_max : r;  /* R-18 */
+        alpha[t] = a;
+    }
+    *lbar = lb;
+    free(lavg);
+    return 0;
+}
+
 int64_t orc_density_to_k(double rho_t, int64_t n_blocks) {
     double kf = floor(rho_t * (double)n_blocks + 0.5);
     int64_t k = (kf > (double)n_blocks) ? n_blocks : (int64_t)kf;

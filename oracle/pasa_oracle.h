@@ -47,6 +47,20 @@ int orc_budget(const double* x_t, const double* x_tm1, const double* x_tm2,
 /* Mean L1 signal l_t alone (step B1 of DESIGN.md §3). */
 double orc_l1(const double* x_t, const double* x_tm1, const double* x_tm2,
               int64_t n, int kind, double h_t, double h_tm1);
+/* Offline calibration, Eqs. 9-11 verbatim (readings R-15,
+ * R-17..R-19).  curves [N][T]: l_t of N trajectories
+ * (entries of dense steps are ignored and may be NaN).
+ *   lavg_t = (sum_n curves[n][t]) / N                  (pointwise mean, R-19)
+ *   T_sparse = { t : t >= floor(dense_frac*T + 0.5) and t >= 2 }     (R-15)
+ *   lbar = (sum_{t in T_sparse} lavg_t) / |T_sparse|    (Eq. 9)
+ *   alpha_t = lavg_t / lbar                             (Eq. 10)
+ *   rho_t = min(rho * alpha_t, rho_max), clipped_t = rho*alpha_t > rho_max (Eq. 11, R-18)
+ *   dense steps: rho_t = 1, alpha_t = 0, clipped_t = 0.
+ * Outputs rho_table[T], alpha[T], clipped[T] (0/1), *lbar.  Returns 0, or -1
+ * on invalid input (N < 1, T < 1, empty T_sparse, lbar <= 0 or not finite). */
+int orc_calibrate(const double* curves, int32_t N, int32_t T, double rho, double dense_frac,
+                  double rho_max, double* rho_table, double* alpha, int32_t* clipped,
+                  double* lbar);
 /* k = clamp(floor(rho_t * n_blocks + 0.5), 1, n_blocks)   (reading R-14) */
 int64_t orc_density_to_k(double rho_t, int64_t n_blocks);
 
