@@ -205,6 +205,24 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 
+/* Offline calibration of the budget table, Eqs. 9-11 verbatim (
+ * readings R-15, R-17..R-19).  HOST pointers; no GPU work.
+ *   l1_curves [N][T]: l_t of N calibration trajectories (e.g. pasa_budget's l1
+ *     of each step, or mean |v_t - v_{t-1}| of dumped noise_pred); entries of
+ *     dense steps are ignored and may be NaN.
+ *   lavg_t = (sum_n l1_curves[n][t]) / N (pointwise mean, R-19);
+ *   T_sparse = { t >= max(floor(dense_frac*T + 0.5), 2) } (R-15);
+ *   l1_mean = mean of lavg over T_sparse (Eq. 9); alpha_t = lavg_t / l1_mean
+ *   (Eq. 10); rho_table[t] = min(rho*alpha_t, rho_max), clipped[t] = 1 if the
+ *   clip applied (Eq. 11, R-18); dense steps: rho_table = 1, alpha = 0.
+ * Outputs rho_table[T], alpha[T], clipped[T] (int32 0/1), *l1_mean; any of
+ * alpha / clipped may be NULL.  Errors: EINVAL (N < 1, T < 1, no sparse step,
+ * rho < 0, rho_max <= 0, non-finite sparse entry), EDEGENERATE (l1_mean <= 0,
+ * SPEC.md:403). */
+pasa_status pasa_calibrate(const double* l1_curves, int32_t N, int32_t T, double rho,
+                           double dense_frac, double rho_max, double* rho_table, double* alpha,
+                           int32_t* clipped, double* l1_mean);
+
 /* SplitMix64 finaliser of seed + (layer+1)*0x9E3779B97F4A7C15 (reading R-11):
  * one independent Philox key per layer. */
 uint64_t pasa_layer_seed(uint64_t seed, int32_t layer);

@@ -3,7 +3,9 @@
 // host and launches nothing on failure; no call allocates device memory.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
+#include <vector>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -129,6 +131,47 @@ uint64_t pasa_layer_seed(uint64_t seed, int32_t layer) {
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
     z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
     return z ^ (z >> 31);
+}
+
+pasa_status pasa_calibrate(const double* l1_curves, int32_t N, int32_t T, double rho,
+                           double dense_frac, double rho_max, double* rho_table, double* alpha,
+                           int32_t* clipped, double* l1_mean) {
+    if (!l1_curves || !rho_table || !l1_mean) return fail(PASA_EINVAL, "NULL argument");
+    if (N < 1 || T < 1) return fail(PASA_EINVAL, "N=%d T=%d", N, T);
+    if (!(rho >= 0.0) || !(rho_max > 0.0) || !(dense_frac >= 0.0))
+        return fail(PASA_EINVAL, "rho / rho_max / dense_frac out of range");
+    const int32_t dense = (int32_t)std::floor(dense_frac * (double)T + 0.5);
+    const int32_t t0 = std::max(dense, 2);                       // R-15
+    if (t0 >= T) return fail(PASA_EINVAL, "no sparse step (T=%d, dense prefix %d)", T, t0);
+    std::vector<double> lavg((size_t)T);
+    for (int32_t t = t0; t < T; ++t) {                           // R-19 pointwise mean
+        double acc = 0.0;
+        for (int32_t n = 0; n < N; ++n) {
+            const double x = l1_curves[(int64_t)n * T + t];
+            if (!std::isfinite(x)) return fail(PASA_EINVAL, "l1_curves[%d][%d] not finite", n, t);
+            acc += x;
+        }
+        lavg[t] = acc / (double)N;
+    }
+    double acc = 0.0;
+    for (int32_t t = t0; t < T; ++t) acc += lavg[t];
+    const double lb = acc / (double)(T - t0);                    // Eq. 9
+    if (!(lb > 0.0)) return fail(PASA_EDEGENERATE, "l1_mean = %g <= 0 (Eq. 10)", lb);
+    for (int32_t t = 0; t < T; ++t) {
+        double a = 0.0, r = 1.0;
+        int32_t c = 0;
+        if (t >= t0) {
+            a = lavg[t] / lb;                                    // Eq. 10
+            const double rp = rho * a;                           // Eq. 11
+            c = rp > rho_max;
+            r = c ? rho_max : rp;                                // R-18
+        }
+        rho_table[t] = r;
+        if (alpha) alpha[t] = a;
+        if (clipped) clipped[t] = c;
+    }
+    *l1_mean = lb;
+    return PASA_OK;
 }
 
 size_t pasa_budget_workspace_bytes(void) {

@@ -115,6 +115,23 @@ class ThreePhase:
             hist = hist[-3:]
         return hist[-1], hist[-2], hist[-3]
 
+    def trajectory(self):
+        """Yields x_0, x_1, ..., x_T in order (the same draws as latents(t))."""
+        g = _gen(self.seed, self.device)
+        x = torch.randn(self.shape, generator=g, device=self.device)
+        vbar = torch.randn(self.shape, generator=g, device=self.device)
+        h = 1.0 / self.T
+        yield x
+        for s in range(self.T):
+            xi = torch.randn(self.shape, generator=g, device=self.device)
+            x = x + h * (vbar + self.amp(s) * xi)
+            yield x
+
+    def expected_l1_offline(self, t: int) -> float:
+        """E|v_t - v_{t-1}| (the paper's offline signal between adjacent steps)."""
+        a1, a2 = self.amp(t), self.amp(t - 1)
+        return math.sqrt(2.0 / math.pi) * math.sqrt(a1 * a1 + a2 * a2)
+
     def expected_l1(self, t: int) -> float:
         """E|v_{t-1} - v_{t-2}| for the online reading R-16 (closed form)."""
         a1, a2 = self.amp(t - 1), self.amp(t - 2)
