@@ -40,7 +40,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
     size_t off_hdr, off_qbar, off_kbar, off_scores, off_sigma, off_kbar_lp, off_vsum, off_ht, off_idx,
-        off_count, off_mask, off_het, off_prior, off_hgs, off_hglob, total;
+        off_count, off_mask, off_het, off_prior, off_hgs, off_hglob, off_part, total;
 };
 
 pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int64_t D) {
@@ -90,6 +90,9 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_prior = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
     L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NG * D * D : 0));
     L.off_hglob = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * D * D : 0));
+    // large groups on the tensor-core statistics kernel: fp32 sums of 32-block chunks
+    const bool big = D == 128 && c->G > 64;
+    L.off_part = o;     o = align_up(o + (big ? sizeof(float) * L.BH * ((L.NK + 31) / 32) * D * D : 0));
     L.total = o;
     return L;
 }
@@ -230,6 +233,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->hgs = pr ? reinterpret_cast<double*>(w + L.off_hgs) : nullptr;
     r->hglob = pr ? reinterpret_cast<double*>(w + L.off_hglob) : nullptr;
     r->het_valid = 0;
+    r->part = (D == 128 && cfg->G > 64) ? reinterpret_cast<float*>(w + L.off_part) : nullptr;
     r->route_dtype = -1;
     r->stats_dtype = -1;
     *out = r;

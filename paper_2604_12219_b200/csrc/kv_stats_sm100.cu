@@ -37,7 +37,10 @@ struct Args {
     __nv_bfloat16* kbar_lp;   // [BH][NK][D]
     __nv_bfloat16* vsum_lp;   // [BH][NK][D]
     __nv_bfloat16* ht;        // [BH][NG][D][D]
+    float* part;              // G > kMaxG: fp32 partial sums [BH][NC][D][D] of 32-block chunks
+    int64_t NC;               // chunks per head (ceil(N_K / 32)) when part != nullptr
 };
+constexpr int kChunkBlocks = 32;
 
 struct Ctl {
     uint64_t full[kStages], empty[kStages], acc_full;
@@ -60,8 +63,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t g = blockIdx.x, bh = blockIdx.y;
     const int64_t b = bh / a.H, h = bh % a.H;
-    const int64_t j0 = g * a.G;
-    const int nb = (int)min((int64_t)a.G, a.NK - j0);   // blocks in this group
+    // one group per CTA (G <= kMaxG), or one 32-block chunk of a large group
+    const int64_t j0 = a.part ? g * kChunkBlocks : g * a.G;
+    const int nb = (int)min(a.part ? (int64_t)kChunkBlocks : (int64_t)a.G, a.NK - j0);
 
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -173,6 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t t_row = tbase + ((uint32_t)((warp & 3) * 32) << 16);
         const float inv = 1.f / (float)nb;
         __nv_bfloat16* out = a.ht + ((bh * a.NG + g) * D + n) * D;
+        float* pout = a.part ? a.part + ((bh * a.NC + g) * D + n) * D : nullptr;
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
             uint32_t raw[32];
@@ -194,6 +199,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     acc[4 * c + 3] = fmaf(-vs, kv.w, acc[4 * c + 3]);
                 }
             }
+            if (pout) {                       // partial sum of the chunk (fp32)
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    reinterpret_cast<float4*>(pout + c0)[q] =
+                        make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+                continue;
+            }
             uint4 pk[4];
             uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
 #pragma unroll
@@ -210,10 +222,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
+// Large groups: H-bar^(g) = (sum of the group's chunk partials, chunks in
+// ascending order) / |G_g|, stored bf16.  Chunks never straddle a group (G is a
+// multiple of 32, or a single group).
+__global__ void __launch_bounds__(256) stats_reduce_kernel(const Args a) {
+    const int64_t g = blockIdx.x, bh = blockIdx.z;
+    const int64_t e = (int64_t)blockIdx.y * 256 + threadIdx.x;      // element of D x D
+    const int64_t c0 = g * a.G / kChunkBlocks;
+    const int64_t jend = min((g + 1) * (int64_t)a.G, a.NK);
+    const int64_t c1 = (jend + kChunkBlocks - 1) / kChunkBlocks;
+    float s = 0.f;
+    for (int64_t c = c0; c < c1; ++c) s += a.part[(bh * a.NC + c) * D * D + e];
+    const float inv = 1.f / (float)(jend - g * a.G);
+    a.ht[(bh * a.NG + g) * D * D + e] = __float2bfloat16_rn(s * inv);
+}
+
 }  // namespace
 
 bool kv_stats_sm100_supported(const pasa_route_s* r) {
-    return r->D == 128 && r->cfg.G <= kMaxG;
+    return r->D == 128 &&
+           (r->cfg.G <= kMaxG || (r->part != nullptr && (r->cfg.G % kChunkBlocks == 0 ||
+                                                         r->cfg.G >= r->NK)));
 }
 
 cudaError_t launch_kv_stats_sm100(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
@@ -233,13 +262,20 @@ cudaError_t launch_kv_stats_sm100(const pasa_tensor& k, const pasa_tensor& v, pa
     a.kbar_lp = reinterpret_cast<__nv_bfloat16*>(r->kbar_lp);
     a.vsum_lp = reinterpret_cast<__nv_bfloat16*>(r->vsum_lp);
     a.ht = reinterpret_cast<__nv_bfloat16*>(r->ht);
+    const bool chunked = r->cfg.G > kMaxG;
+    a.part = chunked ? r->part : nullptr;
+    a.NC = (r->NK + kChunkBlocks - 1) / kChunkBlocks;
     const size_t smem = (size_t)kStages * 2 * kTile + sizeof(Scratch) + 1024;
     cudaError_t e = cudaFuncSetAttribute(kv_stats_sm100_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)r->NG, (unsigned)r->BH);
+    dim3 grid((unsigned)(chunked ? a.NC : r->NG), (unsigned)r->BH);
     kv_stats_sm100_kernel<<<grid, kThreads, smem, st>>>(mK, mV, a);
     *launches += 1;
+    if (chunked) {
+        stats_reduce_kernel<<<dim3((unsigned)r->NG, D * D / 256, (unsigned)r->BH), 256, 0, st>>>(a);
+        *launches += 1;
+    }
     return cudaGetLastError();
 }
 

@@ -34,6 +34,7 @@ struct pasa_route_s {
     void* kbar_lp;                   // [BH][NK][D]   bf16 or fp32 (4 B/elem capacity)
     void* vsum_lp;                   // [BH][NK][D]
     void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)
+    float* part;                     // [BH][ceil(NK/32)][D][D] fp32 chunk sums (D = 128, G > 64)
     int32_t* idx;                    // [BH][NQ][NK]
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]

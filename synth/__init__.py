@@ -81,6 +81,26 @@ def video_qkv(B, grid, H, D, *, seed=7, dtype=torch.bfloat16, device="cpu", n_mo
     return Q.to(dtype), K.to(dtype), V.to(dtype)
 
 
+def correlated_qkv(B, S, H, D, *, strength=1.0, Bk=64, seed=7, dtype=torch.bfloat16,
+                   device="cpu", spread=0.5):
+    """SPEC.md:546 correlated-block generator: keys of KV block j are a shared
+    anchor a_j plus ``spread``*N(0,1) deviations; V rows are ``strength`` times a
+    fixed random linear map of the key deviation plus (1-strength)*N(0,1), so the
+    within-block K-V covariance H_j (Eq. 5) is large; Q rows lean towards their
+    own block's anchor (local attention).  strength in [0, 1]."""
+    g = _gen(seed, device)
+    NK = (S + Bk - 1) // Bk
+    blk = torch.arange(S, device=device) // Bk
+    anchor = torch.randn((B, NK, H, D), generator=g, device=device)
+    dev = spread * torch.randn((B, S, H, D), generator=g, device=device)
+    K = anchor[:, blk] + dev
+    M = torch.randn((H, D, D), generator=g, device=device) / math.sqrt(D)
+    V = strength * torch.einsum("bshd,hde->bshe", dev / spread, M) \
+        + (1.0 - strength) * torch.randn((B, S, H, D), generator=g, device=device)
+    Q = 0.7 * anchor[:, blk] + 0.7 * torch.randn((B, S, H, D), generator=g, device=device)
+    return Q.to(dtype), K.to(dtype), V.to(dtype)
+
+
 @dataclass
 class ThreePhase:
     """v_t = vbar + a_t xi_t, x_{t+1} = x_t + h v_t, h = 1/T, a_t = 3.0 (t < 10),
