@@ -88,7 +88,9 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     const bool pr = c->prior != PASA_PRIOR_NONE;   // Eq. 8 prior buffers (fp64)
     L.off_het = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
     L.off_prior = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
-    L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NG * D * D : 0));
+    const int64_t hcb = pasa::het_chunk_blocks(c->G, L.NK);
+    const int64_t hslots = std::max((L.NK + hcb - 1) / hcb, L.NG);
+    L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * hslots * D * D : 0));
     L.off_hglob = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * D * D : 0));
     // large groups on the tensor-core statistics kernel: fp32 sums of 32-block chunks
     const bool big = D == 128 && c->G > 64;

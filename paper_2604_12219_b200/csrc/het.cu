@@ -9,13 +9,19 @@
 // fp64 on the CUDA cores: the prior feeds the top-k, so it must agree with the
 // fp64 oracle far inside the routing tie tolerance (1e-6 relative);
 // fp32 tensor-core accumulation of 64-term sums would sit at that tolerance.
-// Three launches: group sums of H_j (one CTA per (head, group), all tokens of
-// the group in one accumulator: sum_{j in g} H_j = sum_{n in g} (K_n - Kbar_j(n))^T V_n),
-// the means C (fixed group order, deterministic), then one CTA per (head, block)
-// recomputing H_j and reducing ||H_j - C||_F^2 in a fixed order.
-// Thread layout: D^2/64 threads, each owns a 4-row x 16-column patch of H (fp64
-// registers); 16-token chunks of the centred keys and the values are staged in
-// shared memory as fp64 (column reads are warp broadcasts).
+//
+// Work unit: a chunk of CB consecutive KV blocks (CB divides G, or one group
+// spans everything), one CTA per (chunk, head).  Three launches:
+//   1. het_kernel<SUM>:  chunk sums sum_{j in chunk} H_j (one fp64 accumulator:
+//      sum_{n in chunk} (K_n - Kbar_{j(n)})^T V_n);
+//   2. het_means_kernel: C = (sum over chunks in order) / N_K, and in group mode
+//      the group means (in place, slot g);
+//   3. het_kernel<NORM>: H_j again per block and ||H_j - C||_F^2 reduced in a
+//      fixed order (deterministic).
+// Inside a CTA the K/V rows stream through shared memory in 32-token units:
+// cp.async copies the raw rows of unit u+1 while unit u is converted to fp64
+// (centred keys) and consumed.  D^2/64 threads, each owning a 4-row x 16-column
+// patch of H in fp64 registers; column reads are warp broadcasts.
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -25,139 +31,199 @@
 namespace pasa {
 namespace {
 
-constexpr int kChunk = 16;   // 2 x 16 x 128 fp64 = 32 KB static smem
+constexpr int kUnit = 32;       // tokens per pipeline unit (half a KV block)
 
 struct HetArgs {
     const void* k;
     const void* v;
     int64_t ksB, ksS, ksH, vsB, vsS, vsH;   // element strides
-    int64_t S, H, NK, NG, G;
+    int64_t S, H, NK, NG, G, CB, NC;
     const double* kbar;    // [BH][NK][D] fp64 block means (pool_kernel)
-    double* gsum;          // [BH][NG][D][D] group sums, then (group mode) group means
-    const double* cglob;   // [BH][D][D] global mean (NORM pass, global mode)
+    double* part;          // [BH][max(NC,NG)][D][D] chunk sums, then (group mode) group means
+    double* cglob;         // [BH][D][D] global mean
     int32_t mode;          // PASA_PRIOR_GLOBAL / PASA_PRIOR_GROUP
     double eps;
     double* het;           // [BH][NK]
     double* prior;         // [BH][NK]
 };
 
-__device__ __forceinline__ double ld(const float* p) { return (double)*p; }
-__device__ __forceinline__ double ld(const __nv_bfloat16* p) { return (double)__bfloat162float(*p); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    const int n = valid ? 16 : 0;       // src-size 0: zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ double to_d(float x) { return (double)x; }
+__device__ __forceinline__ double to_d(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
 
 template <typename T, int D, bool NORM>
 __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
     constexpr int NT = D * D / 64;
-    constexpr int RT = D / 4;                // row groups of 4
-    __shared__ __align__(16) double kt[kChunk][D];
-    __shared__ __align__(16) double vt[kChunk][D];
+    constexpr int RT = D / 4;                        // row groups of 4
+    constexpr int ROWB = D * (int)sizeof(T);         // bytes per raw row
+    constexpr int RAWB = kUnit * ROWB;               // bytes per raw unit per tensor
+    extern __shared__ __align__(16) uint8_t smem[];
+    double* kt = reinterpret_cast<double*>(smem);                      // [kUnit][D]
+    double* vt = kt + kUnit * D;                                        // [kUnit][D]
+    uint8_t* raw = reinterpret_cast<uint8_t*>(vt + kUnit * D);         // [2][K|V][RAWB]
     __shared__ double red[NT / 32];
     const int tid = threadIdx.x;
     const int r0 = 4 * (tid % RT), c0 = 16 * (tid / RT);
-    const int64_t bh = blockIdx.y;
+    const int64_t bh = blockIdx.y, chunk = blockIdx.x;
     const int64_t b = bh / a.H, h = bh % a.H;
     const T* K = reinterpret_cast<const T*>(a.k) + b * a.ksB + h * a.ksH;
     const T* V = reinterpret_cast<const T*>(a.v) + b * a.vsB + h * a.vsH;
-    const int64_t j_lo = NORM ? (int64_t)blockIdx.x : (int64_t)blockIdx.x * a.G;
-    const int64_t j_hi = NORM ? j_lo + 1 : min(j_lo + a.G, a.NK);
+    const int64_t j_lo = chunk * a.CB, j_hi = min(j_lo + a.CB, a.NK);
+    const int n_units = (int)(2 * (j_hi - j_lo));
+    const int64_t slots = max(a.NC, a.NG);
+
+    auto issue = [&](int u) {                        // raw rows of unit u -> buffer u & 1
+        const int64_t t0 = j_lo * 64 + (int64_t)u * kUnit;
+        uint8_t* dst = raw + (u & 1) * 2 * RAWB;
+        for (int e = tid; e < 2 * RAWB / 16; e += NT) {
+            const int tens = e / (RAWB / 16), w = e % (RAWB / 16);
+            const int n = w / (ROWB / 16), c16 = w % (ROWB / 16);
+            const int64_t tok = t0 + n;
+            const bool ok = tok < a.S;
+            const T* src = tens ? V + (ok ? tok : 0) * a.vsS : K + (ok ? tok : 0) * a.ksS;
+            cp_async16(dst + tens * RAWB + n * ROWB + c16 * 16,
+                       reinterpret_cast<const uint8_t*>(src) + c16 * 16, ok);
+        }
+        cp_async_commit();
+    };
+
     double acc[4][16];
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
-    for (int64_t j = j_lo; j < j_hi; ++j) {
-        const double* kb = a.kbar + (bh * a.NK + j) * D;
-        const int64_t t0 = j * 64, t1 = min(t0 + 64, a.S);
-        for (int64_t tc = t0; tc < t1; tc += kChunk) {
-            const int n_chunk = (int)min((int64_t)kChunk, t1 - tc);
-            __syncthreads();
-            for (int e = tid; e < kChunk * D; e += NT) {
+    if (n_units > 0) issue(0);
+    for (int u = 0; u < n_units; ++u) {
+        const int64_t j = j_lo + u / 2;
+        const int64_t t0 = j * 64 + (u & 1) * kUnit;
+        const int valid = (int)max((int64_t)0, min((int64_t)kUnit, a.S - t0));
+        cp_async_wait0();
+        __syncthreads();                              // raw(u) landed; kt/vt free
+        {
+            const uint8_t* src = raw + (u & 1) * 2 * RAWB;
+            const double* kb = a.kbar + (bh * a.NK + j) * D;
+            for (int e = tid; e < kUnit * D; e += NT) {
                 const int n = e / D, col = e % D;
                 double kv = 0.0, vv = 0.0;
-                if (n < n_chunk) {
-                    kv = ld(K + (tc + n) * a.ksS + col) - kb[col];   // K_n - Kbar_j in fp64
-                    vv = ld(V + (tc + n) * a.vsS + col);
+                if (n < valid) {                      // ragged tail rows contribute nothing
+                    kv = to_d(reinterpret_cast<const T*>(src)[n * D + col]) - kb[col];
+                    vv = to_d(reinterpret_cast<const T*>(src + RAWB)[n * D + col]);
                 }
-                kt[n][col] = kv;
-                vt[n][col] = vv;
+                kt[n * D + col] = kv;
+                vt[n * D + col] = vv;
             }
-            __syncthreads();
-            for (int n = 0; n < n_chunk; ++n) {
-                const double2 k01 = *reinterpret_cast<const double2*>(&kt[n][r0]);
-                const double2 k23 = *reinterpret_cast<const double2*>(&kt[n][r0 + 2]);
-                const double kr[4] = {k01.x, k01.y, k23.x, k23.y};
-                double vr[16];
+        }
+        __syncthreads();                              // fp64 unit ready; raw(u) consumed
+        if (u + 1 < n_units) issue(u + 1);
+#pragma unroll 4
+        for (int n = 0; n < valid; ++n) {
+            const double2 k01 = *reinterpret_cast<const double2*>(&kt[n * D + r0]);
+            const double2 k23 = *reinterpret_cast<const double2*>(&kt[n * D + r0 + 2]);
+            const double kr[4] = {k01.x, k01.y, k23.x, k23.y};
+            double vr[16];
 #pragma unroll
-                for (int c = 0; c < 16; c += 2) {
-                    const double2 t = *reinterpret_cast<const double2*>(&vt[n][c0 + c]);
-                    vr[c] = t.x;
-                    vr[c + 1] = t.y;
-                }
+            for (int c = 0; c < 16; c += 2) {
+                const double2 t = *reinterpret_cast<const double2*>(&vt[n * D + c0 + c]);
+                vr[c] = t.x;
+                vr[c + 1] = t.y;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int c = 0; c < 16; ++c) acc[i][c] = fma(kr[i], vr[c], acc[i][c]);
+        }
+        if constexpr (NORM) {
+            if (u & 1) {                              // block j complete: ||H_j - C||_F
+                const double* C = a.mode == PASA_PRIOR_GROUP
+                                      ? a.part + (bh * slots + j / a.G) * (int64_t)D * D
+                                      : a.cglob + bh * (int64_t)D * D;
+                double p = 0.0;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) acc[i][c] = fma(kr[i], vr[c], acc[i][c]);
+                    for (int c = 0; c < 16; ++c) {
+                        const double d = acc[i][c] - C[(r0 + i) * D + c0 + c];
+                        p = fma(d, d, p);
+                        acc[i][c] = 0.0;
+                    }
+                // fixed-order reduction: xor tree inside each warp, then warps in order
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+                if ((tid & 31) == 0) red[tid >> 5] = p;
+                __syncthreads();
+                if (tid == 0) {
+                    double tot = 0.0;
+                    for (int w = 0; w < NT / 32; ++w) tot += red[w];
+                    const double hv = sqrt(tot);
+                    a.het[bh * a.NK + j] = hv;
+                    a.prior[bh * a.NK + j] = log(hv + a.eps);
+                }
             }
         }
     }
     if constexpr (!NORM) {
-        double* out = a.gsum + (bh * a.NG + blockIdx.x) * (int64_t)D * D;
+        double* out = a.part + (bh * slots + chunk) * (int64_t)D * D;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int c = 0; c < 16; ++c) out[(r0 + i) * D + c0 + c] = acc[i][c];
-    } else {
-        const double* C = a.mode == PASA_PRIOR_GROUP
-                              ? a.gsum + (bh * a.NG + j_lo / a.G) * (int64_t)D * D
-                              : a.cglob + bh * (int64_t)D * D;
-        double part = 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                const double d = acc[i][c] - C[(r0 + i) * D + c0 + c];
-                part = fma(d, d, part);
-            }
-        // fixed-order reduction: xor tree inside each warp, then warps in order
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if ((tid & 31) == 0) red[tid >> 5] = part;
-        __syncthreads();
-        if (tid == 0) {
-            double tot = 0.0;
-            for (int w = 0; w < NT / 32; ++w) tot += red[w];
-            const double hv = sqrt(tot);
-            a.het[bh * a.NK + j_lo] = hv;
-            a.prior[bh * a.NK + j_lo] = log(hv + a.eps);
-        }
     }
 }
 
-// C: global mean (1/N_K) sum_g gsum_g (groups in ascending order); in group mode
-// the group sums are turned into group means in place (unweighted, App. B).
+// C: global mean (1/N_K) sum_c chunk_c (groups in ascending order, chunks in
+// order inside each group); in group mode the group means (unweighted, App. B)
+// replace slot g (chunk index >= g, and every chunk of groups <= g is read first).
 template <int D>
 __global__ void __launch_bounds__(256) het_means_kernel(HetArgs a) {
     const int64_t bh = blockIdx.y;
     const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (e >= (int64_t)D * D) return;
-    double* gs = a.gsum + bh * a.NG * (int64_t)D * D + e;
-    double s = 0.0;
-    for (int64_t g = 0; g < a.NG; ++g) s += gs[g * (int64_t)D * D];
-    const_cast<double*>(a.cglob)[bh * (int64_t)D * D + e] = s / (double)a.NK;
-    if (a.mode == PASA_PRIOR_GROUP)
-        for (int64_t g = 0; g < a.NG; ++g) {
-            const int64_t cnt = min(a.G, a.NK - g * a.G);
-            gs[g * (int64_t)D * D] = gs[g * (int64_t)D * D] / (double)cnt;
-        }
+    double* p = a.part + bh * max(a.NC, a.NG) * (int64_t)D * D + e;
+    double total = 0.0;
+    for (int64_t g = 0; g < a.NG; ++g) {
+        const int64_t jb = g * a.G, je = min(jb + a.G, a.NK);
+        double s = 0.0;
+        for (int64_t c = jb / a.CB; c < (je + a.CB - 1) / a.CB; ++c) s += p[c * (int64_t)D * D];
+        total += s;
+        if (a.mode == PASA_PRIOR_GROUP) p[g * (int64_t)D * D] = s / (double)(je - jb);
+    }
+    a.cglob[bh * (int64_t)D * D + e] = total / (double)a.NK;
 }
 
 template <typename T, int D>
-void launch_d(const HetArgs& a, int64_t BH, cudaStream_t st) {
-    het_kernel<T, D, false><<<dim3((unsigned)a.NG, (unsigned)BH), D * D / 64, 0, st>>>(a);
+cudaError_t launch_d(const HetArgs& a, int64_t BH, cudaStream_t st) {
+    const size_t smem = (size_t)2 * kUnit * D * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(het_kernel<T, D, false>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return e;
+    if ((e = cudaFuncSetAttribute(het_kernel<T, D, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+        return e;
+    const dim3 grid((unsigned)a.NC, (unsigned)BH);
+    het_kernel<T, D, false><<<grid, D * D / 64, smem, st>>>(a);
     het_means_kernel<D><<<dim3((unsigned)((D * D + 255) / 256), (unsigned)BH), 256, 0, st>>>(a);
-    het_kernel<T, D, true><<<dim3((unsigned)a.NK, (unsigned)BH), D * D / 64, 0, st>>>(a);
+    het_kernel<T, D, true><<<grid, D * D / 64, smem, st>>>(a);
+    return cudaGetLastError();
 }
 
 }  // namespace
+
+// chunk size: the largest divisor of G that is <= 32 (32 when one group spans all)
+int64_t het_chunk_blocks(int64_t G, int64_t NK) {
+    if (G >= NK) return 32;
+    for (int64_t d = 32; d > 1; --d)
+        if (G % d == 0) return d;
+    return 1;
+}
 
 cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                        cudaStream_t st, int* launches) {
@@ -166,17 +232,19 @@ cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s*
     a.ksB = k.sB; a.ksS = k.sS; a.ksH = k.sH;
     a.vsB = v.sB; a.vsS = v.sS; a.vsH = v.sH;
     a.S = r->S; a.H = r->H; a.NK = r->NK; a.NG = r->NG; a.G = r->cfg.G;
-    a.kbar = r->kbar; a.gsum = r->hgs; a.cglob = r->hglob;
+    a.CB = het_chunk_blocks(a.G, a.NK);
+    a.NC = (a.NK + a.CB - 1) / a.CB;
+    a.kbar = r->kbar; a.part = r->hgs; a.cglob = r->hglob;
     a.mode = r->cfg.prior; a.eps = r->cfg.eps;
     a.het = r->het; a.prior = r->prior;
     const bool f32 = k.dtype == PASA_F32;
-    if (r->D == 128) {
-        if (f32) launch_d<float, 128>(a, r->BH, st); else launch_d<__nv_bfloat16, 128>(a, r->BH, st);
-    } else {
-        if (f32) launch_d<float, 64>(a, r->BH, st); else launch_d<__nv_bfloat16, 64>(a, r->BH, st);
-    }
+    cudaError_t e;
+    if (r->D == 128)
+        e = f32 ? launch_d<float, 128>(a, r->BH, st) : launch_d<__nv_bfloat16, 128>(a, r->BH, st);
+    else
+        e = f32 ? launch_d<float, 64>(a, r->BH, st) : launch_d<__nv_bfloat16, 64>(a, r->BH, st);
     *launches += 3;
-    return cudaGetLastError();
+    return e;
 }
 
 }  // namespace pasa

@@ -61,6 +61,8 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
                          cudaStream_t st, int* launches);
 cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                        cudaStream_t st, int* launches);
+// KV blocks per work chunk of the prior kernels (a divisor of G, <= 32)
+int64_t het_chunk_blocks(int64_t G, int64_t NK);
 
 cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                             cudaStream_t st, int* launches);

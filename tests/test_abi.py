@@ -77,7 +77,7 @@ def test_prior_workspace_validation(L):
     base = L.pasa_route_workspace_bytes(ctypes.byref(cfg()), 1, S, H, D)
     withp = L.pasa_route_workspace_bytes(ctypes.byref(cfg(prior=1, eps=1e-6)), 1, S, H, D)
     NK, NG = S // 64, (S // 64 + 31) // 32
-    assert withp - base >= 8 * (2 * H * NK + H * NG * D * D + H * D * D)
+    assert withp - base >= 8 * (2 * H * NK + H * NG * D * D + H * D * D)   # at least
     for bad in (cfg(prior=3, eps=1e-6), cfg(prior=1, eps=0.0), cfg(prior=2, eps=float("nan"))):
         assert L.pasa_route_workspace_bytes(ctypes.byref(bad), 1, S, H, D) == 0
         assert L.pasa_last_error()
