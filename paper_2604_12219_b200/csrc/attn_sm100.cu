@@ -334,21 +334,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
         int64_t g_cur = -1, g_done = -1;
-        // pv_done[b] completes once per op on buffer b (ops b, b+2, ...); seen* = last op whose
-        // completion was consumed.  Before releasing P of op n, op n-2 is consumed, so a
-        // buffer's barrier is never two phases ahead of its consumer.
-        int seen0 = -2, seen1 = -1;
         int sc0 = 0, sc1 = 0;      // S-type ops seen per buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
         const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
+        // pv_done[b] completes once per op on buffer b (ops b, b+2, ...): op m's completion
+        // is phase m >> 1 of pv_done[m & 1].  The warps only ever wait for the LATEST op
+        // issued on a buffer (the PV of op n cannot start before this warpgroup releases
+        // P(n)), so the barrier is never two phases ahead of the awaited one and the parity
+        // test is exact without observing every phase.  Nothing waits per op: S(n) is
+        // written by QK(n), issued after PV(n-2), and tcgen05 ops execute in issue order.
         auto consume_op = [&](int op) {   // wait until the O-MMA of op `op` has completed
             if (op < 0) return;
-            if (op & 1) {
-                while (seen1 < op) { seen1 += 2; mbar_wait_sleep(&ctl.pv_done[1], (seen1 >> 1) & 1); }
-            } else {
-                while (seen0 < op) { seen0 += 2; mbar_wait_sleep(&ctl.pv_done[0], (seen0 >> 1) & 1); }
-            }
+            mbar_wait_sleep(&ctl.pv_done[op & 1], (op >> 1) & 1);
         };
         for (int n = 0; n < nops; ++n) {
             const int s = n & 1;
@@ -496,7 +494,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 tmem_wait_st();
             }
-            consume_op(n - 2);
             tc_fence_before();
             mbar_arrive(&ctl.p_full[s]);
             if (warp == 4 && lane == 0) PASA_TR(TR_SA_ARR, n);

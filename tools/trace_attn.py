@@ -65,12 +65,11 @@ def main():
     print("MMA: p_full-ok times first 16:", mp[:16].tolist())
     print("MMA: v_full-ok minus p_full-ok (median)", float(np.median(mv - mp[:len(mv)])))
     print("MMA: QK k_full wait (median/mean)", float(np.median(mq - mqw)), float(np.mean(mq - mqw)))
-    print("Kprod: issue minus wait start (median/mean)", float(np.median(kp - kpw)),
-          float(np.mean(kp - kpw)))
-    lat = []
-    for u in range(min(len(kp), len(mq))):
-        lat.append(mq[u] - kp[u])
-    print("K issue -> QK start (median)", float(np.median(lat)))
+    if len(kp) and len(kp) == len(kpw):
+        print("Kprod: issue minus wait start (median/mean)", float(np.median(kp - kpw)),
+              float(np.mean(kp - kpw)))
+        lat = [mq[u] - kp[u] for u in range(min(len(kp), len(mq)))]
+        print("K issue -> QK start (median)", float(np.median(lat)))
     ld, mxx, ex, st = col("SA_LD"), col("SA_MAX"), col("SA_EXP"), col("SA_ST")
     if len(ld) > 110 and len(col("SB_ARR")) == 0:
         print("v1 ops 100..120: OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR, ARR->W(next)")
