@@ -86,7 +86,7 @@ enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK,
 
 struct Ctl {
     uint64_t q_full;
-    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t k_full[2], k_empty[2];
     uint64_t s_full[2], p_full[2], pv_done[2];   // pv_done[b]: the O-MMA of an op on buffer b done
     uint32_t tmem_base;
     int32_t nops;
@@ -129,10 +129,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int s = 0; s < 2; ++s) {
             mbar_init(&ctl.k_full[s], 1);
             mbar_init(&ctl.k_empty[s], 1);
-            mbar_init(&ctl.v_full[s], 1);
-            mbar_init(&ctl.v_empty[s], 1);
             mbar_init(&ctl.s_full[s], 1);
-            mbar_init(&ctl.p_full[s], 128);
+            mbar_init(&ctl.p_full[s], 129);   // 128 softmax threads + the V producer (expect_tx)
         }
         mbar_init(&ctl.pv_done[0], 1);
         mbar_init(&ctl.pv_done[1], 1);
@@ -224,28 +222,28 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) {
             for (int n = 0; n < nops; ++n) {
                 const int s = n & 1;
-                mbar_wait_sleep(&ctl.v_empty[s], ((n >> 1) & 1) ^ 1);
+                mbar_wait_sleep(&ctl.pv_done[s], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
                 if (DIAG && (p.dbg & 2)) {
-                    mbar_arrive(&ctl.v_full[s]);
+                    mbar_arrive(&ctl.p_full[s]);
                 } else if (op_type(op) == OP_F) {
                     if (G_::NBOX == 2) {
-                        mbar_arrive_expect_tx(&ctl.v_full[s], G_::HTBOX);
-                        tma_load_3d(dst, &tmHt, &ctl.v_full[s], 64, v * D, (int)bh);
+                        mbar_arrive_expect_tx(&ctl.p_full[s], G_::HTBOX);
+                        tma_load_3d(dst, &tmHt, &ctl.p_full[s], 64, v * D, (int)bh);
                     } else {
-                        mbar_arrive(&ctl.v_full[s]);
+                        mbar_arrive(&ctl.p_full[s]);
                     }
                 } else {
-                    mbar_arrive_expect_tx(&ctl.v_full[s], G_::SLOT);
+                    mbar_arrive_expect_tx(&ctl.p_full[s], G_::SLOT);
 #pragma unroll
                     for (int a = 0; a < G_::NBOX; ++a) {
                         if (op_type(op) == OP_E)
-                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.v_full[s], 64 * a, v * kBK,
+                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.p_full[s], 64 * a, v * kBK,
                                         (int)h, (int)b);
                         else
-                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.v_full[s], 64 * a, v * 64,
+                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.p_full[s], 64 * a, v * 64,
                                         (int)bh);
                     }
                 }
@@ -289,7 +287,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         for (int n = 0; n < nops; ++n) {
             const int s = n & 1;
             if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
-            mbar_wait_c(&ctl.v_full[s], (n >> 1) & 1, spin);
+            // V(n) lands on p_full[s] too (one wait for "P ready and V loaded")
             if (lane == 0) PASA_TR(TR_MMA_V, n);
             mbar_wait_c(&ctl.p_full[s], (n >> 1) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_P, n);
@@ -303,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, dv0 + offv, kIdPV,
                                (n > 0 || kk > 0) ? 1u : 0u);
                     }
-                    mma_commit(&ctl.v_empty[s]);
+
                     mma_commit(&ctl.pv_done[s]);
                     PASA_TR(TR_KPROD_W, n);
                 }
@@ -319,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdF, 1u);
                     }
                     mma_commit(&ctl.k_empty[s]);
-                    mma_commit(&ctl.v_empty[s]);
+
                     mma_commit(&ctl.pv_done[s]);
                 }
             }
