@@ -266,19 +266,20 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int s = n & 1;
             if (lane == 0) PASA_TR(TR_MMA_QKW, n);
             mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
+            if (lane == 0) PASA_TR(TR_SB_W, n);           // K(n) landed
             tc_fence_after();
-            if (lane == 0) {
-                const uint32_t d = tbase + kColS + 64 * s;
+            // the whole warp runs the issue code with warp-uniform operands; elect.sync
+            // picks the issuing lane (no per-instruction elect loop)
+            const uint32_t d = tbase + kColS + 64 * s;
 #pragma unroll
-                for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
-                    const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
-                    mma_ss(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
-                }
-                mma_commit(&ctl.s_full[s]);
-                mma_commit(&ctl.k_empty[s]);
-                PASA_TR(TR_MMA_QK, n);
+            for (int kk = 0; kk < D / 16; ++kk) {
+                const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
+                const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
+                mma_ss_elect(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
             }
+            mma_commit_elect(&ctl.s_full[s]);
+            mma_commit_elect(&ctl.k_empty[s]);
+            if (lane == 0) PASA_TR(TR_MMA_QK, n);
             __syncwarp();
         };
         mbar_wait_sleep(&ctl.q_full, 0);
@@ -294,32 +295,26 @@ __global__ void __launch_bounds__(kThreads, 2)
             tc_fence_after();
             const int32_t op = ctl.ops[n];
             if (op_type(op) != OP_F) {
-                if (lane == 0) {
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 16; ++kk) {
-                        const uint32_t offv = (s * G_::SLOT + kk * 16 * 128) >> 4;
-                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, dv0 + offv, kIdPV,
-                               (n > 0 || kk > 0) ? 1u : 0u);
-                    }
-
-                    mma_commit(&ctl.pv_done[s]);
-                    PASA_TR(TR_KPROD_W, n);
+                for (int kk = 0; kk < kBK / 16; ++kk) {
+                    const uint32_t offv = (s * G_::SLOT + kk * 16 * 128) >> 4;
+                    mma_ts_elect(tbase, tbase + kColS + 64 * s + kk * 8, dv0 + offv, kIdPV,
+                                 (n > 0 || kk > 0) ? 1u : 0u);
                 }
+                mma_commit_elect(&ctl.pv_done[s]);
+                if (lane == 0) PASA_TR(TR_KPROD_W, n);
             } else {
                 mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
                 tc_fence_after();
-                if (lane == 0) {
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t box = (kk >> 2) == 0 ? k_base + s * G_::SLOT
-                                                            : v_base + s * G_::SLOT;
-                        const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
-                        mma_ts(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdF, 1u);
-                    }
-                    mma_commit(&ctl.k_empty[s]);
-
-                    mma_commit(&ctl.pv_done[s]);
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t box = (kk >> 2) == 0 ? k_base + s * G_::SLOT
+                                                        : v_base + s * G_::SLOT;
+                    const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
+                    mma_ts_elect(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdF, 1u);
                 }
+                mma_commit_elect(&ctl.k_empty[s]);
+                mma_commit_elect(&ctl.pv_done[s]);
             }
             __syncwarp();
         }

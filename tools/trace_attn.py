@@ -90,6 +90,10 @@ def main():
                   sa_arr[u + 1] - sa_arr[u])
         per = np.diff(sa_arr[50:-50])
         print("median period", float(np.median(per)), "mean", float(np.mean(per)))
+        kw = col("SB_W")
+        if len(kw) > 120:
+            print("K(n+1) wait only (QKW -> K landed), median over ops 50..-50:",
+                  float(np.median(kw[50:-50] - mqw[50:len(kw) - 50])))
         pv = col("KPROD_W")
         if len(pv) > 120:
             print("MMA warp per op: QKW->QK(n+1) | QK(n+1)->V(n) | V->P(n) | P->PVdone(n) | PVdone->QKW(n+2)")
