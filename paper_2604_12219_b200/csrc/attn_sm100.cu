@@ -96,7 +96,7 @@ struct Ctl {
 
 // DIAG: diagnostics build (trace points, ablation flags, polling waits); the
 // production instantiation compiles all of it out
-template <int D, bool DIAG>
+template <int D, bool DIAG, int EXP>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -566,8 +566,10 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     // request >= 100 KB so at most two CTAs share an SM (2 x 256 TMEM columns)
     size_t smem = (size_t)Geo<D>::BYTES + 1024;
     if (smem < 100 * 1024) smem = 100 * 1024;
-    const bool diag = g_dbg != 0 || g_trace_buf != nullptr;
-    auto kern = diag ? attn_sm100_kernel<D, true> : attn_sm100_kernel<D, false>;
+    // g_dbg bits 0-5 select the diagnostics instantiation
+    const bool diag = (g_dbg & 63) != 0 || g_trace_buf != nullptr;
+    // (EXP selects A/B experiment variants of the production form; none is active)
+    auto kern = diag ? attn_sm100_kernel<D, true, 0> : attn_sm100_kernel<D, false, 0>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)r->NQ, (unsigned)r->BH);

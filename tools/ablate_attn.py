@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Time the tensor-core attention kernels (default and paired variant) under
-diagnostic ablations (pasa_debug_flags)."""
+diagnostic ablations (pasa_debug_flags).  REPS > 1 interleaves the
+configurations and reports min / median (the pool's clocks drift under power cap)."""
 import os
 import sys
 
@@ -21,7 +22,10 @@ z = torch.zeros(64, device="cuda")
 bud(z, z, z, T=50, step=25, rho_table=[cfg["rho"]] * 50)
 route(q, k, bud, 1, 25)
 out = P.attn(q, k, v, route, stats_only=True)
-for variant in os.environ.get("VARIANTS", "default,paired").split(","):
+REPS = int(os.environ.get("REPS", "1"))
+results = {}
+for rep in range(REPS):
+  for variant in os.environ.get("VARIANTS", "default,paired").split(","):
     paired = variant == "paired"
     for flags in [int(f) for f in os.environ.get("FLAGS", "0,1,3").split(",")]:
         _C.lib().pasa_debug_flags(flags)
@@ -33,5 +37,13 @@ for variant in os.environ.get("VARIANTS", "default,paired").split(","):
             P.attn(q, k, v, route, out, reuse_stats=True, paired=paired)
         e1.record()
         torch.cuda.synchronize()
-        print(f"{variant} flags={flags} attn {e0.elapsed_time(e1) / 5:.3f} ms", flush=True)
+        ms = e0.elapsed_time(e1) / 5
+        results.setdefault((variant, flags), []).append(ms)
+        if REPS == 1:
+            print(f"{variant} flags={flags} attn {ms:.3f} ms", flush=True)
 _C.lib().pasa_debug_flags(0)
+if REPS > 1:   # interleaved repetitions: min and median per configuration
+    import statistics
+    for (variant, flags), v in results.items():
+        print(f"{variant} flags={flags} attn min {min(v):.3f} median {statistics.median(v):.3f} ms "
+              f"over {len(v)}", flush=True)
