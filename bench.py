@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--e2e-chunks", type=int, default=20,
+                    help="head chunks of the host pipeline (copies overlapped with compute); "
+                         "1 = copy everything, compute, copy back")
     ap.add_argument("--prior", default="none", choices=["none", "global", "group"],
                     help="Eq. 8 heterogeneity prior in routing (SURVEY.md §8f NEXT 1; off in "
                          "the north-star path)")
@@ -356,19 +359,29 @@ def run_pasa(args):
         hq = q.cpu().pin_memory(); hk = k.cpu().pin_memory(); hv = v.cpu().pin_memory()
         hx = [x.cpu().pin_memory() for x in (x_t, x_tm1, x_tm2)]
         hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-        dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
         h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
         d2h = hout.numel() * hout.element_size()
+        if args.e2e_chunks > 1:
+            # public API for host-resident tensors: head chunks on copy-in / compute /
+            # copy-out streams (paper_2604_12219_b200.pipeline)
+            from paper_2604_12219_b200.pipeline import HostPipeline
+            pipe = HostPipeline(B, S, Hl, D, rcfg, n_chunks=args.e2e_chunks, device=dev)
 
-        def e2e_step():
-            for d, hsrc in zip((dq, dk, dv, *dx), (hq, hk, hv, *hx)):
-                d.copy_(hsrc, non_blocking=True)
-            budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
-                   h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
-            route(dq, dk, budget, seed, t_step, v=dv if use_v else None)
-            P.attn(dq, dk, dv, route, out)
-            hout.copy_(out, non_blocking=True)
+            def e2e_step():
+                pipe(hq, hk, hv, hout, hx, seed, t_step, v_for_prior=use_v, T=50,
+                     rho=cfg["rho"], l1_mean=lbar, h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
+        else:
+            dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
+
+            def e2e_step():
+                for d, hsrc in zip((dq, dk, dv, *dx), (hq, hk, hv, *hx)):
+                    d.copy_(hsrc, non_blocking=True)
+                budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
+                       h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
+                route(dq, dk, budget, seed, t_step, v=dv if use_v else None)
+                P.attn(dq, dk, dv, route, out)
+                hout.copy_(out, non_blocking=True)
 
         e2e_step()
         torch.cuda.synchronize()
@@ -388,7 +401,8 @@ def run_pasa(args):
             te = float(tt[0])
         e2e = {"value": 4.0 * S * S * D * B * H / (te * 1e-3) / 1e12, "unit": UNIT,
                "ms_per_step": te, "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(d2h * world), "steps": n_e2e}
+               "d2h_bytes_per_step": int(d2h * world), "steps": n_e2e,
+               "head_chunks": args.e2e_chunks}
 
     if rank != 0:
         if world > 1:

@@ -223,6 +223,15 @@ pasa_status pasa_calibrate(const double* l1_curves, int32_t N, int32_t T, double
                            double dense_frac, double rho_max, double* rho_table, double* alpha,
                            int32_t* clipped, double* l1_mean);
 
+/* Host <-> device 2-D copy on `stream` (runtime plumbing for callers that keep
+ * q, k, v or the output in HOST memory): `height` rows of `width` bytes, row
+ * pitches `spitch` / `dpitch` bytes, e.g. a contiguous run of heads of a
+ * [B, S, H, D] tensor (rows = B*S).  kind: 1 = host to device, 2 = device to
+ * host.  Pinned host memory makes the copy asynchronous.  Errors: EINVAL (NULL
+ * pointer, width > pitch, bad kind), ECUDA. */
+pasa_status pasa_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                        size_t height, int32_t kind, void* stream);
+
 /* SplitMix64 finaliser of seed + (layer+1)*0x9E3779B97F4A7C15 (reading R-11):
  * one independent Philox key per layer. */
 uint64_t pasa_layer_seed(uint64_t seed, int32_t layer);

@@ -32,7 +32,7 @@ EXPORTS = [
     "pasa_attn", "pasa_attn_ex", "pasa_layer_seed", "pasa_budget_read", "pasa_route_read",
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
     "pasa_version", "pasa_debug_trace", "pasa_debug_flags", "pasa_attn_stats_read",
-    "pasa_route_v", "pasa_route_het_read", "pasa_calibrate",
+    "pasa_route_v", "pasa_route_het_read", "pasa_calibrate", "pasa_copy2d",
 ]
 
 
@@ -100,6 +100,7 @@ def lib():
     L.pasa_route.argtypes = [T, T, P, U64, I32, P, P]
     L.pasa_route_v.argtypes = [T, T, T, P, U64, I32, P, P]
     L.pasa_route_het_read.argtypes = [P, P, P]
+    L.pasa_copy2d.argtypes = [P, SZ, P, SZ, SZ, SZ, I32, P]
     L.pasa_calibrate.argtypes = [P, I32, I32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                  P, P, P, P]
     L.pasa_attn.argtypes = [T, T, T, P, T, P]

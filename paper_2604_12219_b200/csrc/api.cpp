@@ -179,6 +179,19 @@ pasa_status pasa_calibrate(const double* l1_curves, int32_t N, int32_t T, double
     return PASA_OK;
 }
 
+pasa_status pasa_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width,
+                        size_t height, int32_t kind, void* stream) {
+    if (!dst || !src) return fail(PASA_EINVAL, "NULL pointer");
+    if (width > dpitch || width > spitch) return fail(PASA_EINVAL, "width exceeds a pitch");
+    if (kind != 1 && kind != 2) return fail(PASA_EINVAL, "kind=%d (1 = H2D, 2 = D2H)", kind);
+    if (width == 0 || height == 0) return PASA_OK;
+    const cudaError_t e =
+        cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, height,
+                          kind == 1 ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost,
+                          (cudaStream_t)stream);
+    return cuda_status(e, "pasa_copy2d");
+}
+
 size_t pasa_budget_workspace_bytes(void) {
     return sizeof(pasa::BudgetRec) + sizeof(double) * pasa::kBudgetParts;
 }
