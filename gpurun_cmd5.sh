@@ -1,3 +1,4 @@
 python -c "from paper_2604_12219_b200 import build; build.build()" > gpurun_out/build.log 2>&1
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 1 --steps 5 --warmup 3 --no-cpu > gpurun_out/b_trun.json 2> gpurun_out/b_trun.err; tail -c 400 gpurun_out/b_trun.json; tail -3 gpurun_out/b_trun.err
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29512 bench.py --impl reference --gpus 1 --steps 2 --warmup 0 > gpurun_out/b_tref.json 2> gpurun_out/b_tref.err; tail -c 300 gpurun_out/b_tref.json; tail -3 gpurun_out/b_tref.err
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_prior.py -q -x 2>&1 | tail -2
+timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'select|scores|pool|rowstats' -c 8 --csv --log-file gpurun_out/launches6.csv python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --no-graph > /dev/null 2>&1
+python tools/ncu_summary.py launches gpurun_out/launches6.csv

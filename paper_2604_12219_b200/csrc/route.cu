@@ -310,14 +310,41 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
     }
     const uint64_t diff = kand ^ kor;
     uint64_t T = diff ? (kand & ~((2ull << (63 - __clzll(diff))) - 1ull)) : kand;
-    for (int bpos = diff ? 63 - __clzll(diff) : -1; bpos >= 0; --bpos) {
-        const uint64_t cand = T | (1ull << bpos);
+    const int top = diff ? 63 - __clzll(diff) : -1;
+    // T = the largest value with #{key >= T} >= k, bit by bit from the top differing
+    // bit.  Upper half first with 32-bit compares (key >= T_hi:0 <=> hi >= T_hi), then
+    // the lower half among the keys whose upper half equals T_hi (the others are
+    // counted once: hi > T_hi always, hi < T_hi never).
+    uint32_t T_hi = (uint32_t)(T >> 32);
+    for (int bpos = top; bpos >= 32; --bpos) {
+        const uint32_t cand = T_hi | (1u << (bpos - 32));
         int c = 0;
 #pragma unroll
-        for (int m = 0; m < MAXM; ++m) c += key[m] >= cand;
+        for (int m = 0; m < MAXM; ++m) c += (uint32_t)(key[m] >> 32) >= cand;
         c = __reduce_add_sync(0xffffffffu, c);
-        if (c >= k) T = cand;
+        if (c >= k) T_hi = cand;
     }
+    uint32_t T_lo = top >= 32 ? 0u : (uint32_t)T;
+    if (top >= 0) {
+        int gtc = 0;
+        uint32_t lo[MAXM];
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) {
+            const uint32_t hi = (uint32_t)(key[m] >> 32);
+            gtc += hi > T_hi;
+            lo[m] = hi == T_hi ? (uint32_t)key[m] : 0u;   // 0 never reaches a candidate
+        }
+        gtc = __reduce_add_sync(0xffffffffu, gtc);
+        for (int bpos = min(top, 31); bpos >= 0; --bpos) {
+            const uint32_t cand = T_lo | (1u << bpos);
+            int c = 0;
+#pragma unroll
+            for (int m = 0; m < MAXM; ++m) c += lo[m] >= cand;
+            c = gtc + __reduce_add_sync(0xffffffffu, c);
+            if (c >= k) T_lo = cand;
+        }
+    }
+    T = ((uint64_t)T_hi << 32) | T_lo;
     int gt = 0;
 #pragma unroll
     for (int m = 0; m < MAXM; ++m) gt += key[m] > T;
