@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--schedule", action="store_true",
+                    help="also run the 50-step budget schedule (online budget from the "
+                         "three-phase synthetic trajectory): per-step k_t, ms and their sum")
     ap.add_argument("--e2e-chunks", type=int, default=20,
                     help="head chunks of the host pipeline (copies overlapped with compute); "
                          "1 = copy everything, compute, copy back")
@@ -353,6 +356,37 @@ def run_pasa(args):
         except Exception as exc:  # report, do not hide, a capture failure
             graph = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    # ---------------- 50-step budget schedule (BASELINE config for CogVideoX) -----
+    schedule = None
+    if args.schedule:
+        T = 50
+        xs_hist, ks, mss = [], [], []
+        for t, x in enumerate(tp.trajectory()):
+            if t >= T:
+                break
+            xs_hist = (xs_hist + [x.contiguous()])[-3:]
+            lat = xs_hist if len(xs_hist) == 3 else [xs_hist[-1]] * 3   # t < 2: dense anyway
+            ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            if world > 1:
+                dist.barrier()
+            ea.record(stream)
+            budget(lat[2], lat[1], lat[0], T=T, step=t, rho=cfg["rho"], l1_mean=lbar,
+                   h_t=1 / T, h_tm1=1 / T)
+            route(q, k, budget, seed, t, v=v if use_v else None)
+            P.attn(q, k, v, route, out)
+            eb.record(stream)
+            torch.cuda.synchronize()
+            ms_t = ea.elapsed_time(eb)
+            if world > 1:
+                tt = torch.tensor([ms_t], device=dev, dtype=torch.float64)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                ms_t = float(tt[0])
+            ks.append(route.read()["k"])
+            mss.append(ms_t)
+        schedule = {"T": T, "budget": "online (three-phase synthetic trajectory, R-16)",
+                    "k_t": ks, "ms_t": [round(m, 4) for m in mss], "sum_ms": sum(mss),
+                    "sum_k": sum(ks[10:]), "dense_steps": sum(1 for kk_ in ks if kk_ == route.NK)}
+
     # ---------------- e2e through the public API with host buffers --------------
     e2e = None
     if not args.no_e2e:
@@ -456,6 +490,7 @@ def run_pasa(args):
         "gpu_launches": gpu_launches,
         "e2e": e2e,
         "graph": graph,
+        "schedule": schedule,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
