@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="skip the CUDA-graph replay timing")
+    ap.add_argument("--seq-sharded", default="auto", choices=["auto", "yes", "no"],
+                    help="inputs arrive sequence-sharded [B, S/P, H, D] and go through the "
+                         "Ulysses all-to-all (auto: the HunyuanVideo config, per BASELINE.json)")
     ap.add_argument("--schedule", action="store_true",
                     help="also run the 50-step budget schedule (online budget from the "
                          "three-phase synthetic trajectory): per-step k_t, ms and their sum")
@@ -243,15 +246,29 @@ def run_pasa(args):
     Hl = H // world
     off = rank * Hl
     dev = torch.device("cuda", torch.cuda.current_device())
-    # rank-local heads drawn from a per-global-head seed: same data for any N
+    seq_sharded = (args.seq_sharded == "yes"
+                   or (args.seq_sharded == "auto" and args.config == "hunyuan_720p"))
+    if seq_sharded and S % world:
+        raise SystemExit(f"S = {S} does not split over {world} ranks")
+    # every global head drawn from its own seed: the same data for any N
     qs, ks, vs = [], [], []
-    for h in range(off, off + Hl):
+    heads = range(H) if seq_sharded else range(off, off + Hl)
+    r0, r1 = (rank * S // world, (rank + 1) * S // world) if seq_sharded else (0, S)
+    for h in heads:
         q1, k1, v1 = synth.iid_qkv(B, S, 1, D, seed=1000 + 7919 * h, dtype=torch.bfloat16,
                                    device=dev)
-        qs.append(q1); ks.append(k1); vs.append(v1)
+        qs.append(q1[:, r0:r1]); ks.append(k1[:, r0:r1]); vs.append(v1[:, r0:r1])
     q = torch.cat(qs, 2).contiguous(); k = torch.cat(ks, 2).contiguous()
     v = torch.cat(vs, 2).contiguous()
     del qs, ks, vs
+    if seq_sharded:
+        # sequence-sharded input [B, S/P, H, D]: the step starts with the Ulysses
+        # all-to-all to this rank's heads and ends with the inverse
+        from paper_2604_12219_b200 import dist as pdist
+        q_s, k_s, v_s = q, k, v
+        to_heads = (lambda t: pdist.seq_to_head(t)) if world > 1 else (lambda t: t)
+        to_seq = (lambda t: pdist.head_to_seq(t)) if world > 1 else (lambda t: t)
+        q, k, v = (to_heads(t) for t in (q_s, k_s, v_s))
     out = torch.empty_like(q)
     tp = synth.ThreePhase(shape=cfg["latent"], T=50, seed=7, device=dev)
     t_step = args.step_t
@@ -269,9 +286,12 @@ def run_pasa(args):
     table = [cfg["rho"]] * 50 if args.budget == "table" else None
 
     def step(ev=None):
+        nonlocal q, k, v
         budget(x_t, x_tm1, x_tm2, T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
                h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
         launches[0] += P.last_launch_count()
+        if seq_sharded:
+            q, k, v = (to_heads(t) for t in (q_s, k_s, v_s))
         if ev is not None:
             ev[0].record(stream)
         route(q, k, budget, seed, t_step, v=v if use_v else None)
@@ -284,6 +304,8 @@ def run_pasa(args):
             ev[2].record(stream)
         P.attn(q, k, v, route, out, reuse_stats=True)
         launches[0] += P.last_launch_count()
+        if seq_sharded:
+            to_seq(out)
         if ev is not None:
             ev[3].record(stream)
 
@@ -330,7 +352,7 @@ def run_pasa(args):
 
     # ---------------- the same step captured once in a CUDA graph, replayed K times -----
     graph = None
-    if not args.no_graph:
+    if not args.no_graph and not (seq_sharded and world > 1):   # no NCCL inside a capture
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -390,12 +412,27 @@ def run_pasa(args):
     # ---------------- e2e through the public API with host buffers --------------
     e2e = None
     if not args.no_e2e:
-        hq = q.cpu().pin_memory(); hk = k.cpu().pin_memory(); hv = v.cpu().pin_memory()
+        src = (q_s, k_s, v_s) if seq_sharded else (q, k, v)
+        hq, hk, hv = (t.cpu().pin_memory() for t in src)
         hx = [x.cpu().pin_memory() for x in (x_t, x_tm1, x_tm2)]
-        hout = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        hout = torch.empty(src[0].shape, dtype=out.dtype, pin_memory=True)
         h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
         d2h = hout.numel() * hout.element_size()
-        if args.e2e_chunks > 1:
+        if seq_sharded and world > 1:
+            # host shards -> device -> all-to-all -> PASA -> all-to-all -> host shard
+            dsq, dsk, dsv = (torch.empty_like(t) for t in src)
+            dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
+
+            def e2e_step():
+                for d, hsrc in zip((dsq, dsk, dsv, *dx), (hq, hk, hv, *hx)):
+                    d.copy_(hsrc, non_blocking=True)
+                budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
+                       h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
+                qh, kh, vh = (to_heads(t) for t in (dsq, dsk, dsv))
+                route(qh, kh, budget, seed, t_step, v=vh if use_v else None)
+                P.attn(qh, kh, vh, route, out)
+                hout.copy_(to_seq(out), non_blocking=True)
+        elif args.e2e_chunks > 1:
             # public API for host-resident tensors: head chunks on copy-in / compute /
             # copy-out streams (paper_2604_12219_b200.pipeline)
             from paper_2604_12219_b200.pipeline import HostPipeline
@@ -476,7 +513,9 @@ def run_pasa(args):
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
-            "parallelism": f"head-partition x{world}",
+            "parallelism": (f"sequence-sharded input, Ulysses all-to-all x{world} "
+                            "(ms_layer.budget includes the all-to-all of q, k, v)")
+                           if seq_sharded else f"head-partition x{world}",
         },
         "ms_layer": {"budget": float(ph[0]), "route": float(ph[1]), "kv_stats": float(ph[2]),
                      "attn": float(ph[3])},
