@@ -1,4 +1,7 @@
 #!/usr/bin/env python
+"""Summarise gpurun_out/trace.json of the paired-block variant (PASA_ATTN_PAIRED,
+attn_sm100_pair.cu): per-op phases of the two softmax warpgroups and the two
+MMA issuers."""
 import json, os, sys
 import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
