@@ -223,6 +223,33 @@ def test_attn_parity(pasa, case):
     assert torch.equal(out, out2)
 
 
+EDGE_CASES = [
+    # name, S, D, Bq, rho, dtype: degenerate lengths around the block sizes, k = 1
+    ("S1", 1, 128, 128, 0.15, torch.bfloat16),
+    ("S37", 37, 64, 128, 0.5, torch.bfloat16),
+    ("S64", 64, 128, 128, 0.5, torch.bfloat16),
+    ("S65", 65, 128, 128, 0.5, torch.bfloat16),
+    ("S127", 127, 64, 128, 0.5, torch.bfloat16),
+    ("S129", 129, 128, 128, 0.5, torch.bfloat16),
+    ("S129_bq64", 129, 64, 64, 0.5, torch.bfloat16),
+    ("k1", 3000, 128, 128, 0.001, torch.bfloat16),
+    ("k1_fp32", 3000, 64, 128, 0.001, torch.float32),
+    ("kNK_minus_1", 640, 128, 128, 0.9, torch.bfloat16),
+]
+
+
+@pytest.mark.parametrize("case", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
+def test_attn_edge_cases(pasa, case):
+    """Single partial blocks (S < Bk, S < Bq), one-token sequences, lengths one past a
+    block edge, k = 1 (the floor of R-14) and k = N_K - 1: route bit-exact, output
+    within the tolerance of the dtype."""
+    name, S, D, Bq, rho, dtype = case
+    q, k, v = synth.iid_qkv(1, S, 2, D, seed=S + D, dtype=dtype, device="cuda")
+    cfg = pasa.RouteCfg(Bq=Bq, G=32, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, rho)
+    check_attn(pasa, q, k, v, route, got, cfg)
+
+
 def test_tensor_core_matches_simt_kernel(pasa):
     q, k, v = gen_qkv("video", 1, 4100, 2, 128, torch.bfloat16, seed=21)
     cfg = pasa.RouteCfg(Bq=128, G=32)
