@@ -37,7 +37,6 @@ constexpr int kThreads = 256;
 constexpr int kBQ = 128, kBK = 64;
 constexpr int kMaxOps = 2048 + 32 + 64 + 64;
 constexpr int kTmemCols = 256;
-constexpr int kColS = 128;            // S/P/Aq buffers at TMEM columns 128 and 192
 constexpr float kRescaleThresh = 8.f; // log2 units
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
@@ -45,8 +44,12 @@ __device__ __forceinline__ int32_t op_make(int32_t type, int32_t v) { return (ty
 __device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 24; }
 __device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0xFFFFFF; }
 
+// NB = S/P/Aq buffers in TMEM = K ring slots: 2 at d = 128 (TMEM: O 128 + 2 x 64
+// columns), 3 at d = 64 (O 64 + 3 x 64) -- QK of op n+NB-1 is issued before PV of op n.
 template <int D>
 struct Geo {
+    static constexpr int NB = D == 128 ? 2 : 3;
+    static constexpr uint32_t COLS = D == 128 ? 128 : 64;   // first S buffer column
     static constexpr int NBOX = D / 64;
     static constexpr int QBOX = kBQ * 128;          // bytes per 64-col box of Q
     static constexpr int KVBOX = kBK * 128;         // bytes per 64-col box of a K/V tile
@@ -54,7 +57,7 @@ struct Geo {
     static constexpr int HTBOX = D * 128;           // bytes per 64-col box of Hbar^T
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = kBQ * D * 2;
-    static constexpr int OFF_V = OFF_K + 2 * SLOT;
+    static constexpr int OFF_V = OFF_K + NB * SLOT;
     static constexpr int BYTES = OFF_V + 2 * SLOT;
     static_assert(HTBOX <= SLOT, "an Hbar^T box must fit one ring slot");
 };
@@ -86,8 +89,8 @@ enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK,
 
 struct Ctl {
     uint64_t q_full;
-    uint64_t k_full[2], k_empty[2];
-    uint64_t s_full[2], p_full[2], pv_done[2];   // pv_done[b]: the O-MMA of an op on buffer b done
+    uint64_t k_full[3], k_empty[3], s_full[3];   // per K slot / S buffer (n % NB)
+    uint64_t p_full[2], pv_done[2];              // per op parity (n & 1): P ready + V landed; O-MMA done
     uint32_t tmem_base;
     int32_t nops;
     uint32_t mask[64];
@@ -126,12 +129,13 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int q = tid; q < cnt; q += blockDim.x) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
     if (tid == 0) {
         mbar_init(&ctl.q_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < G_::NB; ++s) {
             mbar_init(&ctl.k_full[s], 1);
             mbar_init(&ctl.k_empty[s], 1);
             mbar_init(&ctl.s_full[s], 1);
-            mbar_init(&ctl.p_full[s], 129);   // 128 softmax threads + the V producer (expect_tx)
         }
+        for (int s = 0; s < 2; ++s)
+            mbar_init(&ctl.p_full[s], 129);   // 128 softmax threads + the V producer (expect_tx)
         mbar_init(&ctl.pv_done[0], 1);
         mbar_init(&ctl.pv_done[1], 1);
         fence_barrier_init();
@@ -192,8 +196,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
                             (int)(i * kBQ), (int)h, (int)b);
             for (int n = 0; n < nops; ++n) {
-                const int s = n & 1;
-                mbar_wait_sleep(&ctl.k_empty[s], ((n >> 1) & 1) ^ 1);
+                const int s = n % G_::NB;
+                mbar_wait_sleep(&ctl.k_empty[s], ((n / G_::NB) & 1) ^ 1);
                 uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
@@ -263,14 +267,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint64_t dk0 = umma_desc_sw128(k_base, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(v_base, G_::KVBOX, 1024);
         auto issue_qk = [&](int n) {
-            const int s = n & 1;
+            const int s = n % G_::NB;
             if (lane == 0) PASA_TR(TR_MMA_QKW, n);
-            mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
+            mbar_wait_c(&ctl.k_full[s], (n / G_::NB) & 1, spin);
             if (lane == 0) PASA_TR(TR_SB_W, n);           // K(n) landed
             tc_fence_after();
             // the whole warp runs the issue code with warp-uniform operands; elect.sync
             // picks the issuing lane (no per-instruction elect loop)
-            const uint32_t d = tbase + kColS + 64 * s;
+            const uint32_t d = tbase + G_::COLS + 64 * s;
 #pragma unroll
             for (int kk = 0; kk < D / 16; ++kk) {
                 const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
@@ -284,10 +288,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         };
         mbar_wait_sleep(&ctl.q_full, 0);
         tc_fence_after();
-        if (nops > 0) issue_qk(0);
+        for (int m = 0; m < G_::NB - 1 && m < nops; ++m)
+            if (op_type(ctl.ops[m]) != OP_F) issue_qk(m);
         for (int n = 0; n < nops; ++n) {
-            const int s = n & 1;
-            if (n + 1 < nops && op_type(ctl.ops[n + 1]) != OP_F) issue_qk(n + 1);
+            const int s = n & 1, sb = n % G_::NB;
+            const int nq = n + G_::NB - 1;   // its buffer was last read by PV(n-1), issued before
+            if (nq < nops && op_type(ctl.ops[nq]) != OP_F) issue_qk(nq);
             // V(n) lands on p_full[s] too (one wait for "P ready and V loaded")
             if (lane == 0) PASA_TR(TR_MMA_V, n);
             mbar_wait_c(&ctl.p_full[s], (n >> 1) & 1, spin);
@@ -298,22 +304,22 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int kk = 0; kk < kBK / 16; ++kk) {
                     const uint32_t offv = (s * G_::SLOT + kk * 16 * 128) >> 4;
-                    mma_ts_elect(tbase, tbase + kColS + 64 * s + kk * 8, dv0 + offv, kIdPV,
+                    mma_ts_elect(tbase, tbase + G_::COLS + 64 * sb + kk * 8, dv0 + offv, kIdPV,
                                  (n > 0 || kk > 0) ? 1u : 0u);
                 }
                 mma_commit_elect(&ctl.pv_done[s]);
                 if (lane == 0) PASA_TR(TR_KPROD_W, n);
             } else {
-                mbar_wait_c(&ctl.k_full[s], (n >> 1) & 1, spin);
+                mbar_wait_c(&ctl.k_full[sb], (n / G_::NB) & 1, spin);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t box = (kk >> 2) == 0 ? k_base + s * G_::SLOT
+                    const uint32_t box = (kk >> 2) == 0 ? k_base + sb * G_::SLOT
                                                         : v_base + s * G_::SLOT;
                     const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
-                    mma_ts_elect(tbase, tbase + kColS + 64 * s + kk * 8, bd, kIdF, 1u);
+                    mma_ts_elect(tbase, tbase + G_::COLS + 64 * sb + kk * 8, bd, kIdF, 1u);
                 }
-                mma_commit_elect(&ctl.k_empty[s]);
+                mma_commit_elect(&ctl.k_empty[sb]);
                 mma_commit_elect(&ctl.pv_done[s]);
             }
             __syncwarp();
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
         int64_t g_cur = -1, g_done = -1;
-        int sc0 = 0, sc1 = 0;      // S-type ops seen per buffer (s_full parity)
+        int sc0 = 0, sc1 = 0, sc2 = 0;   // S-type ops seen per S buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
         const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
@@ -341,22 +347,24 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (op < 0) return;
             mbar_wait_sleep(&ctl.pv_done[op & 1], (op >> 1) & 1);
         };
+        // parity of the next s_full phase of S buffer bi (one phase per S-type op on it)
+        auto s_parity = [&](int bi) {
+            const int c = bi == 0 ? sc0++ : (bi == 1 ? sc1++ : sc2++);
+            return c & 1;
+        };
         for (int n = 0; n < nops; ++n) {
-            const int s = n & 1;
+            const int s = n & 1, bi = n % G_::NB;
             const int32_t op = ctl.ops[n];
             const int type = op_type(op), v = op_val(op);
-            const uint32_t t_buf = tbase + lane_off + kColS + 64 * s;
+            const uint32_t t_buf = tbase + lane_off + G_::COLS + 64 * bi;
             if (DIAG && type != OP_F && (p.dbg & 1)) {
                 // diagnostics: skip the softmax arithmetic
-                const int par = (s ? sc1 : sc0) & 1;
-                if (s) ++sc1; else ++sc0;
-                mbar_wait_sleep(&ctl.s_full[s], par);
+                mbar_wait_sleep(&ctl.s_full[bi], s_parity(bi));
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
             } else if (type != OP_F) {
-                const int par = (s ? sc1 : sc0) & 1;
-                if (s) ++sc1; else ++sc0;
+                const int par = s_parity(bi);
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_W, n);
-                mbar_wait_c(&ctl.s_full[s], par, spin);
+                mbar_wait_c(&ctl.s_full[bi], par, spin);
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
@@ -469,7 +477,9 @@ __global__ void __launch_bounds__(kThreads, 2)
                 // (packed bf16x2 multiply: w is rounded to bf16 once, R-21)
                 const float w = p.s * (v == g_done ? A_done : A_cur);
                 const uint32_t w2 = pack_bf16(w, w);
-                consume_op(n - 2);     // the buffer's previous reader (op n-2) has finished
+                // the buffer's previous reader (op n-NB) has finished: with NB = 2 that is
+                // the latest op of its parity; with NB = 3 wait for op n-1 (covers n-3)
+                consume_op(G_::NB == 2 ? n - 2 : n - 1);
                 tc_fence_after();
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {

@@ -71,9 +71,10 @@ def main():
         lat = [mq[u] - kp[u] for u in range(min(len(kp), len(mq)))]
         print("K issue -> QK start (median)", float(np.median(lat)))
     ld, mxx, ex, st = col("SA_LD"), col("SA_MAX"), col("SA_EXP"), col("SA_ST")
-    if len(ld) > 110 and len(col("SB_ARR")) == 0:
-        print("v1 ops 100..120: OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR, ARR->W(next)")
-        for i in range(100, 120):
+    lo = 100 if len(ld) > 130 else max(0, len(ld) // 3)
+    if len(ld) > lo + 12 and len(col("SB_ARR")) == 0:
+        print(f"v1 ops {lo}..{lo + 12}: OK->LD, LD->MAX, MAX->EXP, EXP->ST, ST->ARR, ARR->W(next)")
+        for i in range(lo, lo + 12):
             print(i, ld[i] - sa_ok[i], mxx[i] - ld[i], ex[i] - mxx[i], st[i] - ex[i], sa_arr[i] - st[i],
                   sa_w[i + 1] - sa_arr[i])
     elif len(ld) > 110:
