@@ -337,12 +337,15 @@ def run_pasa(args):
     t_local = ms_total / K
     # per-kernel durations over the timed region (launch-stream events)
     ph = np.zeros(4)
+    per_step = []
     for it in range(K):
         prev = e_start if it == 0 else evs[it - 1][3]
         ph[0] += prev.elapsed_time(evs[it][0])
         for j in range(1, 4):
             ph[j] += evs[it][j - 1].elapsed_time(evs[it][j])
+        per_step.append(prev.elapsed_time(evs[it][3]))
     ph /= K
+    step_p50, step_p90 = (float(np.percentile(per_step, q)) for q in (50, 90))
     t_max = t_local
     if world > 1:
         tt = torch.tensor([t_local] + ph.tolist(), device=dev, dtype=torch.float64)
@@ -504,7 +507,8 @@ def run_pasa(args):
                "sample": desc}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": t_max, "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": t_max, "ms_per_step_p50": step_p50,
+        "ms_per_step_p90": step_p90, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {
             "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
