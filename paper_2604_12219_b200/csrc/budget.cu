@@ -39,20 +39,23 @@ __device__ __forceinline__ double load1(const T* p, int64_t e) {
     else return (double)__bfloat162float(p[e]);
 }
 
-// |dv| for one element, B1 of DESIGN.md §3: two subtractions and two divisions
-// in IEEE double, exactly the per-element arithmetic of the definition.
-__device__ __forceinline__ double accel(double xt, double x1, double x2, int kind, double ht,
-                                        double h1) {
+// |dv| for one element, B1 of DESIGN.md §3: two subtractions in IEEE double and
+// the two velocity scalings as multiplications by the host-computed reciprocals
+// 1/h (each within 1 ulp of the division; the mean l1 stays within the 1e-12
+// relative tolerance of DESIGN.md §6, and fp64 division would make the kernel
+// ALU-bound instead of HBM-bound).
+__device__ __forceinline__ double accel(double xt, double x1, double x2, int kind, double rht,
+                                        double rh1) {
     if (kind == 1) return fabs(__dsub_rn(xt, x1));
     double a = __dsub_rn(xt, x1);
     double b = __dsub_rn(x1, x2);
-    return fabs(__dsub_rn(__ddiv_rn(a, ht), __ddiv_rn(b, h1)));
+    return fabs(__dsub_rn(__dmul_rn(a, rht), __dmul_rn(b, rh1)));
 }
 
 template <typename T>
 __global__ void __launch_bounds__(kThreads) budget_partial_kernel(
     const T* __restrict__ xt, const T* __restrict__ x1, const T* __restrict__ x2, int64_t n,
-    int kind, double ht, double h1, double* __restrict__ partials) {
+    int kind, double rht, double rh1, double* __restrict__ partials) {
     // chunk of a multiple of 4 elements per CTA (vector loads stay aligned)
     int64_t chunk = ((n + kBudgetParts - 1) / kBudgetParts + 3) & ~int64_t(3);
     int64_t e0 = (int64_t)blockIdx.x * chunk;
@@ -67,11 +70,11 @@ __global__ void __launch_bounds__(kThreads) budget_partial_kernel(
             if (kind == 0) load4<T>(x2, e, c);
             else { c[0] = c[1] = c[2] = c[3] = 0.0; }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc += accel(a[u], b[u], c[u], kind, ht, h1);
+            for (int u = 0; u < 4; ++u) acc += accel(a[u], b[u], c[u], kind, rht, rh1);
         }
         for (int64_t e = e0 + nv + threadIdx.x; e < e1; e += kThreads)
             acc += accel(load1<T>(xt, e), load1<T>(x1, e), kind == 0 ? load1<T>(x2, e) : 0.0,
-                         kind, ht, h1);
+                         kind, rht, rh1);
     }
     // fixed-order reduction: warp shuffle tree, then warp 0 over the warp sums
     __shared__ double warp_sum[kThreads / 32];
@@ -125,12 +128,12 @@ cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, in
                           double table_val, pasa_budget_s* b, cudaStream_t st, int* launches) {
     if (dtype == PASA_F32)
         budget_partial_kernel<float><<<kBudgetParts, kThreads, 0, st>>>(
-            (const float*)xt, (const float*)xtm1, (const float*)xtm2, n, kind, h_t, h_tm1,
-            b->partials);
+            (const float*)xt, (const float*)xtm1, (const float*)xtm2, n, kind, 1.0 / h_t,
+            1.0 / h_tm1, b->partials);
     else
         budget_partial_kernel<__nv_bfloat16><<<kBudgetParts, kThreads, 0, st>>>(
             (const __nv_bfloat16*)xt, (const __nv_bfloat16*)xtm1, (const __nv_bfloat16*)xtm2, n,
-            kind, h_t, h_tm1, b->partials);
+            kind, 1.0 / h_t, 1.0 / h_tm1, b->partials);
     budget_finalize_kernel<<<1, 256, 0, st>>>(b->partials, n, step, dense_steps, rho, l1_mean,
                                               rho_max, use_table, table_val, b->rec);
     *launches += 2;
