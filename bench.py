@@ -500,7 +500,7 @@ def run_pasa(args):
         pass
     value = 4.0 * S * S * D * B * H / (t_max * 1e-3) / 1e12
     cpu = None
-    if not args.no_cpu:
+    if not args.no_cpu and world == 1:   # the oracle baseline: rank 0 at N = 1 only
         cv, secs, desc, _ = oracle_sample(cfg, args.cpu_qblocks)
         import oracle
         cpu = {"value": cv, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
