@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--prior", default="none", choices=["none", "global", "group"],
                     help="Eq. 8 heterogeneity prior in routing (SURVEY.md §8f NEXT 1; off in "
                          "the north-star path)")
-    ap.add_argument("--cpu-qblocks", type=int, default=48, help="oracle sample size")
+    ap.add_argument("--cpu-qblocks", type=int, default=256,
+                    help="oracle sample size (q-blocks of one head; ~10 s of CPU work)")
     return ap.parse_args()
 
 
