@@ -34,7 +34,7 @@ struct pasa_route_s {
     void* kbar_lp;                   // [BH][NK][D]   bf16 or fp32 (4 B/elem capacity)
     void* vsum_lp;                   // [BH][NK][D]
     void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)
-    float* part;                     // [BH][ceil(NK/32)][D][D] fp32 chunk sums (D = 128, G > 64)
+    float* part;                     // [BH][ceil(NK/32)][D][D] fp32 chunk sums (G > 64)
     int32_t* idx;                    // [BH][NQ][NK]
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]
@@ -66,7 +66,7 @@ int64_t het_chunk_blocks(int64_t G, int64_t NK);
 
 cudaError_t launch_kv_stats(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                             cudaStream_t st, int* launches);
-// tensor-core statistics pass (d = 128, bf16, G <= 64); launch_kv_stats dispatches to it
+// tensor-core statistics pass (bf16, d = 128 or 64); launch_kv_stats dispatches to it
 bool kv_stats_sm100_supported(const pasa_route_s* r);
 cudaError_t launch_kv_stats_sm100(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                                   cudaStream_t st, int* launches);

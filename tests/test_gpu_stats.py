@@ -49,15 +49,18 @@ def test_kv_stats_vs_oracle(pasa, S, D, G):
         assert err <= 1e-2, err
 
 
-def test_kv_stats_kernels_agree(pasa):
-    """The tcgen05 statistics kernel and the mma.sync one (diagnostic flag 16) agree."""
+@pytest.mark.parametrize("D,G", [(128, 32), (64, 32), (64, 128), (128, 4096)])
+def test_kv_stats_kernels_agree(pasa, D, G):
+    """The tcgen05 statistics kernel (d = 64 with a zero-padded M = 128 operand; groups
+    of more than 64 blocks in reduced chunks) and the mma.sync one (diagnostic flag
+    16) agree."""
     from paper_2604_12219_b200 import _C
-    q, k, v = synth.iid_qkv(1, 6000, 2, 128, seed=5, dtype=torch.bfloat16, device="cuda")
-    route, _ = _run(pasa, q, k, v, 32)
+    q, k, v = synth.iid_qkv(1, 6000, 2, D, seed=5, dtype=torch.bfloat16, device="cuda")
+    route, _ = _run(pasa, q, k, v, G)
     a = route.stats()[2]
     old = _C.lib().pasa_debug_flags(16)
     try:
-        route2, _ = _run(pasa, q, k, v, 32)
+        route2, _ = _run(pasa, q, k, v, G)
         b = route2.stats()[2]
     finally:
         _C.lib().pasa_debug_flags(old)
