@@ -93,7 +93,7 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * hslots * D * D : 0));
     L.off_hglob = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * D * D : 0));
     // large groups on the tensor-core statistics kernel: fp32 sums of 32-block chunks
-    const bool big = c->G > 64;
+    const bool big = c->G > 32;
     L.off_part = o;     o = align_up(o + (big ? sizeof(float) * L.BH * ((L.NK + 31) / 32) * D * D : 0));
     L.total = o;
     return L;
@@ -248,7 +248,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->hgs = pr ? reinterpret_cast<double*>(w + L.off_hgs) : nullptr;
     r->hglob = pr ? reinterpret_cast<double*>(w + L.off_hglob) : nullptr;
     r->het_valid = 0;
-    r->part = cfg->G > 64 ? reinterpret_cast<float*>(w + L.off_part) : nullptr;
+    r->part = cfg->G > 32 ? reinterpret_cast<float*>(w + L.off_part) : nullptr;
     r->route_dtype = -1;
     r->stats_dtype = -1;
     *out = r;

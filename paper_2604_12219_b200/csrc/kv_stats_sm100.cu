@@ -8,8 +8,9 @@
 // operands MN-major: Ht[n][k] = sum_t V[t][n] K[t][k]); the second (the exact centring
 // correction, rank 1 per block) is accumulated in fp32 on CUDA cores.  Per-block H_j is
 // never materialised.  One CTA per (head, group) -- or per 32-block
-// chunk of a group larger than 64 blocks, reduced afterwards in a fixed order --,
-// 4-stage TMA ring, HBM bound: 2 S d * 2 bytes per head.
+// chunk of a group larger than 32 blocks, reduced afterwards in a fixed order --,
+// 2-stage (d = 128) / 4-stage (d = 64) TMA ring with two CTAs per SM, HBM bound:
+// 2 S d * 2 bytes per head.
 // d = 64: the MMA keeps M = 128 with the A operand's second 64-row half pointed at a
 // zeroed 8 KB region of the stage (rows 64..127 of the accumulator are 0 and unused).
 #include <cuda.h>
@@ -26,9 +27,9 @@ namespace {
 using namespace ptx;
 
 constexpr int kBk = 64;
-constexpr int kStages = 4;
+constexpr int kMaxStages = 4;
 constexpr int kBox = kBk * 128;             // 8 KB: 64 tokens x 64 dims (128-byte rows)
-constexpr int kMaxG = 64;                   // blocks per group handled by one CTA's smem
+constexpr int kMaxG = 32;                   // blocks per group handled by one CTA's smem
 constexpr int kThreads = 256;               // warp 0 TMA, warp 1 MMA, warps 4-7 math
 constexpr int kChunkBlocks = 32;
 
@@ -38,6 +39,8 @@ struct SGeo {
     static constexpr int TILE = kBk * D * 2;            // one K or V block tile
     // stage: K tile | V tile | (d = 64) zero box for the A operand's padded rows
     static constexpr int STAGE = 2 * TILE + (D == 64 ? kBox : 0);
+    // ring depth per CTA: two CTAs per SM (one's epilogue overlaps the other's loads)
+    static constexpr int STAGES = D == 64 ? 4 : 2;
 };
 
 struct Args {
@@ -52,7 +55,7 @@ struct Args {
 };
 
 struct Ctl {
-    uint64_t full[kStages], empty[kStages], acc_full;
+    uint64_t full[kMaxStages], empty[kMaxStages], acc_full;
     uint32_t tmem_base;
 };
 template <int D>
@@ -63,7 +66,7 @@ struct Scratch {              // dynamic smem after the TMA stages
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     kv_stats_sm100_kernel(const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const Args a) {
     using G_ = SGeo<D>;
@@ -72,7 +75,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     __shared__ Ctl ctl;
-    Scratch<D>& sc = *reinterpret_cast<Scratch<D>*>(smem + kStages * G_::STAGE);
+    Scratch<D>& sc = *reinterpret_cast<Scratch<D>*>(smem + G_::STAGES * G_::STAGE);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t g = blockIdx.x, bh = blockIdx.y;
     const int64_t b = bh / a.H, h = bh % a.H;
@@ -81,7 +84,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nb = (int)min(a.part ? (int64_t)kChunkBlocks : (int64_t)a.G, a.NK - j0);
 
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < G_::STAGES; ++s) {
             mbar_init(&ctl.full[s], 1);
             mbar_init(&ctl.empty[s], 2);     // MMA commit + the math warpgroup
         }
@@ -93,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_relinquish();
     }
     if constexpr (D == 64) {                 // the zero boxes (never written by TMA)
-        for (int e = tid; e < kStages * kBox / 16; e += kThreads) {
+        for (int e = tid; e < G_::STAGES * kBox / 16; e += kThreads) {
             const int s = e / (kBox / 16), w = e % (kBox / 16);
             reinterpret_cast<uint4*>(smem + s * G_::STAGE + 2 * G_::TILE)[w] =
                 make_uint4(0u, 0u, 0u, 0u);
@@ -115,8 +118,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             for (int jj = 0; jj < nb; ++jj) {
-                const int s = jj % kStages;
-                mbar_wait_sleep(&ctl.empty[s], ((jj / kStages) & 1) ^ 1);
+                const int s = jj % G_::STAGES;
+                mbar_wait_sleep(&ctl.empty[s], ((jj / G_::STAGES) & 1) ^ 1);
                 uint8_t* st = smem + s * G_::STAGE;
                 mbar_arrive_expect_tx(&ctl.full[s], 2 * G_::TILE);
                 const int tok = (int)((j0 + jj) * kBk);
@@ -135,8 +138,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kId = idesc_bf16_f32(128, D, 1, 1);
         const uint64_t d0 = umma_desc_sw128(smem_u32(smem), kBox, 1024);
         for (int jj = 0; jj < nb; ++jj) {
-            const int s = jj % kStages;
-            mbar_wait_sleep(&ctl.full[s], (jj / kStages) & 1);
+            const int s = jj % G_::STAGES;
+            mbar_wait_sleep(&ctl.full[s], (jj / G_::STAGES) & 1);
             tc_fence_after();
             if (lane == 0) {
 #pragma unroll
@@ -160,8 +163,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int rg = mt / CH;
         const int bx = chunk >> 3, c16 = chunk & 7;
         for (int jj = 0; jj < nb; ++jj) {
-            const int s = jj % kStages;
-            mbar_wait_sleep(&ctl.full[s], (jj / kStages) & 1);
+            const int s = jj % G_::STAGES;
+            mbar_wait_sleep(&ctl.full[s], (jj / G_::STAGES) & 1);
             const uint8_t* vt = smem + s * G_::STAGE + G_::TILE + bx * kBox;
             float acc[8];
 #pragma unroll
@@ -288,7 +291,7 @@ cudaError_t launch_d(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r
     const bool chunked = r->cfg.G > kMaxG;
     a.part = chunked ? r->part : nullptr;
     a.NC = (r->NK + kChunkBlocks - 1) / kChunkBlocks;
-    const size_t smem = (size_t)kStages * SGeo<D>::STAGE + sizeof(Scratch<D>) + 1024;
+    const size_t smem = (size_t)SGeo<D>::STAGES * SGeo<D>::STAGE + sizeof(Scratch<D>) + 1024;
     auto kern = kv_stats_sm100_kernel<D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
