@@ -33,6 +33,16 @@ namespace {
 
 constexpr int kUnit = 32;       // tokens per pipeline unit (half a KV block)
 
+// the NORM pass stages its C in shared memory when it fits next to the token units
+template <typename T, int D>
+constexpr size_t het_smem_units() {
+    return (size_t)2 * kUnit * D * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
+}
+template <typename T, int D>
+constexpr bool het_stage_c() {
+    return het_smem_units<T, D>() + (size_t)D * D * sizeof(double) <= (size_t)227 * 1024;
+}
+
 struct HetArgs {
     const void* k;
     const void* v;
@@ -69,6 +79,7 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
     double* kt = reinterpret_cast<double*>(smem);                      // [kUnit][D]
     double* vt = kt + kUnit * D;                                        // [kUnit][D]
     uint8_t* raw = reinterpret_cast<uint8_t*>(vt + kUnit * D);         // [2][K|V][RAWB]
+    double* cs = reinterpret_cast<double*>(raw + 4 * RAWB);            // NORM: C [D][D]
     __shared__ double red[NT / 32];
     const int tid = threadIdx.x;
     const int r0 = 4 * (tid % RT), c0 = 16 * (tid / RT);
@@ -101,6 +112,15 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
     if (n_units > 0) issue(0);
+    if constexpr (NORM && het_stage_c<T, D>()) {
+        // the chunk's C (one group, or the global mean) staged once: every block of the
+        // chunk reads it from shared memory instead of L2
+        const double* Cg = a.mode == PASA_PRIOR_GROUP
+                               ? a.part + (bh * slots + j_lo / a.G) * (int64_t)D * D
+                               : a.cglob + bh * (int64_t)D * D;
+        for (int e = tid; e < D * D / 2; e += NT)
+            reinterpret_cast<double2*>(cs)[e] = reinterpret_cast<const double2*>(Cg)[e];
+    }
     for (int u = 0; u < n_units; ++u) {
         const int64_t j = j_lo + u / 2;
         const int64_t t0 = j * 64 + (u & 1) * kUnit;
@@ -142,9 +162,12 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
         }
         if constexpr (NORM) {
             if (u & 1) {                              // block j complete: ||H_j - C||_F
-                const double* C = a.mode == PASA_PRIOR_GROUP
-                                      ? a.part + (bh * slots + j / a.G) * (int64_t)D * D
-                                      : a.cglob + bh * (int64_t)D * D;
+                // C staged at CTA start (the chunk lies in one group), else read from L2
+                const double* C = het_stage_c<T, D>()
+                                      ? cs
+                                      : (a.mode == PASA_PRIOR_GROUP
+                                             ? a.part + (bh * slots + j / a.G) * (int64_t)D * D
+                                             : a.cglob + bh * (int64_t)D * D);
                 double p = 0.0;
 #pragma unroll
                 for (int i = 0; i < 4; ++i)
@@ -200,18 +223,19 @@ __global__ void __launch_bounds__(256) het_means_kernel(HetArgs a) {
 
 template <typename T, int D>
 cudaError_t launch_d(const HetArgs& a, int64_t BH, cudaStream_t st) {
-    const size_t smem = (size_t)2 * kUnit * D * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
+    const size_t smem_sum = het_smem_units<T, D>();
+    const size_t smem_norm = smem_sum + (het_stage_c<T, D>() ? (size_t)D * D * sizeof(double) : 0);
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(het_kernel<T, D, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sum)) != cudaSuccess)
         return e;
     if ((e = cudaFuncSetAttribute(het_kernel<T, D, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_norm)) != cudaSuccess)
         return e;
     const dim3 grid((unsigned)a.NC, (unsigned)BH);
-    het_kernel<T, D, false><<<grid, D * D / 64, smem, st>>>(a);
+    het_kernel<T, D, false><<<grid, D * D / 64, smem_sum, st>>>(a);
     het_means_kernel<D><<<dim3((unsigned)((D * D + 255) / 256), (unsigned)BH), 256, 0, st>>>(a);
-    het_kernel<T, D, true><<<grid, D * D / 64, smem, st>>>(a);
+    het_kernel<T, D, true><<<grid, D * D / 64, smem_norm, st>>>(a);
     return cudaGetLastError();
 }
 
