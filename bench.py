@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--seq-sharded", default="auto", choices=["auto", "yes", "no"],
                     help="inputs arrive sequence-sharded [B, S/P, H, D] and go through the "
                          "Ulysses all-to-all (auto: the HunyuanVideo config, per BASELINE.json)")
+    ap.add_argument("--no-dense", action="store_true",
+                    help="skip the dense torch SDPA context timing (speedup vs dense)")
     ap.add_argument("--schedule", action="store_true",
                     help="also run the 50-step budget schedule (online budget from the "
                          "three-phase synthetic trajectory): per-step k_t, ms and their sum")
@@ -382,6 +384,28 @@ def run_pasa(args):
         except Exception as exc:  # report, do not hide, a capture failure
             graph = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    # ---------------- context: dense attention on the same shapes (library SDPA) -----
+    dense = None
+    if not args.no_dense and rank == 0:
+        try:
+            import torch.nn.functional as F
+            qt, kt, vt = (t.transpose(1, 2) for t in (q, k, v))      # [B, H, S, D] views
+            F.scaled_dot_product_attention(qt, kt, vt)
+            torch.cuda.synchronize()
+            da, db = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            da.record()
+            for _ in range(2):
+                F.scaled_dot_product_attention(qt, kt, vt)
+            db.record()
+            torch.cuda.synchronize()
+            td = da.elapsed_time(db) / 2
+            dense = {"what": "torch scaled_dot_product_attention (dense, bf16) on this rank's q, k, v; "
+                             "context only, not a baseline of the method",
+                     "ms": td, "tflops": 4.0 * S * S * D * B * q.shape[2] / (td * 1e-3) / 1e12,
+                     "speedup_vs_dense_attn": td / float(ph[2] + ph[3])}
+        except Exception as exc:  # e.g. out of memory for the dense workspace
+            dense = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # ---------------- 50-step budget schedule (BASELINE config for CogVideoX) -----
     schedule = None
     if args.schedule:
@@ -535,6 +559,7 @@ def run_pasa(args):
         "e2e": e2e,
         "graph": graph,
         "schedule": schedule,
+        "dense_context": dense,
         "cpu_baseline": cpu,
     }
     print(json.dumps(line), flush=True)
