@@ -5,10 +5,10 @@
 // DESIGN.md §3).  Design notes: DESIGN.md §7.
 //
 // One CTA per (head, 128-row query block); 2 CTAs per SM (TMEM 2 x 256 cols,
-// ~97 KB smem each) so one CTA's softmax overlaps the other's MMAs.
+// ~97 KB smem each at d = 128) so one CTA's softmax overlaps the other's MMAs.
 // Warp roles (256 threads):
 //   warp 0  TMA producer of the K ring (K tiles / Kbar chunks / Hbar^T box 0)
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer
+//   warp 1  TMEM allocator + tcgen05.mma issuer (warp-converged, elect.sync)
 //   warp 2  TMA producer of the V ring (V tiles / Vsum chunks / Hbar^T box 1)
 //   warps 4-7  softmax / correction / epilogue, one query row per thread
 // The CTA walks one "op" list:
