@@ -96,6 +96,10 @@ struct Ctl {
     uint32_t mask[64];
     int32_t ops[kMaxOps];
 };
+// EXP 1 (groups of 8 or 16 blocks): the 8-column P sums of the last C op, per row
+struct CtlSG : Ctl {
+    float sg[8][kBQ];
+};
 
 // DIAG: diagnostics build (trace points, ablation flags, polling waits); the
 // production instantiation compiles all of it out
@@ -111,7 +115,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
-    __shared__ Ctl ctl;
+    __shared__ std::conditional_t<EXP == 1, CtlSG, Ctl> ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool spin = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
@@ -333,6 +337,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
         int64_t g_cur = -1, g_done = -1;
+        int c_last = 0;   // G = 8 or 16: chunk of the last C op (ctl.sg holds its group sums)
         int sc0 = 0, sc1 = 0, sc2 = 0;   // S-type ops seen per S buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
@@ -459,6 +464,22 @@ __global__ void __launch_bounds__(kThreads, 2)
                     // denominator: n_j * p_j; every dropped block has 64 tokens except the last
                     const float pl = clast >= 0 ? ex2(fmaf(xlast, cs, negm)) : 0.f;
                     l += 64.f * (h0 + h1) - (64.f - wlast) * pl;
+                    if constexpr (EXP == 1) {
+                        // small groups: 8-column sums of this chunk's P (bf16 as stored;
+                        // the first-order weight is rounded to bf16 anyway, R-21)
+#pragma unroll
+                        for (int k8 = 0; k8 < 8; ++k8) {
+                            float sgk = 0.f;
+#pragma unroll
+                            for (int q2 = 0; q2 < 4; ++q2) {
+                                const float2 f = __bfloat1622float2(
+                                    *reinterpret_cast<const __nv_bfloat162*>(&pk[4 * k8 + q2]));
+                                sgk += f.x + f.y;
+                            }
+                            ctl.sg[k8][r] = sgk;
+                        }
+                        c_last = v;
+                    }
                     // group sums A_{t,g} (each 32-block half lies in one group)
                     const int64_t j0 = 64 * (int64_t)v;
                     const int64_t g0 = j0 / p.G;
@@ -475,7 +496,17 @@ __global__ void __launch_bounds__(kThreads, 2)
             } else {
                 // F(g): write Aq = bf16(s * A_{t,g} * q_t) into the TMEM A buffer
                 // (packed bf16x2 multiply: w is rounded to bf16 once, R-21)
-                const float w = p.s * (v == g_done ? A_done : A_cur);
+                float A = v == g_done ? A_done : A_cur;
+                if constexpr (EXP == 1) {            // group v of the last C op's chunk
+                    const int kg = v - (64 * c_last) / p.G;
+                    A = 0.f;
+#pragma unroll
+                    for (int k8 = 0; k8 < 8; ++k8) {
+                        if (p.G == 8 && kg == k8) A = ctl.sg[k8][r];
+                        if (p.G == 16 && 2 * kg == k8) A = ctl.sg[k8][r] + ctl.sg[k8 + 1][r];
+                    }
+                }
+                const float w = p.s * A;
                 const uint32_t w2 = pack_bf16(w, w);
                 // the buffer's previous reader (op n-NB) has finished: with NB = 2 that is
                 // the latest op of its parity; with NB = 3 wait for op n-1 (covers n-3)
@@ -573,13 +604,17 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     prm.trace_x = g_trace_x;
     prm.trace_y = g_trace_y;
     prm.dbg = g_dbg;
-    // request >= 100 KB so at most two CTAs share an SM (2 x 256 TMEM columns)
+    // request >= 80 KB so at most two CTAs share an SM (2 x 256 TMEM columns; a third
+    // would block in tcgen05.alloc) while two still fit next to the static Ctl
     size_t smem = (size_t)Geo<D>::BYTES + 1024;
-    if (smem < 100 * 1024) smem = 100 * 1024;
+    if (smem < (r->cfg.G < 32 ? 80 : 100) * 1024) smem = (r->cfg.G < 32 ? 80 : 100) * 1024;
     // g_dbg bits 0-5 select the diagnostics instantiation
     const bool diag = (g_dbg & 63) != 0 || g_trace_buf != nullptr;
-    // (EXP selects A/B experiment variants of the production form; none is active)
-    auto kern = diag ? attn_sm100_kernel<D, true, 0> : attn_sm100_kernel<D, false, 0>;
+    const bool small_groups = r->cfg.comp == PASA_COMP_GROUPED && r->cfg.G < 32;
+    // EXP 1: groups of 8 or 16 blocks (per-8-column sums in shared memory); the G >= 32
+    // instantiation carries none of that code
+    auto kern = small_groups ? (diag ? attn_sm100_kernel<D, true, 1> : attn_sm100_kernel<D, false, 1>)
+                             : (diag ? attn_sm100_kernel<D, true, 0> : attn_sm100_kernel<D, false, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)r->NQ, (unsigned)r->BH);
@@ -596,9 +631,9 @@ cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const 
         snprintf(why, why_len, "needs Bq=128, Bk=64");
         return cudaErrorNotSupported;
     }
-    if (r->cfg.comp == PASA_COMP_GROUPED && r->cfg.G % 32 != 0 && r->cfg.G < r->NK) {
-        snprintf(why, why_len, "grouped compensation needs G %% 32 == 0 or G >= N_K (G=%d)",
-                 r->cfg.G);
+    if (r->cfg.comp == PASA_COMP_GROUPED && !sm100_supports_group(r->cfg.G, r->NK)) {
+        snprintf(why, why_len, "grouped compensation with G = %d (supported: 8, 16, 32, 64, "
+                 "multiples of 128, >= N_K)", r->cfg.G);
         return cudaErrorNotSupported;
     }
     if (r->W > 64) {

@@ -75,10 +75,11 @@ cudaError_t launch_attn_simt(const pasa_tensor& q, const pasa_tensor& k, const p
                              pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                              int* launches);
 
-// group sizes the tensor-core kernel's group-sum bookkeeping covers: every 32-block
-// mask word inside one group, and at most two groups per 64-block half-chunk
+// group sizes the tensor-core kernel's group-sum bookkeeping covers: 8 and 16 (per-8-column
+// sums of each 64-block chunk kept in shared memory), or every 32-block mask word inside
+// one group with at most two groups per 64-block chunk
 inline bool sm100_supports_group(int64_t G, int64_t NK) {
-    return G == 32 || G == 64 || G % 128 == 0 || G >= NK;
+    return G == 8 || G == 16 || G == 32 || G == 64 || G % 128 == 0 || G >= NK;
 }
 
 // returns cudaErrorNotSupported if the configuration is outside the kernel's domain

@@ -8,8 +8,8 @@ inputs: the measurement reference, not part of the product path) by relative
 Frobenius error ||O - O_dense||_F / ||O_dense||_F, and the statistics + attention
 kernels are timed with CUDA events.  G = 1 is the per-block first-order
 expansion (exact Taylor order, Eq. 5), G >= N_K is PISA's global H-bar (Eq. 6),
-G = 32 is PASA.  Group sizes outside the tensor-core kernel's set
-(1, 8, 16) run on the CUDA-core kernel, so their timings are not comparable.
+G = 32 is PASA.  G = 1 runs on the CUDA-core kernel (per-block first
+order: one 128x128x128 product per dropped block), so its timing is not comparable.
 
 Generators: ``correlated`` (strength 1: the first-order term
 matters) and ``video`` (smooth latent-grid keys, synth.video_qkv).
@@ -66,7 +66,7 @@ def run(q, k, v, *, rho=0.15, beta=0.1, seed=42, step=25, reps=5):
             torch.cuda.synchronize()
             rows.append({"G": G, "comp": comp, "rel_frobenius": rel_fro(out, dense),
                          "attn_ms": e0.elapsed_time(e1) / reps,
-                         "kernel": "tcgen05" if g in (32, 64) or g % 128 == 0 or g >= NK
+                         "kernel": "tcgen05" if g in (8, 16, 32, 64) or g % 128 == 0 or g >= NK
                          else "cuda-core"})
     return rows
 

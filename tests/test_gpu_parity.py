@@ -203,7 +203,10 @@ ATTN_CASES = [
     ("tc_d128_4100_zeroth", 1, 4100, 2, 128, 128, 32, "zeroth", 0.15, torch.bfloat16, "video"),
     ("tc_d64_4100_none", 1, 4100, 2, 64, 128, 32, "none", 0.15, torch.bfloat16, "iid"),
     ("fp32_d128_4100", 1, 4100, 1, 128, 128, 32, "grouped", 0.15, torch.float32, "video"),
-    ("tc_d128_g8_simt", 1, 4100, 1, 128, 128, 8, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d128_g8", 1, 4100, 1, 128, 128, 8, "grouped", 0.15, torch.bfloat16, "video"),
+    ("tc_d64_g16", 1, 9000, 2, 64, 128, 16, "grouped", 0.2, torch.bfloat16, "video"),
+    ("tc_d128_g16_ragged", 1, 4100, 1, 128, 128, 16, "grouped", 0.3, torch.bfloat16, "iid"),
+    ("tc_d128_g4_simt", 1, 4100, 1, 128, 128, 4, "grouped", 0.15, torch.bfloat16, "video"),
     ("tc_d128_g96_simt", 1, 8200, 1, 128, 128, 96, "grouped", 0.15, torch.bfloat16, "video"),
     ("tc_d128_20000_g128", 1, 20000, 1, 128, 128, 128, "grouped", 0.15, torch.bfloat16, "video"),
     ("tc_d64_20000_g64", 1, 20000, 1, 64, 128, 64, "grouped", 0.2, torch.bfloat16, "video"),
