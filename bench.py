@@ -102,6 +102,11 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # the first sample lands before the timed region starts (right after the
+            # warm-up steps), so short regions still report the clocks they ran at
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
