@@ -38,3 +38,29 @@ def test_pipeline_matches_device_call_bitwise(n_chunks):
     assert torch.equal(hout, ref.cpu())
     assert pipe.h2d_bytes == 3 * q.numel() * 2 + sum(x.numel() * 4 for x in xs)
     assert pipe.d2h_bytes == ref.numel() * 2
+
+
+def test_pipeline_d64_with_prior_bitwise():
+    """d = 64, the Eq. 8 prior (pasa_route_v per chunk), B = 2, uneven head chunks."""
+    from paper_2604_12219_b200 import build
+    build.build()
+    import paper_2604_12219_b200 as P
+    from paper_2604_12219_b200.pipeline import HostPipeline
+    B, S, H, D = 2, 4100, 5, 64
+    q, k, v = synth.video_qkv(B, (1, 1, S), H, D, seed=6, dtype=torch.bfloat16, device="cuda")
+    tp = synth.ThreePhase(shape=(16, 4, 12, 16), T=50, seed=2, device="cuda")
+    xs = [x.contiguous() for x in tp.latents(30)]
+    kw = dict(T=50, rho=0.15, l1_mean=tp.expected_l1_mean(), h_t=0.02, h_tm1=0.02)
+    cfg = P.RouteCfg(Bq=128, G=32, prior="global")
+    bud = P.Budget()
+    bud(*xs, step=30, **kw)
+    route = P.Route(B, S, H, D, cfg)
+    route(q, k, bud, 5, 30, v=v)
+    ref = P.attn(q, k, v, route)
+    hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+    hx = [x.cpu().pin_memory() for x in xs]
+    hout = torch.empty(ref.shape, dtype=ref.dtype, pin_memory=True)
+    pipe = HostPipeline(B, S, H, D, cfg, n_chunks=2)
+    pipe(hq, hk, hv, hout, hx, 5, 30, v_for_prior=True, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(hout, ref.cpu())
