@@ -249,6 +249,8 @@ __global__ void __launch_bounds__(kRsRows * 2) rowstats_kernel(const double* __r
 // route's mask word; the ascending index list follows from ballot prefix counts.
 // ---------------------------------------------------------------------------
 constexpr int kSelWarps = 4;
+// 5 CTAs (20 warps) per SM for M <= 40: a few spilled registers cost less than the
+// lost occupancy (route at Wan-14B 1.52 -> 1.34 ms with the window search below)
 
 __device__ __forceinline__ uint64_t orderable(double x) {
     x = __dadd_rn(x, 0.0);  // -0.0 -> +0.0: the oracle's double compare treats them as equal
@@ -279,7 +281,7 @@ struct SelArgs {
 };
 
 template <int MAXM>
-__global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
+__global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 2) select_kernel(SelArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);   // bh * NQ + i
     if (row >= a.rows) return;
@@ -335,8 +337,62 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
     // bit.  Upper half first with 32-bit compares (key >= T_hi:0 <=> hi >= T_hi), then
     // the lower half among the keys whose upper half equals T_hi (the others are
     // counted once: hi > T_hi always, hi < T_hi never).
+    //
+    // Shortcut (top >= 48): once the top 16 bits of T are fixed, the keys sharing them are
+    // usually few (a 1/16-binade window around the k-th score).  If there are at most
+    // 64, they are compacted into shared memory (two per lane) and the remaining bits
+    // are searched over those two registers instead of all M; the keys above the
+    // window are counted once.  Same T as the full search.
+    __shared__ uint64_t cbuf[kSelWarps][64];
     uint32_t T_hi = (uint32_t)(T >> 32);
-    for (int bpos = top; bpos >= 32; --bpos) {
+    int bpos = top;
+    for (; bpos >= 48; --bpos) {
+        const uint32_t cand = T_hi | (1u << (bpos - 32));
+        int c = 0;
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) c += (uint32_t)(key[m] >> 32) >= cand;
+        c = __reduce_add_sync(0xffffffffu, c);
+        if (c >= k) T_hi = cand;
+    }
+    if (top >= 48) {
+        // window = keys whose top 16 bits equal T's (32-bit compares on the upper half)
+        const uint32_t tw = T_hi >> 16;
+        int gw = 0, ew = 0;
+#pragma unroll
+        for (int m = 0; m < MAXM; ++m) {
+            const uint32_t h16 = (uint32_t)(key[m] >> 48);
+            gw += h16 > tw;
+            ew += h16 == tw;   // an absent key (0) can only match if tw = 0; it never counts below
+        }
+        gw = __reduce_add_sync(0xffffffffu, gw);
+        ew = __reduce_add_sync(0xffffffffu, ew);
+        if (ew <= 64) {
+            uint64_t* cb = cbuf[threadIdx.x >> 5];
+            const uint32_t lt = (1u << lane) - 1u;
+            int base = 0;
+#pragma unroll
+            for (int m = 0; m < MAXM; ++m) {
+                const bool in = (uint32_t)(key[m] >> 48) == tw;
+                const uint32_t b = __ballot_sync(0xffffffffu, in);
+                if (in) cb[base + __popc(b & lt)] = key[m];
+                base += __popc(b);
+            }
+            __syncwarp();
+            const uint64_t c0 = lane < ew ? cb[lane] : 0ull;
+            const uint64_t c1 = lane + 32 < ew ? cb[lane + 32] : 0ull;
+            __syncwarp();
+            uint64_t Tc = (uint64_t)T_hi << 32;
+            for (; bpos >= 0; --bpos) {
+                const uint64_t cand = Tc | (1ull << bpos);
+                const int c = gw + __reduce_add_sync(0xffffffffu, (c0 >= cand) + (c1 >= cand));
+                if (c >= k) Tc = cand;
+            }
+            T_hi = (uint32_t)(Tc >> 32);
+            T = Tc;
+            bpos = -2;   // done
+        }
+    }
+    for (; bpos >= 32; --bpos) {
         const uint32_t cand = T_hi | (1u << (bpos - 32));
         int c = 0;
 #pragma unroll
@@ -345,7 +401,9 @@ __global__ void __launch_bounds__(32 * kSelWarps) select_kernel(SelArgs a) {
         if (c >= k) T_hi = cand;
     }
     uint32_t T_lo = top >= 32 ? 0u : (uint32_t)T;
-    if (top >= 0) {
+    if (bpos == -2) {
+        T_lo = (uint32_t)T;
+    } else if (top >= 0) {
         int gtc = 0;
         uint32_t lo[MAXM];
 #pragma unroll

@@ -154,12 +154,19 @@ ROUTE_CASES = [
     ("ragged4100", 2, 4100, 2, 64, 128, 0.1, 0.15, "video"),
     ("beta0", 1, 4100, 2, 128, 128, 0.0, 0.15, "iid"),
     ("bigbeta", 1, 2048, 1, 128, 128, 5.0, 0.3, "iid"),
+    # N_K = 256: the select kernel's compacted-window search (few keys near the k-th)
+    ("iid16k", 1, 16384, 2, 128, 128, 0.1, 0.15, "iid"),
+    # every score within one 1/16 binade: the window holds > 64 keys -> full bit search
+    ("clustered16k", 1, 16384, 2, 128, 128, 0.1, 0.15, "clustered"),
 ]
 
 
 def gen_qkv(gen, B, S, H, D, dtype, seed=1000):
     if gen == "iid":
         return synth.iid_qkv(B, S, H, D, seed=seed, dtype=dtype, device="cuda")
+    if gen == "clustered":   # q, k = 1 + small noise: all block scores near s * d
+        q, k, v = synth.iid_qkv(B, S, H, D, seed=seed, dtype=torch.float32, device="cuda")
+        return ((1 + 0.05 * q).to(dtype), (1 + 0.05 * k).to(dtype), v.to(dtype))
     F = max(1, S // (32 * 32))
     grid = (F, 32, S // (32 * F)) if S % (32 * F) == 0 else (1, 1, S)
     return synth.video_qkv(B, grid, H, D, seed=seed, dtype=dtype, device="cuda")
