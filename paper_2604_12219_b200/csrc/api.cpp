@@ -378,9 +378,14 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
         e = pasa::launch_attn_simt(*q, *k, *v, route, *out, s, &launches);
     } else {
         char why[256] = {0};
-        e = (flags & PASA_ATTN_PAIRED)
-                ? pasa::launch_attn_sm100_pair(*q, *k, *v, route, *out, s, &launches, why, sizeof(why))
-                : pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        // diagnostics (pasa_debug_flags / pasa_debug_trace) live in the single-warpgroup kernel
+        const bool diag = (pasa::g_dbg & 63) != 0 || pasa::g_trace_buf != nullptr;
+        if (flags & PASA_ATTN_PAIRED)
+            e = pasa::launch_attn_sm100_pair(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        else if (!(flags & PASA_ATTN_SINGLE_WG) && !diag && pasa::attn_sm100_pp_supported(route))
+            e = pasa::launch_attn_sm100_pp(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        else
+            e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
         if (e == cudaErrorNotSupported) {
             g_launches = launches;
             return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);

@@ -86,6 +86,12 @@ inline bool sm100_supports_group(int64_t G, int64_t NK) {
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                               int* launches, char* why, size_t why_len);
+// default where it applies: two softmax warpgroups per CTA taking alternate ops
+// (G = 32 / 64 or no grouped term, d = 64 / 128); attn_sm100_pp.cu
+bool attn_sm100_pp_supported(const pasa_route_s* r);
+cudaError_t launch_attn_sm100_pp(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                                 pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                                 int* launches, char* why, size_t why_len);
 // variant: one CTA per SM, kept blocks processed in pairs (N = 128 QK^T), two
 // independent softmax warpgroups (PASA_ATTN_PAIRED)
 cudaError_t launch_attn_sm100_pair(const pasa_tensor& q, const pasa_tensor& k,
