@@ -202,10 +202,11 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
 /*   PASA_ATTN_PAIRED       use the paired-block tensor-core variant (one CTA per SM, kept
  *                          blocks processed two at a time; same results up to rounding) */
 #define PASA_ATTN_PAIRED 8u
-/*   PASA_ATTN_SINGLE_WG    use the single-softmax-warpgroup tensor-core kernel even where the
- *                          two-warpgroup kernel applies (A/B comparison; same results up to
- *                          the fp32 summation order of the softmax denominator) */
-#define PASA_ATTN_SINGLE_WG 16u
+/*   PASA_ATTN_PINGPONG     use the one-CTA-per-SM variant (Q in TMEM, QK^T as a TS MMA, four
+ *                          S/P buffers, two softmax warpgroups on alternate ops) where it
+ *                          applies (d = 64 / 128, G = 32 / 64 or no grouped term); same
+ *                          results up to the fp32 summation order of the denominator */
+#define PASA_ATTN_PINGPONG 16u
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 

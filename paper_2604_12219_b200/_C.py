@@ -24,7 +24,7 @@ PASA_ATTN_STATS_ONLY = 2
 PASA_ATTN_REUSE_STATS = 4
 PRIOR = {"none": 0, "global": 1, "group": 2}
 PASA_ATTN_PAIRED = 8
-PASA_ATTN_SINGLE_WG = 16
+PASA_ATTN_PINGPONG = 16
 
 # every symbol include/pasa.h declares (tests check the library exports them all)
 EXPORTS = [

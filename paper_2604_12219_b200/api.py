@@ -208,10 +208,10 @@ class Route:
 
 
 def attn(q, k, v, route: Route, out=None, *, force_simt=False, stats_only=False,
-         reuse_stats=False, paired=False, single_wg=False, stream=None):
+         reuse_stats=False, paired=False, pingpong=False, stream=None):
     """pasa_attn: returns out ([B, S, H, D], q's dtype).  stats_only / reuse_stats
     split the call into its statistics and attention kernels (PASA_ATTN_* flags);
-    single_wg selects the single-softmax-warpgroup tensor-core kernel (A/B)."""
+    pingpong selects the one-CTA-per-SM two-warpgroup variant (A/B)."""
     if out is None:
         out = torch.empty_like(q)
     qd, kd, vd, od = tensor_desc(q), tensor_desc(k), tensor_desc(v), tensor_desc(out)
@@ -219,7 +219,7 @@ def attn(q, k, v, route: Route, out=None, *, force_simt=False, stats_only=False,
              | (_C.PASA_ATTN_STATS_ONLY if stats_only else 0)
              | (_C.PASA_ATTN_REUSE_STATS if reuse_stats else 0)
              | (_C.PASA_ATTN_PAIRED if paired else 0)
-             | (_C.PASA_ATTN_SINGLE_WG if single_wg else 0))
+             | (_C.PASA_ATTN_PINGPONG if pingpong else 0))
     _C.check(_C.lib().pasa_attn_ex(ctypes.byref(qd), ctypes.byref(kd), ctypes.byref(vd),
                                    route.handle, ctypes.byref(od), flags, _stream_ptr(stream)),
              "pasa_attn")

@@ -382,7 +382,7 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
         const bool diag = (pasa::g_dbg & 63) != 0 || pasa::g_trace_buf != nullptr;
         if (flags & PASA_ATTN_PAIRED)
             e = pasa::launch_attn_sm100_pair(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
-        else if (!(flags & PASA_ATTN_SINGLE_WG) && !diag && pasa::attn_sm100_pp_supported(route))
+        else if ((flags & PASA_ATTN_PINGPONG) && !diag && pasa::attn_sm100_pp_supported(route))
             e = pasa::launch_attn_sm100_pp(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
         else
             e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));

@@ -90,7 +90,12 @@ enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK,
 struct Ctl {
     uint64_t q_full;
     uint64_t k_full[3], k_empty[3], s_full[3];   // per K slot / S buffer (n % NB)
-    uint64_t p_full[2], pv_done[2];              // per op parity (n & 1): P ready + V landed; O-MMA done
+    // p_full per S buffer (n % NB): P ready + V landed.  With NB = 3 the softmax can finish
+    // op n+2 before V(n) has even been requested (QK(n+2) is issued before PV(n)), so a
+    // barrier shared by ops n and n+2 would count op n+2's arrivals into op n's phase and
+    // let PV(n) read an unloaded V tile; one barrier per S buffer cannot be lapped, since
+    // QK(n+NB) follows PV(n).  pv_done per V slot (n & 1): O-MMA done.
+    uint64_t p_full[3], pv_done[2];
     uint32_t tmem_base;
     int32_t nops;
     uint32_t mask[64];
@@ -138,7 +143,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_init(&ctl.k_empty[s], 1);
             mbar_init(&ctl.s_full[s], 1);
         }
-        for (int s = 0; s < 2; ++s)
+        for (int s = 0; s < G_::NB; ++s)
             mbar_init(&ctl.p_full[s], 129);   // 128 softmax threads + the V producer (expect_tx)
         mbar_init(&ctl.pv_done[0], 1);
         mbar_init(&ctl.pv_done[1], 1);
@@ -229,29 +234,29 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ======================= V-ring producer =======================
         if (lane == 0) {
             for (int n = 0; n < nops; ++n) {
-                const int s = n & 1;
+                const int s = n & 1, pb = n % G_::NB;
                 mbar_wait_sleep(&ctl.pv_done[s], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
                 if (DIAG && (p.dbg & 2)) {
-                    mbar_arrive(&ctl.p_full[s]);
+                    mbar_arrive(&ctl.p_full[pb]);
                 } else if (op_type(op) == OP_F) {
                     if (G_::NBOX == 2) {
-                        mbar_arrive_expect_tx(&ctl.p_full[s], G_::HTBOX);
-                        tma_load_3d(dst, &tmHt, &ctl.p_full[s], 64, v * D, (int)bh);
+                        mbar_arrive_expect_tx(&ctl.p_full[pb], G_::HTBOX);
+                        tma_load_3d(dst, &tmHt, &ctl.p_full[pb], 64, v * D, (int)bh);
                     } else {
-                        mbar_arrive(&ctl.p_full[s]);
+                        mbar_arrive(&ctl.p_full[pb]);
                     }
                 } else {
-                    mbar_arrive_expect_tx(&ctl.p_full[s], G_::SLOT);
+                    mbar_arrive_expect_tx(&ctl.p_full[pb], G_::SLOT);
 #pragma unroll
                     for (int a = 0; a < G_::NBOX; ++a) {
                         if (op_type(op) == OP_E)
-                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.p_full[s], 64 * a, v * kBK,
+                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.p_full[pb], 64 * a, v * kBK,
                                         (int)h, (int)b);
                         else
-                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.p_full[s], 64 * a, v * 64,
+                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.p_full[pb], 64 * a, v * 64,
                                         (int)bh);
                     }
                 }
@@ -300,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (nq < nops && op_type(ctl.ops[nq]) != OP_F) issue_qk(nq);
             // V(n) lands on p_full[s] too (one wait for "P ready and V loaded")
             if (lane == 0) PASA_TR(TR_MMA_V, n);
-            mbar_wait_c(&ctl.p_full[s], (n >> 1) & 1, spin);
+            mbar_wait_c(&ctl.p_full[sb], (n / G_::NB) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_P, n);
             tc_fence_after();
             const int32_t op = ctl.ops[n];
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_wait_st();
             }
             tc_fence_before();
-            mbar_arrive(&ctl.p_full[s]);
+            mbar_arrive(&ctl.p_full[bi]);
             if (warp == 4 && lane == 0) PASA_TR(TR_SA_ARR, n);
         }
         // ---- epilogue: O / l -> bf16 -> global ----

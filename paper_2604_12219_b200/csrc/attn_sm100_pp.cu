@@ -1,12 +1,18 @@
-// attn_sm100_pp.cu -- pasa_attn on the tcgen05 tensor cores with two softmax
-// warpgroups per CTA that take alternate ops ("ping-pong").  Same method and op
-// list as attn_sm100.cu (Eq. 7; grouped first-order term,
-// PAPER.md:310-313, App. B :503-506; readings R-1..R-5, R-21, R-22), same TMEM
-// budget (O + two S/P buffers = 256 columns, 2 CTAs per SM), but the two S
-// buffers are now worked on CONCURRENTLY: warpgroup w owns buffer w and every op
-// n with n % 2 == w.  The single-warpgroup kernel was latency-bound by its
-// QK -> softmax -> PV chain; here two softmax chains per CTA (four
-// per SM) keep the tensor pipe fed.
+// attn_sm100_pp.cu -- pasa_attn on the tcgen05 tensor cores, one CTA per SM with
+// two softmax warpgroups that take alternate ops ("ping-pong").  Same method and
+// op list as attn_sm100.cu (Eq. 7; grouped first-order term,
+// PAPER.md:310-313, App. B :503-506; readings R-1..R-5, R-21, R-22).
+//
+// Why this shape: the 2-CTA/SM kernel reads Q from shared memory
+// for every QK^T (SS MMA: 48 KB of operand reads per 64-key op at d = 128) while
+// TMA writes the next K and V tiles (32 KB) into the same shared memory; with PV's
+// 16 KB that is 96 KB per op through one 128 B/clk port, more than the tensor
+// math needs.  Here Q sits in TMEM and QK^T is a TS MMA (only the 16 KB K tile is
+// read from shared memory), which needs 64 TMEM columns more than the 2-CTA layout
+// has.  So one CTA owns the SM's 512 columns: O (D) + Q (D/2) + four S/P buffers
+// of 64.  Op n uses buffer / K slot / V slot n % 4 and is worked on by softmax
+// warpgroup n % 2, so each warpgroup has the S of its next op computed while it
+// works on the current one, and QK(n+4) is issued right after PV(n).
 //
 // What the two warpgroups share, and how:
 //   * the running max m.  It is the same sequential rule as the single-warpgroup
@@ -27,8 +33,8 @@
 //     barrier (an F op never moves m, so no rescale is needed in between).
 // Warp roles (384 threads): warp 0 K-ring TMA producer, warp 1 TMEM allocator +
 // MMA issuer, warp 2 V-ring TMA producer, warp 3 idle; warps 4-7 softmax
-// warpgroup 0 (even ops), warps 8-11 softmax warpgroup 1 (odd ops).  Registers
-// are moved from warpgroup 0 to the softmax warpgroups with setmaxnreg.
+// warpgroup 0 (even ops), warps 8-11 softmax warpgroup 1 (odd ops); both copy
+// their rows of Q from shared memory into TMEM before the first QK^T.
 // Domain: bf16, Bq = 128, Bk = 64, d = 64 or 128, compensation NONE / ZEROTH /
 // GROUPED with G = 32 or 64 (other G: attn_sm100.cu).
 #include <cuda.h>
@@ -49,7 +55,7 @@ using namespace ptx;
 constexpr int kThreads = 384;
 constexpr int kBQ = 128, kBK = 64;
 constexpr int kMaxOps = 2048 + 32 + 64 + 64;
-constexpr int kTmemCols = 256;
+constexpr int kTmemCols = 512;
 constexpr float kRescaleThresh = 8.f;   // log2 units
 // named barriers (0 = __syncthreads)
 constexpr uint32_t kBarEpi = 1;      // epilogue: the two l partials
@@ -64,18 +70,14 @@ __device__ __forceinline__ uint16_t op_make(uint32_t type, uint32_t v) {
 __device__ __forceinline__ uint32_t op_type(uint32_t op) { return op >> 14; }
 __device__ __forceinline__ uint32_t op_val(uint32_t op) { return op & 0x3FFFu; }
 
-template <int R>
-__device__ __forceinline__ void regs_dec() {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(R));
-}
-template <int R>
-__device__ __forceinline__ void regs_inc() {
-    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(R));
-}
+constexpr int NS = 4;   // S/P buffers in TMEM = K slots = V slots; op n uses buffer n % NS
 
 template <int D>
 struct Geo {
-    static constexpr uint32_t COLS = D;             // O columns; S buffer w at COLS + 64 w
+    // TMEM columns: O [0, D), Q [D, D + D/2) (bf16 pairs), S/P buffer b at SCOL + 64 b
+    static constexpr uint32_t QCOL = D;
+    static constexpr uint32_t SCOL = D + 64;
+    static_assert(SCOL + 64 * NS <= 512, "TMEM budget");
     static constexpr int NBOX = D / 64;
     static constexpr int QBOX = kBQ * 128;          // bytes per 64-col box of Q
     static constexpr int KVBOX = kBK * 128;         // bytes per 64-col box of a K/V tile
@@ -83,8 +85,8 @@ struct Geo {
     static constexpr int HTBOX = D * 128;           // bytes per 64-col box of Hbar^T
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = kBQ * D * 2;
-    static constexpr int OFF_V = OFF_K + 2 * SLOT;
-    static constexpr int BYTES = OFF_V + 2 * SLOT;
+    static constexpr int OFF_V = OFF_K + NS * SLOT;
+    static constexpr int BYTES = OFF_V + NS * SLOT;
     static_assert(HTBOX <= SLOT, "an Hbar^T box must fit one ring slot");
 };
 
@@ -101,9 +103,9 @@ struct Params {
 };
 
 struct Ctl {
-    uint64_t q_full;
-    uint64_t k_full[2], k_empty[2], s_full[2];   // per K slot / S buffer (n & 1)
-    uint64_t p_full[2], pv_done[2];              // per op parity: P ready + V landed; O-MMA done
+    uint64_t q_full, q_tmem;                       // Q landed in smem / copied into TMEM
+    uint64_t k_full[NS], k_empty[NS], s_full[NS];  // per K slot / S buffer (n % NS)
+    uint64_t p_full[NS], pv_done[NS];              // per buffer: P ready + V landed; O-MMA done
     uint32_t tmem_base;
     int32_t nops;
     uint32_t mask[64];
@@ -114,7 +116,7 @@ struct Ctl {
 };
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 1)
     attn_sm100_pp_kernel(const __grid_constant__ CUtensorMap tmQ,
                          const __grid_constant__ CUtensorMap tmK,
                          const __grid_constant__ CUtensorMap tmV,
@@ -140,7 +142,8 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int q = tid; q < cnt; q += blockDim.x) ctl.ops[q] = op_make(OP_E, (uint32_t)p.idx[row * (int64_t)NK + q]);
     if (tid == 0) {
         mbar_init(&ctl.q_full, 1);
-        for (int s = 0; s < 2; ++s) {
+        mbar_init(&ctl.q_tmem, 256);
+        for (int s = 0; s < NS; ++s) {
             mbar_init(&ctl.k_full[s], 1);
             mbar_init(&ctl.k_empty[s], 1);
             mbar_init(&ctl.s_full[s], 1);
@@ -194,7 +197,6 @@ __global__ void __launch_bounds__(kThreads, 2)
     const uint32_t tbase = ctl.tmem_base;
 
     if (warp < 4) {
-        regs_dec<32>();
         if (warp == 0) {
             // ======================= K-ring producer =======================
             if (lane == 0) {
@@ -202,26 +204,26 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a)
                     tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
-                                (int)(i * kBQ), (int)h, (int)b);
+                                i * kBQ, h, b);
                 for (int n = 0; n < nops; ++n) {
-                    const int s = n & 1;
-                    mbar_wait_sleep(&ctl.k_empty[s], ((n >> 1) & 1) ^ 1);
+                    const int s = n % NS;
+                    mbar_wait_sleep(&ctl.k_empty[s], ((n / NS) & 1) ^ 1);
                     uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                     const uint32_t op = ctl.ops[n];
                     const int v = (int)op_val(op);
                     if (op_type(op) == OP_F) {
                         mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
-                        tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
+                        tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, bh);
                     } else {
                         mbar_arrive_expect_tx(&ctl.k_full[s], G_::SLOT);
 #pragma unroll
                         for (int a = 0; a < G_::NBOX; ++a) {
                             if (op_type(op) == OP_E)
                                 tma_load_4d(dst + a * G_::KVBOX, &tmK, &ctl.k_full[s], 64 * a,
-                                            v * kBK, (int)h, (int)b);
+                                            v * kBK, h, b);
                             else
                                 tma_load_3d(dst + a * G_::KVBOX, &tmKb, &ctl.k_full[s], 64 * a,
-                                            v * 64, (int)bh);
+                                            v * 64, bh);
                         }
                     }
                 }
@@ -231,15 +233,15 @@ __global__ void __launch_bounds__(kThreads, 2)
             // ======================= V-ring producer =======================
             if (lane == 0) {
                 for (int n = 0; n < nops; ++n) {
-                    const int s = n & 1;
-                    mbar_wait_sleep(&ctl.pv_done[s], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
+                    const int s = n % NS;
+                    mbar_wait_sleep(&ctl.pv_done[s], ((n / NS) & 1) ^ 1);   // PV(n-NS) read the slot
                     uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                     const uint32_t op = ctl.ops[n];
                     const int v = (int)op_val(op);
                     if (op_type(op) == OP_F) {
                         if (G_::NBOX == 2) {
                             mbar_arrive_expect_tx(&ctl.p_full[s], G_::HTBOX);
-                            tma_load_3d(dst, &tmHt, &ctl.p_full[s], 64, v * D, (int)bh);
+                            tma_load_3d(dst, &tmHt, &ctl.p_full[s], 64, v * D, bh);
                         } else {
                             mbar_arrive(&ctl.p_full[s]);
                         }
@@ -249,10 +251,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                         for (int a = 0; a < G_::NBOX; ++a) {
                             if (op_type(op) == OP_E)
                                 tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.p_full[s], 64 * a,
-                                            v * kBK, (int)h, (int)b);
+                                            v * kBK, h, b);
                             else
                                 tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.p_full[s], 64 * a,
-                                            v * 64, (int)bh);
+                                            v * 64, bh);
                         }
                     }
                 }
@@ -260,87 +262,98 @@ __global__ void __launch_bounds__(kThreads, 2)
             __syncwarp();
         } else if (warp == 1) {
             // ======================= MMA issuer =======================
-            // per op n (buffer s = n & 1): wait P(n) -> PV(n) (or F(n)) -> QK(n+2) into the
-            // same buffer (tcgen05 ops run in issue order, so PV(n) has read P(n) first)
-            constexpr uint32_t kIdQK = idesc_bf16_f32(128, kBK, 0, 0);   // Q x K^T, both K-major
+            // QK^T reads Q from TMEM (TS MMA: only the K tile comes from shared memory).
+            // Per op n (buffer s = n % NS): wait P(n) -> PV(n) (or F(n)) -> QK(n+NS) into the
+            // same buffer (tcgen05 ops run in issue order, so PV(n) has read P(n) first).
+            constexpr uint32_t kIdQK = idesc_bf16_f32(128, kBK, 0, 0);   // Q (TMEM) x K^T (K-major)
             constexpr uint32_t kIdPV = idesc_bf16_f32(128, D, 0, 1);     // P (TMEM) x V (MN-major)
             constexpr uint32_t kIdF = idesc_bf16_f32(128, D, 0, 0);      // Aq (TMEM) x Hbar^T (K-major)
-            const uint32_t q_base = smem_u32(smem + G_::OFF_Q);
             const uint32_t k_base = smem_u32(smem + G_::OFF_K);
             const uint32_t v_base = smem_u32(smem + G_::OFF_V);
-            const uint64_t dq0 = umma_desc_sw128(q_base, 16, 1024);
             const uint64_t dk0 = umma_desc_sw128(k_base, 16, 1024);
             const uint64_t dv0 = umma_desc_sw128(v_base, G_::KVBOX, 1024);
             auto issue_qk = [&](int n) {
-                const int s = n & 1;
-                mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
+                const int s = n % NS;
+                mbar_wait_sleep(&ctl.k_full[s], (n / NS) & 1);
                 tc_fence_after();
-                const uint32_t d = tbase + G_::COLS + 64 * s;
+                const uint32_t d = tbase + G_::SCOL + 64 * s;
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
                     const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
-                    mma_ss_elect(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
+                    mma_ts_elect(d, tbase + G_::QCOL + kk * 8, dk0 + offk, kIdQK, kk > 0);
                 }
                 mma_commit_elect(&ctl.s_full[s]);
                 mma_commit_elect(&ctl.k_empty[s]);
                 __syncwarp();
             };
-            mbar_wait_sleep(&ctl.q_full, 0);
+            mbar_wait_sleep(&ctl.q_tmem, 0);   // the softmax warps copied Q into TMEM
             tc_fence_after();
-            for (int m = 0; m < 2 && m < nops; ++m)
+            for (int m = 0; m < NS && m < nops; ++m)
                 if (op_type(ctl.ops[m]) != OP_F) issue_qk(m);
             for (int n = 0; n < nops; ++n) {
-                const int s = n & 1;
-                mbar_wait_sleep(&ctl.p_full[s], (n >> 1) & 1);   // P(n) ready and V(n) landed
+                const int s = n % NS;
+                mbar_wait_sleep(&ctl.p_full[s], (n / NS) & 1);   // P(n) ready and V(n) landed
                 tc_fence_after();
                 const uint32_t op = ctl.ops[n];
                 if (op_type(op) != OP_F) {
 #pragma unroll
                     for (int kk = 0; kk < kBK / 16; ++kk) {
                         const uint32_t offv = (s * G_::SLOT + kk * 16 * 128) >> 4;
-                        mma_ts_elect(tbase, tbase + G_::COLS + 64 * s + kk * 8, dv0 + offv, kIdPV,
+                        mma_ts_elect(tbase, tbase + G_::SCOL + 64 * s + kk * 8, dv0 + offv, kIdPV,
                                      (n > 0 || kk > 0) ? 1u : 0u);
                     }
                     mma_commit_elect(&ctl.pv_done[s]);
                 } else {
-                    mbar_wait_sleep(&ctl.k_full[s], (n >> 1) & 1);
+                    mbar_wait_sleep(&ctl.k_full[s], (n / NS) & 1);
                     tc_fence_after();
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
                         const uint32_t box = (kk >> 2) == 0 ? k_base + s * G_::SLOT
                                                             : v_base + s * G_::SLOT;
                         const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
-                        mma_ts_elect(tbase, tbase + G_::COLS + 64 * s + kk * 8, bd, kIdF, 1u);
+                        mma_ts_elect(tbase, tbase + G_::SCOL + 64 * s + kk * 8, bd, kIdF, 1u);
                     }
                     mma_commit_elect(&ctl.k_empty[s]);
                     mma_commit_elect(&ctl.pv_done[s]);
                 }
                 __syncwarp();
-                if (n + 2 < nops && op_type(ctl.ops[n + 2]) != OP_F) issue_qk(n + 2);
+                if (n + NS < nops && op_type(ctl.ops[n + NS]) != OP_F) issue_qk(n + NS);
             }
         }
     } else {
-        regs_inc<104>();
         // =================== softmax / correction / epilogue ===================
         const int wg = (warp >> 2) - 1;                       // 0: even ops, 1: odd ops
         const int r = (warp & 3) * 32 + lane;                 // query row in the block
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t t_o = tbase + lane_off;
-        const uint32_t t_buf = tbase + lane_off + G_::COLS + 64 * wg;
         const uint8_t* qrow = smem + G_::OFF_Q;
+        // Q -> TMEM (the A operand of QK^T): warpgroup w copies 64-column box w of its rows
+        mbar_wait_sleep(&ctl.q_full, 0);
+        if (wg < G_::NBOX) {
+            uint32_t qa[32];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+                const uint4 u = *reinterpret_cast<const uint4*>(qrow + wg * G_::QBOX + r * 128 +
+                                                                ((cc ^ (r & 7)) << 4));
+                qa[cc * 4 + 0] = u.x; qa[cc * 4 + 1] = u.y; qa[cc * 4 + 2] = u.z; qa[cc * 4 + 3] = u.w;
+            }
+            tmem_st32(t_o + G_::QCOL + 32 * wg, qa);
+            tmem_wait_st();
+        }
+        tc_fence_before();
+        mbar_arrive(&ctl.q_tmem);
         float m_ref = -INFINITY;   // the reference max this warpgroup's l is relative to
         float l = 0.f;
-        int sc = 0;                // S-type ops seen on this warpgroup's buffer (s_full parity)
+        int sc0 = 0, sc1 = 0;      // S-type ops seen on this warpgroup's two buffers (s_full parity)
         const int n_last = NK - 1;
         const int nlast_len = p.S - n_last * 64;
         const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
-        // pv_done[b] completes once per op on buffer b (ops b, b+2, ...): op m's completion is
-        // phase m >> 1 of pv_done[m & 1]; only the latest op issued on a buffer is ever
+        // pv_done[b] completes once per op on buffer b (ops b, b+NS, ...): op m's completion is
+        // phase m / NS of pv_done[m % NS]; only the latest op issued on a buffer is ever
         // awaited (PV(n) cannot start before P(n) is released), so the parity test is exact.
         auto consume_op = [&](int op) {
             if (op < 0) return;
-            mbar_wait_sleep(&ctl.pv_done[op & 1], (op >> 1) & 1);
+            mbar_wait_sleep(&ctl.pv_done[op % NS], (op / NS) & 1);
         };
         // m_{n-1}: decided by the other warpgroup (op n-1); n = 0 starts from -inf
         auto chain_get = [&](int n) -> float {
@@ -356,8 +369,10 @@ __global__ void __launch_bounds__(kThreads, 2)
             const uint32_t op = ctl.ops[n];
             const uint32_t type = op_type(op);
             const int v = (int)op_val(op);
+            const int bsel = (n >> 1) & 1;                    // which of this warpgroup's buffers
+            const uint32_t t_buf = tbase + lane_off + G_::SCOL + 64 * (n % NS);
             if (type != OP_F) {
-                mbar_wait_sleep(&ctl.s_full[wg], (sc++) & 1);
+                mbar_wait_sleep(&ctl.s_full[n % NS], ((bsel ? sc1++ : sc0++)) & 1);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
                 tmem_ld32(t_buf, sa);
@@ -467,7 +482,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (m_prev != m_ref) { l *= ex2(m_ref - m_prev); m_ref = m_prev; }
                 const float w = p.s * A;
                 const uint32_t w2 = pack_bf16(w, w);
-                consume_op(n - 2);   // the buffer's previous reader
+                consume_op(n - NS);   // the buffer's previous reader
                 tc_fence_after();
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {
@@ -486,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_wait_st();
             }
             tc_fence_before();
-            mbar_arrive(&ctl.p_full[n & 1]);
+            mbar_arrive(&ctl.p_full[n % NS]);
         }
         // ---- epilogue: final reference max, l = l_0 + l_1, O / l -> bf16 -> global ----
         if (((nops - 1) & 1) != wg) {   // the other warpgroup decided the last op
@@ -563,10 +578,10 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     prm.idx = r->idx; prm.count = r->count; prm.mask = r->mask;
     prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
     prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
-    // at least ~80 KB so at most two CTAs share an SM (2 x 256 TMEM columns; a third
-    // would block in tcgen05.alloc)
+    // one CTA per SM (it allocates all 512 TMEM columns): request more than half the
+    // shared memory so a second CTA never waits in tcgen05.alloc
     size_t smem = (size_t)Geo<D>::BYTES + 1024;
-    if (smem < 80 * 1024) smem = 80 * 1024;
+    if (smem < 120 * 1024) smem = 120 * 1024;
     auto kern = attn_sm100_pp_kernel<D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

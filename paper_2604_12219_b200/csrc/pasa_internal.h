@@ -86,8 +86,8 @@ inline bool sm100_supports_group(int64_t G, int64_t NK) {
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                               int* launches, char* why, size_t why_len);
-// default where it applies: two softmax warpgroups per CTA taking alternate ops
-// (G = 32 / 64 or no grouped term, d = 64 / 128); attn_sm100_pp.cu
+// variant (PASA_ATTN_PINGPONG): one CTA per SM, Q in TMEM, two softmax warpgroups on
+// alternate ops (G = 32 / 64 or no grouped term, d = 64 / 128); attn_sm100_pp.cu
 bool attn_sm100_pp_supported(const pasa_route_s* r);
 cudaError_t launch_attn_sm100_pp(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                                  pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,

@@ -75,8 +75,8 @@ def check_route(P, q, k, cfg, rho, seed=42, step=25, heads=None):
     return route, got, ties
 
 
-def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None):
-    out = P.attn(q, k, v, route, force_simt=force_simt)
+def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, pingpong=False):
+    out = P.attn(q, k, v, route, force_simt=force_simt, pingpong=pingpong)
     torch.cuda.synchronize()
     B, S, H, D = q.shape
     if pairs is None:
@@ -233,6 +233,28 @@ def test_attn_parity(pasa, case):
     assert torch.equal(out, out2)
 
 
+PINGPONG_CASES = [c for c in ATTN_CASES if c[0] in (
+    "tc_d128_1000", "tc_d128_4100_g32", "tc_d64_4100_g32", "tc_d128_4100_g64",
+    "tc_d128_4100_zeroth", "tc_d64_4100_none", "tc_d64_20000_g64", "tc_d128_odd_k")]
+
+
+@pytest.mark.parametrize("case", PINGPONG_CASES, ids=[c[0] for c in PINGPONG_CASES])
+def test_attn_parity_pingpong(pasa, case):
+    """The one-CTA-per-SM variant (PASA_ATTN_PINGPONG: Q in TMEM, two softmax
+    warpgroups on alternate ops) against the oracle, and against the default kernel:
+    the same running-max decisions and PV order, so they differ only by the fp32
+    summation order of the denominator (a few bf16 ulps of the output)."""
+    name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
+    q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=11)
+    cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, rho)
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pingpong=True)
+    ref = pasa.attn(q, k, v, route)
+    rel = (out.float() - ref.float()).abs().max().item() / ref.float().abs().max().item()
+    assert rel <= 1e-2, rel
+    assert torch.equal(out, pasa.attn(q, k, v, route, pingpong=True))
+
+
 EDGE_CASES = [
     # name, S, D, Bq, rho, dtype: degenerate lengths around the block sizes, k = 1
     ("S1", 1, 128, 128, 0.15, torch.bfloat16),
@@ -248,8 +270,9 @@ EDGE_CASES = [
 ]
 
 
+@pytest.mark.parametrize("pingpong", [False, True], ids=["default", "pingpong"])
 @pytest.mark.parametrize("case", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
-def test_attn_edge_cases(pasa, case):
+def test_attn_edge_cases(pasa, case, pingpong):
     """Single partial blocks (S < Bk, S < Bq), one-token sequences, lengths one past a
     block edge, k = 1 (the floor of R-14) and k = N_K - 1: route bit-exact, output
     within the tolerance of the dtype."""
@@ -257,7 +280,7 @@ def test_attn_edge_cases(pasa, case):
     q, k, v = synth.iid_qkv(1, S, 2, D, seed=S + D, dtype=dtype, device="cuda")
     cfg = pasa.RouteCfg(Bq=Bq, G=32, beta=0.1)
     route, got, _ = check_route(pasa, q, k, cfg, rho)
-    check_attn(pasa, q, k, v, route, got, cfg)
+    check_attn(pasa, q, k, v, route, got, cfg, pingpong=pingpong)
 
 
 def test_tensor_core_matches_simt_kernel(pasa):
@@ -326,6 +349,7 @@ def _pairs(H, NQ, heads, nq):
 @pytest.mark.parametrize("name,gen,heads,nq", [
     ("wan13b_480p", "video", [0, 5, 11], 12),
     ("wan14b_720p", "iid", [0, 39], 6),
+    ("cogvideox5b", "video", [0, 23, 47], 8),
 ])
 def test_full_config_sampled(pasa, name, gen, heads, nq):
     """BASELINE.json configs at full size, in the launch configuration bench.py
@@ -344,3 +368,28 @@ def test_full_config_sampled(pasa, name, gen, heads, nq):
     assert ties <= 4
     NQ = route.NQ
     check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, NQ, heads, nq))
+
+
+@pytest.mark.parametrize("pingpong", [False, True], ids=["default", "pingpong"])
+@pytest.mark.parametrize("name", ["wan13b_480p", "cogvideox5b", "wan14b_720p", "hunyuan_720p"])
+def test_full_config_repeat_finite_bitwise(pasa, name, pingpong):
+    """Every BASELINE config at full size in bench.py's launch configuration, three
+    times: the whole output is finite and bitwise identical run to run.  (A barrier
+    lapped by a softmax running two ops ahead at d = 64 once let PV read an unloaded
+    V tile: a few rows of NaN in some runs, invisible to sampled parity.)"""
+    c = synth.CONFIGS[name]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    q, k, v = synth.iid_qkv(B, S, H, D, seed=1004, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=c["Bq"], G=c["G"], beta=0.1)
+    route = pasa.Route(B, S, H, D, cfg)
+    route(q, k, make_budget(pasa, c["rho"]), pasa.layer_seed(42, 0), 25)
+    first = None
+    for _ in range(3):
+        out = torch.full_like(q, float("nan"))
+        pasa.attn(q, k, v, route, out, pingpong=pingpong)
+        torch.cuda.synchronize()
+        assert bool(torch.isfinite(out).all())
+        if first is None:
+            first = out
+        else:
+            assert torch.equal(out, first)

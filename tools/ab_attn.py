@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """A/B timing of the tensor-core attention kernels on one config: the default
-(two softmax warpgroups where it applies) against the single-warpgroup kernel,
+(single softmax warpgroup, 2 CTAs/SM) against the ping-pong variant (one CTA/SM,
+Q in TMEM, two softmax warpgroups),
 interleaved repetitions (the pool's clocks drift under power cap), min / median.
     CFG=wan14b_720p REPS=8 python tools/ab_attn.py"""
 import os
@@ -26,21 +27,21 @@ bud(z, z, z, T=50, step=25, rho_table=[float(os.environ.get("RHO", cfg["rho"]))]
 route(q, k, bud, 1, 25)
 out = P.attn(q, k, v, route, stats_only=True)
 ref = torch.empty_like(q)
-P.attn(q, k, v, route, ref, reuse_stats=True, single_wg=True)
-P.attn(q, k, v, route, out, reuse_stats=True)
+P.attn(q, k, v, route, ref, reuse_stats=True, pingpong=True)
+P.attn(q, k, v, route, out, reuse_stats=True, pingpong=False)
 torch.cuda.synchronize()
 d = (out.float() - ref.float()).abs().max().item() / ref.float().abs().max().item()
-print(f"max|default - single_wg| / max|O| = {d:.3e}", flush=True)
+print(f"max|default - pingpong| / max|O| = {d:.3e}", flush=True)
 REPS = int(os.environ.get("REPS", "6"))
 res = {}
 for rep in range(REPS):
-    for name, sw in (("default", False), ("single_wg", True)):
+    for name, sw in (("default", False), ("pingpong", True)):
         for _ in range(2):
-            P.attn(q, k, v, route, out, reuse_stats=True, single_wg=sw)
+            P.attn(q, k, v, route, out, reuse_stats=True, pingpong=sw)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(5):
-            P.attn(q, k, v, route, out, reuse_stats=True, single_wg=sw)
+            P.attn(q, k, v, route, out, reuse_stats=True, pingpong=sw)
         e1.record()
         torch.cuda.synchronize()
         res.setdefault(name, []).append(e0.elapsed_time(e1) / 5)
