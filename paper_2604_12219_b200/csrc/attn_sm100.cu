@@ -341,7 +341,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint8_t* qrow = smem + G_::OFF_Q;
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
-        int64_t g_cur = -1, g_done = -1;
+        int g_cur = -1, g_done = -1;          // 32-bit group bookkeeping (N_K <= 2048)
+        const int G32 = (int)p.G, NK32 = (int)NK;
         int c_last = 0;   // G = 8 or 16: chunk of the last C op (ctl.sg holds its group sums)
         int sc0 = 0, sc1 = 0, sc2 = 0;   // S-type ops seen per S buffer (s_full parity)
         const int64_t n_last = NK - 1;
@@ -392,10 +393,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 } else {
                     const uint64_t kept = (uint64_t)ctl.mask[2 * v] |
                                           ((2 * v + 1 < p.W) ? (uint64_t)ctl.mask[2 * v + 1] << 32 : 0ull);
-                    const int64_t rem = NK - 64 * (int64_t)v;
+                    const int rem = NK32 - 64 * v;
                     const uint64_t inb = rem >= 64 ? ~0ull : ((1ull << rem) - 1ull);
                     valid = ~kept & inb;
-                    if (rem <= 64) { clast = (int)(rem - 1); wlast = (float)nlast_len; }
+                    if (rem <= 64) { clast = rem - 1; wlast = (float)nlast_len; }
                 }
                 if (valid != ~0ull) {   // masked columns -> -inf (ragged block, kept blocks)
 #pragma unroll
@@ -486,12 +487,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                         c_last = v;
                     }
                     // group sums A_{t,g} (each 32-block half lies in one group)
-                    const int64_t j0 = 64 * (int64_t)v;
-                    const int64_t g0 = j0 / p.G;
+                    const int j0 = 64 * v;
+                    const int g0 = j0 / G32;
                     if (g0 != g_cur) { A_cur = 0.f; g_cur = g0; }
                     A_cur += h0;
-                    if (j0 + 32 < NK) {
-                        const int64_t g1 = (j0 + 32) / p.G;
+                    if (j0 + 32 < NK32) {
+                        const int g1 = (j0 + 32) / G32;
                         if (g1 != g0) { A_done = A_cur; g_done = g0; A_cur = h1; g_cur = g1; }
                         else A_cur += h1;
                     }

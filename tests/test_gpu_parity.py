@@ -350,6 +350,7 @@ def _pairs(H, NQ, heads, nq):
     ("wan13b_480p", "video", [0, 5, 11], 12),
     ("wan14b_720p", "iid", [0, 39], 6),
     ("cogvideox5b", "video", [0, 23, 47], 8),
+    ("hunyuan_720p", "iid", [0, 23], 4),
 ])
 def test_full_config_sampled(pasa, name, gen, heads, nq):
     """BASELINE.json configs at full size, in the launch configuration bench.py
