@@ -37,7 +37,7 @@ typedef enum {
     PASA_EINVAL = 1,        /* bad scalar argument (beta < 0, h = 0, step outside [0,T), ...) */
     PASA_ESHAPE = 2,        /* shape / stride mismatch between tensors or with the handle      */
     PASA_EDTYPE = 3,        /* dtype mismatch                                                    */
-    PASA_EUNSUPPORTED = 4,  /* D not in {64,128}, Bq not in {64,128}, Bk != 64, ...              */
+    PASA_EUNSUPPORTED = 4,  /* D not in {64,128}, Bq not in {64,128,256}, Bk != 64, ...          */
     PASA_EDEGENERATE = 5,   /* l-bar <= 0 (Eq. 10 cannot normalise)                 */
     PASA_ECUDA = 6,         /* a CUDA launch or driver call failed                               */
     PASA_ENOSPACE = 7       /* workspace smaller than the *_workspace_bytes() requirement        */
@@ -91,7 +91,8 @@ typedef enum { PASA_PRIOR_NONE = 0, PASA_PRIOR_GLOBAL = 1, PASA_PRIOR_GROUP = 2 
 
 /* Routing / attention configuration (fixed per route handle). */
 typedef struct {
-    int32_t Bq;              /* query block: 64 or 128 (reading R-7)                           */
+    int32_t Bq;              /* query block: 64, 128 or 256 (reading R-7; 256: bf16 tensor-core 
+                              * attention only)                          */
     int32_t Bk;              /* key block: 64                                                  */
     int32_t G;               /* blocks per group, >= 1 (32 default); G >= N_K = PISA global */
     int32_t comp;            /* pasa_comp                                                      */

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpasa.so")
+LIB_PATH = os.environ.get("PASA_LIB") or os.path.join(_HERE, "lib", "libpasa.so")   # override: A/B builds
 
 PASA_OK, PASA_EINVAL, PASA_ESHAPE, PASA_EDTYPE, PASA_EUNSUPPORTED = 0, 1, 2, 3, 4
 PASA_EDEGENERATE, PASA_ECUDA, PASA_ENOSPACE = 5, 6, 7

@@ -47,8 +47,8 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
     if (!c) return fail(PASA_EINVAL, "route cfg is NULL");
     if (B < 1 || S < 1 || H < 1) return fail(PASA_ESHAPE, "B, S, H must be >= 1");
     if (D != 64 && D != 128) return fail(PASA_EUNSUPPORTED, "D=%lld not in {64,128}", (long long)D);
-    if (c->Bq != 64 && c->Bq != 128)
-        return fail(PASA_EUNSUPPORTED, "Bq=%d not in {64,128}", c->Bq);
+    if (c->Bq != 64 && c->Bq != 128 && c->Bq != 256)
+        return fail(PASA_EUNSUPPORTED, "Bq=%d not in {64,128,256}", c->Bq);
     if (c->Bk != 64) return fail(PASA_EUNSUPPORTED, "Bk=%d != 64", c->Bk);
     if (c->G < 1) return fail(PASA_EINVAL, "G=%d < 1", c->G);
     if (c->comp < 0 || c->comp > 2) return fail(PASA_EINVAL, "comp=%d", c->comp);
@@ -371,6 +371,22 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     // global group); fp32 I/O, Bq = 64 and finer groups run the CUDA-core kernel
     // (documented in include/pasa.h and DESIGN.md §7).
     const pasa_route_cfg& c = route->cfg;
+    if (c.Bq == 256) {
+        // Bq = 256 (NEXT 4 throughput variant) exists only as the tensor-core kernel
+        if (q->dtype != PASA_BF16 || (flags & (PASA_ATTN_FORCE_SIMT | PASA_ATTN_PAIRED |
+                                               PASA_ATTN_PINGPONG)) ||
+            !pasa::attn_sm100_q256_supported(route)) {
+            g_launches = launches;
+            return fail(PASA_EUNSUPPORTED, "Bq = 256 runs only the bf16 tensor-core kernel "
+                        "(d 64 / 128, G a multiple of 32 or >= N_K, no FORCE_SIMT / PAIRED / PINGPONG)");
+        }
+        char why[256] = {0};
+        cudaError_t e = pasa::launch_attn_sm100_q256(*q, *k, *v, route, *out, s, &launches, why,
+                                                     sizeof(why));
+        g_launches = launches;
+        if (e == cudaErrorNotSupported) return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);
+        return cuda_status(e, "attention launch");
+    }
     const bool fine_groups = c.comp == PASA_COMP_GROUPED && !pasa::sm100_supports_group(c.G, route->NK);
     const bool simt = q->dtype == PASA_F32 || (flags & PASA_ATTN_FORCE_SIMT) || c.Bq != 128 ||
                       fine_groups;

@@ -405,17 +405,6 @@ __global__ void __launch_bounds__(kThreads, 2)
                         if (!((valid >> (c + 32)) & 1ull)) sb[c] = 0xff800000u;
                     }
                 }
-                // raw row max (scale > 0 commutes), four independent chains
-                float mr0 = -INFINITY, mr1 = -INFINITY, mr2 = -INFINITY, mr3 = -INFINITY;
-#pragma unroll
-                for (int c = 0; c < 16; c += 2) {
-                    mr0 = fmax3(mr0, __uint_as_float(sa[c]), __uint_as_float(sa[c + 1]));
-                    mr1 = fmax3(mr1, __uint_as_float(sb[c]), __uint_as_float(sb[c + 1]));
-                    mr2 = fmax3(mr2, __uint_as_float(sa[c + 16]), __uint_as_float(sa[c + 17]));
-                    mr3 = fmax3(mr3, __uint_as_float(sb[c + 16]), __uint_as_float(sb[c + 17]));
-                }
-                const float mx = fmaxf(fmax3(mr0, mr1, mr2), mr3) * cs;
-                if (warp == 4 && lane == 0) PASA_TR(TR_SA_MAX, n);
                 // raw logit of the ragged last block (C ops)
                 float xlast = -INFINITY;
                 if (clast >= 0) {
@@ -425,14 +414,59 @@ __global__ void __launch_bounds__(kThreads, 2)
                         if (c + 32 == clast) xlast = __uint_as_float(sb[c]);
                     }
                 }
+                // Exponentials against the current reference m first (FFMA2 for s*x - m,
+                // FADD2 sums).  If the row sum is below 2^8, every x - m < 8, so the rescale
+                // rule (mx > m + 8) cannot fire and the row max is not needed; otherwise
+                // (the first op: m = -inf gives NaN; or a possible new maximum) the exact max
+                // decides as before and the exponentials are redone if m moved.  The m
+                // sequence, and so every P, is the same as with the max taken every op.
+                float h0, h1;
+                uint32_t pk[32];
+                const float2 cs2 = make_float2(cs, cs);
+                auto exps = [&](float mref) {
+                    const float2 nm2 = make_float2(-mref, -mref);
+                    float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const float2 xa = ffma2(make_float2(__uint_as_float(sa[2 * c]),
+                                                            __uint_as_float(sa[2 * c + 1])), cs2, nm2);
+                        const float2 xb = ffma2(make_float2(__uint_as_float(sb[2 * c]),
+                                                            __uint_as_float(sb[2 * c + 1])), cs2, nm2);
+                        const float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
+                        a0 = fadd2(a0, make_float2(p0, p1));
+                        a1 = fadd2(a1, make_float2(p2, p3));
+                        pk[c] = pack_bf16(p0, p1);
+                        pk[16 + c] = pack_bf16(p2, p3);
+                    }
+                    h0 = a0.x + a0.y;
+                    h1 = a1.x + a1.y;
+                };
+                exps(m);
                 float corr = 1.f;
                 bool resc = false;
-                if (mx > m + kRescaleThresh) {
-                    corr = ex2(m - mx);       // 0 when m = -inf
-                    resc = n > 0;
-                    m = mx;
-                    l *= corr;
-                    A_cur *= corr;
+                if (__any_sync(0xffffffffu, !(h0 + h1 < 256.f))) {
+                    // raw row max (scale > 0 commutes), four independent chains
+                    float mr0 = -INFINITY, mr1 = -INFINITY, mr2 = -INFINITY, mr3 = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < 16; c += 2) {
+                        mr0 = fmax3(mr0, __uint_as_float(sa[c]), __uint_as_float(sa[c + 1]));
+                        mr1 = fmax3(mr1, __uint_as_float(sb[c]), __uint_as_float(sb[c + 1]));
+                        mr2 = fmax3(mr2, __uint_as_float(sa[c + 16]), __uint_as_float(sa[c + 17]));
+                        mr3 = fmax3(mr3, __uint_as_float(sb[c + 16]), __uint_as_float(sb[c + 17]));
+                    }
+                    const float mx = fmaxf(fmax3(mr0, mr1, mr2), mr3) * cs;
+                    if (warp == 4 && lane == 0) PASA_TR(TR_SA_MAX, n);
+                    const bool moved = mx > m + kRescaleThresh;
+                    if (moved) {
+                        corr = ex2(m - mx);       // 0 when m = -inf
+                        resc = n > 0;
+                        m = mx;
+                        l *= corr;
+                        A_cur *= corr;
+                    }
+                    // warp-uniform redo (lanes whose m did not move recompute the same
+                    // values): no divergent path around the warp-collective TMEM store
+                    if (__any_sync(0xffffffffu, moved)) exps(m);
                 }
                 if (__any_sync(0xffffffffu, resc)) {
                     consume_op(n - 2);
@@ -448,20 +482,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                         tmem_st32(t_o + c0, o);
                     }
                 }
-                float h0 = 0.f, h1 = 0.f;
-                uint32_t pk[32];
                 const float negm = -m;
-#pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    const float p0 = ex2(fmaf(__uint_as_float(sa[2 * c]), cs, negm));
-                    const float p1 = ex2(fmaf(__uint_as_float(sa[2 * c + 1]), cs, negm));
-                    const float p2 = ex2(fmaf(__uint_as_float(sb[2 * c]), cs, negm));
-                    const float p3 = ex2(fmaf(__uint_as_float(sb[2 * c + 1]), cs, negm));
-                    h0 += p0 + p1;
-                    h1 += p2 + p3;
-                    pk[c] = pack_bf16(p0, p1);
-                    pk[16 + c] = pack_bf16(p2, p3);
-                }
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_EXP, n);
                 tmem_st32(t_buf, pk);
                 if (type == OP_E) {
@@ -514,9 +535,15 @@ __global__ void __launch_bounds__(kThreads, 2)
                 }
                 const float w = p.s * A;
                 const uint32_t w2 = pack_bf16(w, w);
-                // the buffer's previous reader (op n-NB) has finished: with NB = 2 that is
-                // the latest op of its parity; with NB = 3 wait for op n-1 (covers n-3)
-                consume_op(G_::NB == 2 ? n - 2 : n - 1);
+                // the buffer's previous reader (op n-NB) has finished: wait for op n-2 (PVs
+                // complete in order, so this covers n-3 at NB = 3).  Not n-1: a parity wait is
+                // exact only while the barrier is at most one phase behind, and on entry to an
+                // F op only PV(n-4) is known complete (an F op has no s_full wait; the previous
+                // op's S(n-1) was computed by a QK issued before PV(n-3)), so pv_done[(n-1)&1]
+                // may still be at op n-3's phase -- a wait for n-1 would then pass at once
+                // (the round-1 d = 64 hang / NaN under changed softmax timing).  Op n-2 is
+                // safe: its predecessor on the barrier, n-4, is complete.
+                consume_op(n - 2);
                 tc_fence_after();
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {

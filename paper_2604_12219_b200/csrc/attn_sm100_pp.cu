@@ -511,7 +511,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ctl.lpart[wg][r] = l;
         bar_sync(kBarEpi, 256);
         const float inv = 1.f / (ctl.lpart[0][r] + ctl.lpart[1][r]);
-        consume_op(nops - 2);
+        // every PV done.  Parity waits are exact only while the barrier is at most one phase
+        // behind: this warpgroup's last op guarantees PV(nops-6) complete, so first wait for
+        // op nops-4 (its predecessor on the barrier, nops-8, is complete), which completes
+        // every PV up to nops-4 and makes the wait for nops-1 exact.
+        consume_op(nops - 4);
         consume_op(nops - 1);
         tc_fence_after();
         const int t = i * kBQ + r;

@@ -92,6 +92,12 @@ bool attn_sm100_pp_supported(const pasa_route_s* r);
 cudaError_t launch_attn_sm100_pp(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                                  pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                                  int* launches, char* why, size_t why_len);
+// Bq = 256: one CTA per SM, two 128-row tiles sharing every
+// operand tile the op brings from L2; attn_sm100_q256.cu
+bool attn_sm100_q256_supported(const pasa_route_s* r);
+cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                                   pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                                   int* launches, char* why, size_t why_len);
 // variant: one CTA per SM, kept blocks processed in pairs (N = 128 QK^T), two
 // independent softmax warpgroups (PASA_ATTN_PAIRED)
 cudaError_t launch_attn_sm100_pair(const pasa_tensor& q, const pasa_tensor& k,

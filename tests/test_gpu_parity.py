@@ -255,6 +255,51 @@ def test_attn_parity_pingpong(pasa, case):
     assert torch.equal(out, pasa.attn(q, k, v, route, pingpong=True))
 
 
+Q256_CASES = [
+    # Bq = 256: one route per 256 queries, two 128-row M tiles
+    # sharing every K/V / centroid / Hbar tile
+    ("q256_d128_1000", 1, 1000, 2, 128, 256, 32, "grouped", 0.15, torch.bfloat16, "iid"),
+    ("q256_d128_4100_g32", 1, 4100, 2, 128, 256, 32, "grouped", 0.15, torch.bfloat16, "video"),
+    ("q256_d64_4100_g32", 2, 4100, 2, 64, 256, 32, "grouped", 0.15, torch.bfloat16, "video"),
+    ("q256_d128_4100_g64", 1, 4100, 2, 128, 256, 64, "grouped", 0.15, torch.bfloat16, "video"),
+    ("q256_d128_4100_global", 1, 4100, 2, 128, 256, 4096, "grouped", 0.15, torch.bfloat16, "iid"),
+    ("q256_d128_4100_zeroth", 1, 4100, 2, 128, 256, 32, "zeroth", 0.15, torch.bfloat16, "video"),
+    ("q256_d64_4100_none", 1, 4100, 2, 64, 256, 32, "none", 0.15, torch.bfloat16, "iid"),
+    ("q256_d128_20000_g128", 1, 20000, 1, 128, 256, 128, "grouped", 0.15, torch.bfloat16, "video"),
+    ("q256_d64_9000_odd_k", 1, 9000, 2, 64, 256, 32, "grouped", 0.11, torch.bfloat16, "iid"),
+]
+
+
+@pytest.mark.parametrize("case", Q256_CASES, ids=[c[0] for c in Q256_CASES])
+def test_attn_parity_q256(pasa, case):
+    """Bq = 256 routing (bit-exact against the oracle's route at Bq = 256) and the
+    two-tile tensor-core kernel against the oracle's attention at Bq = 256."""
+    name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
+    q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=13)
+    cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, rho)
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg)
+    assert torch.equal(out, pasa.attn(q, k, v, route))
+
+
+@pytest.mark.parametrize("S", [1, 100, 256, 257, 511, 640])
+def test_attn_q256_edges(pasa, S):
+    """Bq = 256 around the tile edges: a q-block with only tile 0 live, exactly one
+    q-block, one row past it, and k = 1."""
+    q, k, v = synth.iid_qkv(1, S, 2, 128, seed=S + 7, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=256, G=32, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, 0.3 if S > 64 else 1.0)
+    check_attn(pasa, q, k, v, route, got, cfg)
+
+
+def test_attn_q256_rejects_unsupported(pasa):
+    q, k, v = synth.iid_qkv(1, 1000, 1, 64, seed=3, dtype=torch.float32, device="cuda")
+    route = pasa.Route(1, 1000, 1, 64, pasa.RouteCfg(Bq=256, G=32))
+    route(q, k, make_budget(pasa, 0.3), 1, 25)
+    with pytest.raises(pasa.PasaError):
+        pasa.attn(q, k, v, route)
+
+
 EDGE_CASES = [
     # name, S, D, Bq, rho, dtype: degenerate lengths around the block sizes, k = 1
     ("S1", 1, 128, 128, 0.15, torch.bfloat16),
@@ -394,3 +439,20 @@ def test_full_config_repeat_finite_bitwise(pasa, name, pingpong):
             first = out
         else:
             assert torch.equal(out, first)
+
+
+def test_full_config_q256_sampled(pasa):
+    """Wan 2.1-14B 720p at full size with Bq = 256: route bit-exact on two heads,
+    attention on sampled (head, q-block) pairs incl. the ragged last one, whole output
+    finite and bitwise reproducible."""
+    c = synth.CONFIGS["wan14b_720p"]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    q, k, v = synth.iid_qkv(B, S, H, D, seed=1005, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=256, G=c["G"], beta=0.1)
+    heads = [0, 39]
+    route, got, ties = check_route(pasa, q, k, cfg, c["rho"], seed=pasa.layer_seed(42, 0),
+                                   step=25, heads=heads)
+    assert ties <= 4
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, route.NQ, heads, 5))
+    assert bool(torch.isfinite(out).all())
+    assert torch.equal(out, pasa.attn(q, k, v, route))
