@@ -12,7 +12,12 @@ timeout 600 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_
 for c in wan13b_480p cogvideox5b hunyuan_720p; do
   timeout 400 python bench.py --config "$c" --no-cpu > "gpurun_out/bench_$c.json" 2> "gpurun_out/bench_$c.err"
 done
+timeout 400 python bench.py --config cogvideox5b --schedule --no-cpu --no-e2e > gpurun_out/bench_cogvideox5b_schedule.json 2> gpurun_out/bench_cogvideox5b_schedule.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+# power / clock per attention variant (the long configs run under the 1000 W cap)
+timeout 300 python tools/power_probe.py > gpurun_out/power_wan14b.txt 2>&1
+CFG=cogvideox5b SECS=3 timeout 200 python tools/power_probe.py > gpurun_out/power_cogvideox5b.txt 2>&1
+timeout 300 python tools/q256_time.py > gpurun_out/q256_wan14b.txt 2>&1
 # launch list (serialised, cold cache: only the shares are comparable with bench.py)
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none \
   -k regex:'budget|pool|scores|select|stats|attn|rowstats' -c 16 --csv \
