@@ -256,13 +256,16 @@ def run_pasa(args):
 
     cfg = synth.CONFIGS[args.config]
     B, S, H, D = cfg["B"], cfg["S"], cfg["H"], cfg["D"]
-    if H % world:
-        raise SystemExit(f"{H} heads do not split over {world} ranks")
-    Hl = H // world
-    off = rank * Hl
-    dev = torch.device("cuda", torch.cuda.current_device())
+    from paper_2604_12219_b200 import dist as pdist
     seq_sharded = (args.seq_sharded == "yes"
                    or (args.seq_sharded == "auto" and args.config == "hunyuan_720p"))
+    # contiguous head partition (uneven allowed, e.g. 12 heads over 8 ranks); the
+    # Ulysses all-to-all of sequence-sharded input needs equal head chunks
+    try:
+        off, Hl = pdist.head_range(H, world, rank, even=seq_sharded)
+    except ValueError as exc:
+        raise SystemExit(str(exc))
+    dev = torch.device("cuda", torch.cuda.current_device())
     if seq_sharded and S % world:
         raise SystemExit(f"S = {S} does not split over {world} ranks")
     # every global head drawn from its own seed: the same data for any N
@@ -279,7 +282,6 @@ def run_pasa(args):
     if seq_sharded:
         # sequence-sharded input [B, S/P, H, D]: the step starts with the Ulysses
         # all-to-all to this rank's heads and ends with the inverse
-        from paper_2604_12219_b200 import dist as pdist
         q_s, k_s, v_s = q, k, v
         to_heads = (lambda t: pdist.seq_to_head(t)) if world > 1 else (lambda t: t)
         to_seq = (lambda t: pdist.head_to_seq(t)) if world > 1 else (lambda t: t)
@@ -506,13 +508,17 @@ def run_pasa(args):
         bq.record(stream)
         torch.cuda.synchronize()
         te = a.elapsed_time(bq) / n_e2e
+        h2d_all, d2h_all = h2d, d2h
         if world > 1:
             tt = torch.tensor([te], device=dev, dtype=torch.float64)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             te = float(tt[0])
+            nb = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)   # uneven heads
+            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
+            h2d_all, d2h_all = float(nb[0]), float(nb[1])
         e2e = {"value": 4.0 * S * S * D * B * H / (te * 1e-3) / 1e12, "unit": UNIT,
-               "ms_per_step": te, "h2d_bytes_per_step": int(h2d * world),
-               "d2h_bytes_per_step": int(d2h * world), "steps": n_e2e,
+               "ms_per_step": te, "h2d_bytes_per_step": int(h2d_all),
+               "d2h_bytes_per_step": int(d2h_all), "steps": n_e2e,
                "head_chunks": args.e2e_chunks}
 
     if rank != 0:

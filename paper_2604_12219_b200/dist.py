@@ -20,12 +20,19 @@ import torch
 import torch.distributed as dist
 
 
-def head_range(H: int, world: int, rank: int):
-    """Contiguous head partition: returns (head_offset, local_heads)."""
-    if H % world:
+def head_range(H: int, world: int, rank: int, even: bool = False):
+    """Contiguous head partition: rank r owns global heads [floor(r H / P),
+    floor((r+1) H / P)); returns (head_offset, local_heads).  Uneven splits are
+    allowed (Wan-1.3B's 12 heads over 8 ranks: 1, 2, 1, 2, ...) unless
+    ``even`` (the Ulysses all-to-all needs equal head chunks)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} of world {world}")
+    if even and H % world:
         raise ValueError(f"{H} heads do not split evenly over {world} ranks")
-    n = H // world
-    return rank * n, n
+    if H < world:
+        raise ValueError(f"{H} heads cannot give each of {world} ranks a head")
+    off = H * rank // world
+    return off, H * (rank + 1) // world - off
 
 
 def seq_to_head(x: torch.Tensor, group=None) -> torch.Tensor:
@@ -67,7 +74,7 @@ def ulysses_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     P = dist.get_world_size(group)
     r = dist.get_rank(group)
     H = q.shape[2]
-    off, _ = head_range(H, P, r)
+    off, _ = head_range(H, P, r, even=True)
     qh, kh, vh = (seq_to_head(t, group) for t in (q, k, v))
     oh = local_attn(qh, kh, vh, off, H)
     return head_to_seq(oh, group)

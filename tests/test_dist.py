@@ -57,8 +57,49 @@ def _worker(rank, world, port, q, k, v, ref, errs):
 def test_head_range():
     assert pdist.head_range(40, 8, 3) == (15, 5)
     assert pdist.head_range(24, 4, 0) == (0, 6)
+    # uneven (Wan-1.3B: 12 heads over 8 ranks): contiguous, disjoint, covering
+    parts = [pdist.head_range(12, 8, r) for r in range(8)]
+    assert [n for _, n in parts] == [1, 2, 1, 2, 1, 2, 1, 2]
+    assert all(parts[r][0] + parts[r][1] == parts[r + 1][0] for r in range(7))
+    assert parts[-1][0] + parts[-1][1] == 12
     with pytest.raises(ValueError):
-        pdist.head_range(12, 8, 0)
+        pdist.head_range(12, 8, 0, even=True)
+    with pytest.raises(ValueError):
+        pdist.head_range(4, 8, 0)
+
+
+def _uneven_worker(rank, world, port, q, k, v, ref, errs):
+    """Uneven head partition (3 heads over 2 ranks): each rank runs PASA on its own
+    heads with Philox keyed on the global head; the gathered result equals the
+    single-process one exactly."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, S, H, D = q.shape
+        off, Hl = pdist.head_range(H, world, rank)
+        hs = slice(off, off + Hl)
+        mine = _oracle_pasa(q[:, :, hs].contiguous(), k[:, :, hs].contiguous(),
+                            v[:, :, hs].contiguous(), off, H).reshape(B, S, Hl, D)
+        parts = []
+        for r in range(world):                    # uneven shards: one broadcast per rank
+            n = pdist.head_range(H, world, r)[1]
+            buf = mine.contiguous() if r == rank else torch.empty(B, S, n, D, dtype=mine.dtype)
+            dist.broadcast(buf, src=r)
+            parts.append(buf)
+        errs[rank] = float((torch.cat(parts, 2) - ref).abs().max())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_uneven_head_partition_gloo_world2():
+    g = torch.Generator().manual_seed(1)
+    B, S, H, D = 1, 256, 3, 8
+    q, k, v = (torch.randn(B, S, H, D, generator=g, dtype=torch.float64) for _ in range(3))
+    ref = _oracle_pasa(q, k, v, 0, H)
+    errs = mp.Manager().dict()
+    mp.spawn(_uneven_worker, args=(2, _free_port(), q, k, v, ref, errs), nprocs=2, join=True)
+    assert errs[0] == 0.0 and errs[1] == 0.0
 
 
 def test_ulysses_gloo_world2_matches_single_process():
