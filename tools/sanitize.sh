@@ -12,3 +12,7 @@ tail -3 gpurun_out/san_memcheck2.log; grep "ERROR SUMMARY" gpurun_out/san_memche
 timeout 900 compute-sanitizer --tool racecheck --print-limit 20 --log-file gpurun_out/san_race.txt \
   python -m pytest tests/test_gpu_parity.py -q -x -k "ragged1000 or iid16k or clustered" > gpurun_out/san_race.log 2>&1
 tail -3 gpurun_out/san_race.log; grep "ERROR SUMMARY\|RACECHECK SUMMARY" gpurun_out/san_race.txt | head
+# the round's attention variants: ping-pong (one CTA/SM, Q in TMEM) and Bq = 256 (two tiles)
+timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 --log-file gpurun_out/san_memcheck3.txt \
+  python -m pytest tests/test_gpu_parity.py -q -x -k "pingpong and (tc_d128_4100_g32 or tc_d64_4100_g32 or S65 or k1) or q256_d128_4100_g32 or q256_d64_4100_g32 or q256_d128_20000 or test_attn_q256_edges" > gpurun_out/san_memcheck3.log 2>&1
+tail -3 gpurun_out/san_memcheck3.log; grep "ERROR SUMMARY" gpurun_out/san_memcheck3.txt | head
