@@ -281,7 +281,10 @@ struct SelArgs {
 };
 
 template <int MAXM>
-__global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 2) select_kernel(SelArgs a) {
+// occupancy over registers: a few spilled keys cost less than idle warps (route at
+// Wan-14B 1.52 -> 1.34 ms with 5 CTAs/SM for MAXM <= 40; HunyuanVideo's MAXM = 64
+// 2.70 -> 2.03 ms with 4 instead of 2 CTAs/SM, 3, 5 and 6 measured slower)
+__global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 4) select_kernel(SelArgs a) {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);   // bh * NQ + i
     if (row >= a.rows) return;
