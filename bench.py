@@ -516,10 +516,25 @@ def run_pasa(args):
             nb = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)   # uneven heads
             dist.all_reduce(nb, op=dist.ReduceOp.SUM)
             h2d_all, d2h_all = float(nb[0]), float(nb[1])
+        # the e2e roofline: this rank's pinned-host -> device copy bandwidth, measured with
+        # one contiguous 512 MB copy (best of 3), and the step's H2D bytes at that rate
+        hb = torch.empty(1 << 28, dtype=torch.bfloat16, pin_memory=True)
+        db = torch.empty(1 << 28, dtype=torch.bfloat16, device=dev)
+        bw = 0.0
+        for _ in range(3):
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
+            db.copy_(hb, non_blocking=True)
+            c1.record(stream)
+            torch.cuda.synchronize()
+            bw = max(bw, hb.numel() * 2 / (c0.elapsed_time(c1) * 1e-3) / 1e9)
+        del hb, db
         e2e = {"value": 4.0 * S * S * D * B * H / (te * 1e-3) / 1e12, "unit": UNIT,
                "ms_per_step": te, "h2d_bytes_per_step": int(h2d_all),
                "d2h_bytes_per_step": int(d2h_all), "steps": n_e2e,
-               "head_chunks": args.e2e_chunks}
+               "head_chunks": args.e2e_chunks,
+               "pcie_h2d_gbs": bw, "h2d_bound_ms": h2d / (bw * 1e9) * 1e3,
+               "frac_of_h2d_bound": (h2d / (bw * 1e9) * 1e3) / te}
 
     if rank != 0:
         if world > 1:
