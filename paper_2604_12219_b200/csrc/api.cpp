@@ -378,7 +378,7 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
             !pasa::attn_sm100_q256_supported(route)) {
             g_launches = launches;
             return fail(PASA_EUNSUPPORTED, "Bq = 256 runs only the bf16 tensor-core kernel "
-                        "(d 64 / 128, G a multiple of 32 or >= N_K, no FORCE_SIMT / PAIRED / PINGPONG)");
+                        "(d 64 / 128, G in {32, 64, k*128, >= N_K}, no FORCE_SIMT / PAIRED / PINGPONG)");
         }
         char why[256] = {0};
         cudaError_t e = pasa::launch_attn_sm100_q256(*q, *k, *v, route, *out, s, &launches, why,

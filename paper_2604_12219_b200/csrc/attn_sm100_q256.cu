@@ -17,8 +17,8 @@
 // twice, once per tile, on the same shared-memory B operand.
 // Warp roles (384 threads): warp 0 K-ring TMA producer, warp 1 TMEM allocator +
 // MMA issuer, warp 2 V-ring TMA producer, warp 3 idle, warps 4-11 softmax.
-// Domain: bf16, Bq = 256, Bk = 64, d = 64 or 128, G % 32 == 0 (up to one
-// global group) or no grouped term.
+// Domain: bf16, Bq = 256, Bk = 64, d = 64 or 128, G in {32, 64, multiples of 128,
+// >= N_K} or no grouped term.
 #include <cuda.h>
 #include <cuda_bf16.h>
 
@@ -534,7 +534,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
 
 bool attn_sm100_q256_supported(const pasa_route_s* r) {
     return r->cfg.Bq == kBQ && r->cfg.Bk == kBK && (r->D == 128 || r->D == 64) && r->W <= 64 &&
-           (r->cfg.comp != PASA_COMP_GROUPED || r->cfg.G % 32 == 0 || r->cfg.G >= r->NK);
+           (r->cfg.comp != PASA_COMP_GROUPED || r->cfg.G == 32 || r->cfg.G == 64 ||
+            r->cfg.G % 128 == 0 || r->cfg.G >= r->NK);   // the attn_sm100.cu group set minus 8, 16
 }
 
 cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
@@ -542,7 +543,7 @@ cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, c
                                    int* launches, char* why, size_t why_len) {
     if (!attn_sm100_q256_supported(r)) {
         snprintf(why, why_len, "Bq = 256 kernel: needs Bk=64, d in {64, 128}, N_K <= 2048, "
-                 "G a multiple of 32 (or >= N_K) for grouped compensation");
+                 "G in {32, 64, multiples of 128, >= N_K} for grouped compensation");
         return cudaErrorNotSupported;
     }
     cudaError_t e = r->D == 128 ? launch_d<128>(q, k, v, r, out, st, why, why_len)
