@@ -5,9 +5,11 @@
 // R-21, R-22); what changes is the data movement: every operand tile an op brings
 // from L2 (K_j + V_j, a Kbar / Vsum chunk, or Hbar^(g)T) feeds TWO 128-row M tiles.
 //
-// Why: at Bq = 128 every op costs ~1,000 SM cycles whatever its softmax or MMA
-// work, in step with the 32 KB tile it brings from L2 (DESIGN.md §7,
-// profiles/r01_attn_pingpong.md).  Here one CTA per SM owns the SM's 512 TMEM
+// Built to test whether the L2 bytes per FLOP bound the Bq = 128 kernel (every op
+// costs ~1,000 SM cycles whatever its softmax or MMA work): it halves them, and is
+// slower (24.1 vs 22.6 ms at Wan-14B), because that launch runs at the board power
+// limit and this layout spends more energy per launch (DESIGN.md §7,
+// profiles/r01_attn_power.md).  Here one CTA per SM owns the SM's 512 TMEM
 // columns as two independent halves, tile t in {0, 1} at column 256 t:
 //   O_t (D columns) + two S/P buffers of 64 columns,
 // and two softmax warpgroups (warps 4-7: rows 0-127, warps 8-11: rows 128-255),
