@@ -13,6 +13,10 @@
 // of 64.  Op n uses buffer / K slot / V slot n % 4 and is worked on by softmax
 // warpgroup n % 2, so each warpgroup has the S of its next op computed while it
 // works on the current one, and QK(n+4) is issued right after PV(n).
+// Measured (PASA_ATTN_PINGPONG, parity-tested): slower than the default kernel
+// (25.3 vs 22.6 ms at Wan-14B, 1.45 vs 1.18 ms at CogVideoX): the Wan-14B launch
+// runs at the board power limit and this layout spends more energy per launch
+// (profiles/r01_attn_power.md).
 //
 // What the two warpgroups share, and how:
 //   * the running max m.  It is the same sequential rule as the single-warpgroup
