@@ -416,9 +416,9 @@ def test_full_config_sampled(pasa, name, gen, heads, nq):
     check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, NQ, heads, nq))
 
 
-@pytest.mark.parametrize("pingpong", [False, True], ids=["default", "pingpong"])
+@pytest.mark.parametrize("variant", ["default", "pingpong", "q256"])
 @pytest.mark.parametrize("name", ["wan13b_480p", "cogvideox5b", "wan14b_720p", "hunyuan_720p"])
-def test_full_config_repeat_finite_bitwise(pasa, name, pingpong):
+def test_full_config_repeat_finite_bitwise(pasa, name, variant):
     """Every BASELINE config at full size in bench.py's launch configuration, three
     times: the whole output is finite and bitwise identical run to run.  (A barrier
     lapped by a softmax running two ops ahead at d = 64 once let PV read an unloaded
@@ -426,13 +426,13 @@ def test_full_config_repeat_finite_bitwise(pasa, name, pingpong):
     c = synth.CONFIGS[name]
     B, S, H, D = c["B"], c["S"], c["H"], c["D"]
     q, k, v = synth.iid_qkv(B, S, H, D, seed=1004, dtype=torch.bfloat16, device="cuda")
-    cfg = pasa.RouteCfg(Bq=c["Bq"], G=c["G"], beta=0.1)
+    cfg = pasa.RouteCfg(Bq=256 if variant == "q256" else c["Bq"], G=c["G"], beta=0.1)
     route = pasa.Route(B, S, H, D, cfg)
     route(q, k, make_budget(pasa, c["rho"]), pasa.layer_seed(42, 0), 25)
     first = None
     for _ in range(3):
         out = torch.full_like(q, float("nan"))
-        pasa.attn(q, k, v, route, out, pingpong=pingpong)
+        pasa.attn(q, k, v, route, out, pingpong=variant == "pingpong")
         torch.cuda.synchronize()
         assert bool(torch.isfinite(out).all())
         if first is None:
