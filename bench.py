@@ -557,6 +557,18 @@ def run_pasa(args):
     except (OSError, ValueError):
         pass
     value = 4.0 * S * S * D * B * H / (t_max * 1e-3) / 1e12
+    # secondary roofline of the attention kernel: its exponentials on the MUFU pipe
+    # (16 ex2 / clk / SM measured, tools/mufu_bench.cu; 128 x 64 per E or C op, the C ops
+    # being every 64-block chunk with a dropped block -- all of them at these densities)
+    clocks = clk.summary()
+    n_c = 0 if kk >= NK else (NK + 63) // 64
+    n_exp = B * Hl * route.NQ * (kk + n_c) * 128 * 64
+    f_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    mufu = {"bound": "mufu", "achieved": n_exp / (t_attn * 1e-3) / 1e12,
+            "peak": 16 * 148 * f_hz / 1e12, "unit": "Tex2/s",
+            "peak_kind": "16 ex2/clk/SM x 148 SMs at the sampled median SM clock",
+            "exps_per_launch": n_exp}
+    mufu["frac"] = mufu["achieved"] / mufu["peak"]
     cpu = None
     if not args.no_cpu and world == 1:   # the oracle baseline: rank 0 at N = 1 only
         cv, secs, desc, _ = oracle_sample(cfg, args.cpu_qblocks)
@@ -587,7 +599,8 @@ def run_pasa(args):
                      "peak": peak, "peak_kind": f"bf16 dense, sustained ({which})",
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "flops_per_launch": attn_flops},
-        "clocks": clk.summary(),
+        "roofline_mufu": mufu,
+        "clocks": clocks,
         "gpu_launches": gpu_launches,
         "e2e": e2e,
         "graph": graph,
