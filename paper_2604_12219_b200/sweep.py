@@ -41,7 +41,7 @@ def rel_fro(a, b):
     return float((a.float() - b).norm() / b.norm())
 
 
-def run(q, k, v, *, rho=0.15, beta=0.1, seed=42, step=25, reps=5):
+def run(q, k, v, *, rho=0.15, beta=0.1, seed=42, step=25, reps=5, bq256=False):
     B, S, H, D = q.shape
     NK = (S + 63) // 64
     dense = dense_reference(q, k, v)
@@ -68,6 +68,21 @@ def run(q, k, v, *, rho=0.15, beta=0.1, seed=42, step=25, reps=5):
                          "attn_ms": e0.elapsed_time(e1) / reps,
                          "kernel": "tcgen05" if g in (8, 16, 32, 64) or g % 128 == 0 or g >= NK
                          else "cuda-core"})
+    if bq256:
+        # routing granularity (NEXT 4 / reading R-29): one kept set per 256 queries
+        for comp in COMPS:
+            route = Route(B, S, H, D, RouteCfg(Bq=256, G=32, comp=comp, beta=beta))
+            route(q, k, budget, seed, step)
+            out = attn(q, k, v, route)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(reps):
+                attn(q, k, v, route, out)
+            e1.record()
+            torch.cuda.synchronize()
+            rows.append({"G": 32, "comp": comp, "Bq": 256, "rel_frobenius": rel_fro(out, dense),
+                         "attn_ms": e0.elapsed_time(e1) / reps, "kernel": "tcgen05 (Bq 256)"})
     return rows
 
 
@@ -80,6 +95,8 @@ def main(argv=None) -> int:
     ap.add_argument("--seeds", type=int, default=4)
     ap.add_argument("--generator", default="correlated", choices=["correlated", "video"])
     ap.add_argument("--out", default=None)
+    ap.add_argument("--bq256", action="store_true",
+                    help="also route at Bq = 256 (G = 32, all three modes)")
     a = ap.parse_args(argv)
     import synth
     per_seed = []
@@ -90,12 +107,12 @@ def main(argv=None) -> int:
             F = max(1, a.S // (32 * 32))
             q, k, v = synth.video_qkv(1, (F, 32, a.S // (32 * F)), a.H, a.D, seed=seed,
                                       device="cuda")
-        per_seed.append(run(q, k, v, rho=a.rho))
+        per_seed.append(run(q, k, v, rho=a.rho, bq256=a.bq256))
     table = []
     for n, r in enumerate(per_seed[0]):
         errs = [ps[n]["rel_frobenius"] for ps in per_seed]
         ms = [ps[n]["attn_ms"] for ps in per_seed]
-        table.append({"G": r["G"], "comp": r["comp"], "kernel": r["kernel"],
+        table.append({"G": r["G"], "comp": r["comp"], "Bq": r.get("Bq", 128), "kernel": r["kernel"],
                       "rel_frobenius_mean": float(np.mean(errs)),
                       "rel_frobenius_std": float(np.std(errs)),
                       "attn_ms_median": float(np.median(ms))})
