@@ -57,9 +57,9 @@ def parse():
     ap.add_argument("--schedule", action="store_true",
                     help="also run the 50-step budget schedule (online budget from the "
                          "three-phase synthetic trajectory): per-step k_t, ms and their sum")
-    ap.add_argument("--e2e-chunks", type=int, default=20,
-                    help="head chunks of the host pipeline (copies overlapped with compute); "
-                         "1 = copy everything, compute, copy back")
+    ap.add_argument("--e2e-chunks", type=int, default=0,
+                    help="head chunks of the host pipeline for e2e (1 = serial copy/compute; "
+                         "0 = auto: about one chunk per 0.12 ms of device step, 4..20)")
     ap.add_argument("--prior", default="none", choices=["none", "global", "group"],
                     help="Eq. 8 heterogeneity prior in routing (SURVEY.md §8f NEXT 1; off in "
                          "the north-star path)")
@@ -460,6 +460,9 @@ def run_pasa(args):
         hout = torch.empty(src[0].shape, dtype=out.dtype, pin_memory=True)
         h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
         d2h = hout.numel() * hout.element_size()
+        # head chunks: about one per 0.12 ms of device step (enough work per chunk to fill
+        # the GPU and hide the per-chunk launches; Wan-14B 20, CogVideoX / Wan-1.3B 12)
+        n_chunks = args.e2e_chunks or max(4, min(20, round(t_max / 0.12)))
         if seq_sharded and world > 1:
             # host shards -> device -> all-to-all -> PASA -> all-to-all -> host shard
             dsq, dsk, dsv = (torch.empty_like(t) for t in src)
@@ -474,11 +477,11 @@ def run_pasa(args):
                 route(qh, kh, budget, seed, t_step, v=vh if use_v else None)
                 P.attn(qh, kh, vh, route, out)
                 hout.copy_(to_seq(out), non_blocking=True)
-        elif args.e2e_chunks > 1:
+        elif n_chunks > 1:
             # public API for host-resident tensors: head chunks on copy-in / compute /
             # copy-out streams (paper_2604_12219_b200.pipeline)
             from paper_2604_12219_b200.pipeline import HostPipeline
-            pipe = HostPipeline(B, S, Hl, D, rcfg, n_chunks=args.e2e_chunks, device=dev)
+            pipe = HostPipeline(B, S, Hl, D, rcfg, n_chunks=n_chunks, device=dev)
 
             def e2e_step():
                 pipe(hq, hk, hv, hout, hx, seed, t_step, v_for_prior=use_v, T=50,
@@ -532,7 +535,7 @@ def run_pasa(args):
         e2e = {"value": 4.0 * S * S * D * B * H / (te * 1e-3) / 1e12, "unit": UNIT,
                "ms_per_step": te, "h2d_bytes_per_step": int(h2d_all),
                "d2h_bytes_per_step": int(d2h_all), "steps": n_e2e,
-               "head_chunks": args.e2e_chunks,
+               "head_chunks": n_chunks,
                "pcie_h2d_gbs": bw, "h2d_bound_ms": h2d / (bw * 1e9) * 1e3,
                "frac_of_h2d_bound": (h2d / (bw * 1e9) * 1e3) / te}
 
