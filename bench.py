@@ -85,7 +85,7 @@ def algorithmic_flops_per_head(S, D, NK, NG, k, Bk=64):
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled during the timed region."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw.instant,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -146,7 +146,7 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm.sort()
         watts.sort()
-        # board power: the long configs run at the 1,000 W limit (sw_power_cap), where the
+        # board power (instant samples): the long configs run at the 1,000 W limit (sw_power_cap), where the
         # step time is the step's energy / power
         return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm), "power_w": watts[len(watts) // 2] if watts else None}
