@@ -183,9 +183,12 @@ pasa_status pasa_route_v(const pasa_tensor* q, const pasa_tensor* k, const pasa_
  *   A_{t,g} = sum_{j in U_i cap G_g} e^{s q.Kbar_j - m}; comp ZEROTH drops the
  *   Hbar term, NONE drops every U term.  q and k must be the buffers the route
  *   was built from; v and out have the same B,S,H,D (out may have its own
- *   strides).  bf16 I/O with Bq = 128 and G % 32 == 0 (or G >= N_K) runs the
- *   tcgen05/TMEM/TMA kernel (fp32 accumulate; Kbar, Vsum, Hbar stored bf16,
- *   R-21); fp32 I/O, Bq = 64 or finer groups run the fp32 CUDA-core kernel.
+ *   strides).  bf16 I/O with Bq = 128 and G in {8, 16, 32, 64, multiples of 128,
+ *   >= N_K} runs the tcgen05/TMEM/TMA kernel (fp32 accumulate; Kbar, Vsum, Hbar
+ *   stored bf16, R-21); Bq = 256 (R-29) runs the two-tile tcgen05 kernel (bf16,
+ *   G in {32, 64, multiples of 128, >= N_K}; anything else at Bq = 256 is
+ *   EUNSUPPORTED); fp32 I/O, Bq = 64 or other group sizes run the fp32 CUDA-core
+ *   kernel.
  *   Errors: ESHAPE, EDTYPE, EINVAL (route never built). */
 pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                       pasa_route_h route, pasa_tensor* out, void* stream);
