@@ -115,8 +115,10 @@ size_t pasa_budget_workspace_bytes(void);
 /* Route workspace for tensors of shape [B, S, H, D]: pooled Qbar/Kbar (fp64),
  * the low-precision Kbar / Vsum / grouped Hbar used by pasa_attn, the index
  * list idx [B*H][N_Q][N_K] int32 (first count entries valid), count
- * [B*H][N_Q] int32 and mask [B*H][N_Q][ceil(N_K/32)] u32.  Returns 0 if the
- * configuration is invalid (see pasa_last_error()). */
+ * [B*H][N_Q] int32 and mask [B*H][N_Q][ceil(N_K/32)] u32; with the Eq. 8 prior
+ * enabled also every block's fp64 H_j (8 D^2 bytes per block and head: 6.2 GB
+ * for a Wan-14B layer of 40 heads).  Returns 0 if the configuration is invalid
+ * (see pasa_last_error()). */
 size_t pasa_route_workspace_bytes(const pasa_route_cfg* cfg, int64_t B, int64_t S, int64_t H,
                                   int64_t D);
 /* Bind a handle to caller-owned device workspace `dev_ws` of `bytes` bytes.

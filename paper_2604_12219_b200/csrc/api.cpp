@@ -40,7 +40,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
     size_t off_hdr, off_qbar, off_kbar, off_scores, off_sigma, off_kbar_lp, off_vsum, off_ht, off_idx,
-        off_count, off_mask, off_het, off_prior, off_hgs, off_hglob, off_part, total;
+        off_count, off_mask, off_het, off_prior, off_hj, off_hgs, off_hglob, off_part, total;
 };
 
 pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int64_t D) {
@@ -88,9 +88,10 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     const bool pr = c->prior != PASA_PRIOR_NONE;   // Eq. 8 prior buffers (fp64)
     L.off_het = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
     L.off_prior = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK : 0));
-    const int64_t hcb = pasa::het_chunk_blocks(c->G, L.NK);
-    const int64_t hslots = std::max((L.NK + hcb - 1) / hcb, L.NG);
-    L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * hslots * D * D : 0));
+    // every block's H_j in fp64 (8 D^2 bytes per block: 6.2 GB for a Wan-14B layer),
+    // computed once and read by the means and norm passes
+    L.off_hj = o;       o = align_up(o + (pr ? sizeof(double) * L.BH * L.NK * D * D : 0));
+    L.off_hgs = o;      o = align_up(o + (pr ? sizeof(double) * L.BH * L.NG * D * D : 0));
     L.off_hglob = o;    o = align_up(o + (pr ? sizeof(double) * L.BH * D * D : 0));
     // large groups on the tensor-core statistics kernel: fp32 sums of 32-block chunks
     const bool big = c->G > 32;
@@ -245,6 +246,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     const bool pr = cfg->prior != PASA_PRIOR_NONE;
     r->het = pr ? reinterpret_cast<double*>(w + L.off_het) : nullptr;
     r->prior = pr ? reinterpret_cast<double*>(w + L.off_prior) : nullptr;
+    r->hj = pr ? reinterpret_cast<double*>(w + L.off_hj) : nullptr;
     r->hgs = pr ? reinterpret_cast<double*>(w + L.off_hgs) : nullptr;
     r->hglob = pr ? reinterpret_cast<double*>(w + L.off_hglob) : nullptr;
     r->het_valid = 0;

@@ -10,16 +10,15 @@
 // fp64 oracle far inside the routing tie tolerance (1e-6 relative);
 // fp32 tensor-core accumulation of 64-term sums would sit at that tolerance.
 //
-// Work unit: a chunk of CB consecutive KV blocks (CB divides G, or one group
-// spans everything), one CTA per (chunk, head).  Three launches:
-//   1. het_kernel<SUM>:  chunk sums sum_{j in chunk} H_j (one fp64 accumulator:
-//      sum_{n in chunk} (K_n - Kbar_{j(n)})^T V_n);
-//   2. het_means_kernel: C = (sum over chunks in order) / N_K, and in group mode
-//      the group means (in place, slot g);
-//   3. het_kernel<NORM>: H_j again per block and ||H_j - C||_F^2 reduced in a
-//      fixed order (deterministic).
-// Inside a CTA the K/V rows stream through shared memory in 32-token units:
-// cp.async copies the raw rows of unit u+1 while unit u is converted to fp64
+// Three launches, each H_j computed once (B200: 180 GB of HBM, so every block's
+// H_j is kept, 8 D^2 bytes per block, rather than recomputed for the norm):
+//   1. het_hj_kernel:    H_j of every block into hj[bh][j] (one CTA per chunk of CB
+//      consecutive blocks);
+//   2. het_means_kernel: C = (1/N_K) sum_j H_j in ascending j (the oracle's order),
+//      and in group mode the group means (slot g of hgs);
+//   3. het_norm_kernel:  ||H_j - C||_F^2 per block, fixed-order reduction.
+// Inside a het_hj_kernel CTA the K/V rows stream through shared memory in 32-token
+// units: cp.async copies the raw rows of unit u+1 while unit u is converted to fp64
 // (centred keys) and consumed.  D^2/64 threads, each owning a 4-row x 16-column
 // patch of H in fp64 registers; column reads are warp broadcasts.
 #include <cuda_bf16.h>
@@ -33,14 +32,9 @@ namespace {
 
 constexpr int kUnit = 32;       // tokens per pipeline unit (half a KV block)
 
-// the NORM pass stages its C in shared memory when it fits next to the token units
 template <typename T, int D>
 constexpr size_t het_smem_units() {
     return (size_t)2 * kUnit * D * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
-}
-template <typename T, int D>
-constexpr bool het_stage_c() {
-    return het_smem_units<T, D>() + (size_t)D * D * sizeof(double) <= (size_t)227 * 1024;
 }
 
 struct HetArgs {
@@ -49,7 +43,8 @@ struct HetArgs {
     int64_t ksB, ksS, ksH, vsB, vsS, vsH;   // element strides
     int64_t S, H, NK, NG, G, CB, NC;
     const double* kbar;    // [BH][NK][D] fp64 block means (pool_kernel)
-    double* part;          // [BH][max(NC,NG)][D][D] chunk sums, then (group mode) group means
+    double* hj;            // [BH][NK][D][D] H_j of every block
+    double* part;          // [BH][>= NG][D][D] group means (group mode)
     double* cglob;         // [BH][D][D] global mean
     int32_t mode;          // PASA_PRIOR_GLOBAL / PASA_PRIOR_GROUP
     double eps;
@@ -69,8 +64,8 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ double to_d(float x) { return (double)x; }
 __device__ __forceinline__ double to_d(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
 
-template <typename T, int D, bool NORM>
-__global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
+template <typename T, int D>
+__global__ void __launch_bounds__(D * D / 64, 1) het_hj_kernel(HetArgs a) {
     constexpr int NT = D * D / 64;
     constexpr int RT = D / 4;                        // row groups of 4
     constexpr int ROWB = D * (int)sizeof(T);         // bytes per raw row
@@ -79,8 +74,6 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
     double* kt = reinterpret_cast<double*>(smem);                      // [kUnit][D]
     double* vt = kt + kUnit * D;                                        // [kUnit][D]
     uint8_t* raw = reinterpret_cast<uint8_t*>(vt + kUnit * D);         // [2][K|V][RAWB]
-    double* cs = reinterpret_cast<double*>(raw + 4 * RAWB);            // NORM: C [D][D]
-    __shared__ double red[NT / 32];
     const int tid = threadIdx.x;
     const int r0 = 4 * (tid % RT), c0 = 16 * (tid / RT);
     const int64_t bh = blockIdx.y, chunk = blockIdx.x;
@@ -89,7 +82,6 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
     const T* V = reinterpret_cast<const T*>(a.v) + b * a.vsB + h * a.vsH;
     const int64_t j_lo = chunk * a.CB, j_hi = min(j_lo + a.CB, a.NK);
     const int n_units = (int)(2 * (j_hi - j_lo));
-    const int64_t slots = max(a.NC, a.NG);
 
     auto issue = [&](int u) {                        // raw rows of unit u -> buffer u & 1
         const int64_t t0 = j_lo * 64 + (int64_t)u * kUnit;
@@ -112,15 +104,6 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
 #pragma unroll
         for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
     if (n_units > 0) issue(0);
-    if constexpr (NORM && het_stage_c<T, D>()) {
-        // the chunk's C (one group, or the global mean) staged once: every block of the
-        // chunk reads it from shared memory instead of L2
-        const double* Cg = a.mode == PASA_PRIOR_GROUP
-                               ? a.part + (bh * slots + j_lo / a.G) * (int64_t)D * D
-                               : a.cglob + bh * (int64_t)D * D;
-        for (int e = tid; e < D * D / 2; e += NT)
-            reinterpret_cast<double2*>(cs)[e] = reinterpret_cast<const double2*>(Cg)[e];
-    }
     for (int u = 0; u < n_units; ++u) {
         const int64_t j = j_lo + u / 2;
         const int64_t t0 = j * 64 + (u & 1) * kUnit;
@@ -160,82 +143,80 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_kernel(HetArgs a) {
 #pragma unroll
                 for (int c = 0; c < 16; ++c) acc[i][c] = fma(kr[i], vr[c], acc[i][c]);
         }
-        if constexpr (NORM) {
-            if (u & 1) {                              // block j complete: ||H_j - C||_F
-                // C staged at CTA start (the chunk lies in one group), else read from L2
-                const double* C = het_stage_c<T, D>()
-                                      ? cs
-                                      : (a.mode == PASA_PRIOR_GROUP
-                                             ? a.part + (bh * slots + j / a.G) * (int64_t)D * D
-                                             : a.cglob + bh * (int64_t)D * D);
-                double p = 0.0;
+        if (u & 1) {                                  // block j complete: store H_j
+            double* out = a.hj + (bh * a.NK + j) * (int64_t)D * D;
 #pragma unroll
-                for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < 4; ++i)
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) {
-                        const double d = acc[i][c] - C[(r0 + i) * D + c0 + c];
-                        p = fma(d, d, p);
-                        acc[i][c] = 0.0;
-                    }
-                // fixed-order reduction: xor tree inside each warp, then warps in order
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
-                if ((tid & 31) == 0) red[tid >> 5] = p;
-                __syncthreads();
-                if (tid == 0) {
-                    double tot = 0.0;
-                    for (int w = 0; w < NT / 32; ++w) tot += red[w];
-                    const double hv = sqrt(tot);
-                    a.het[bh * a.NK + j] = hv;
-                    a.prior[bh * a.NK + j] = log(hv + a.eps);
+                for (int c = 0; c < 16; c += 2) {
+                    *reinterpret_cast<double2*>(&out[(r0 + i) * D + c0 + c]) =
+                        make_double2(acc[i][c], acc[i][c + 1]);
+                    acc[i][c] = 0.0;
+                    acc[i][c + 1] = 0.0;
                 }
-            }
         }
-    }
-    if constexpr (!NORM) {
-        double* out = a.part + (bh * slots + chunk) * (int64_t)D * D;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int c = 0; c < 16; ++c) out[(r0 + i) * D + c0 + c] = acc[i][c];
     }
 }
 
-// C: global mean (1/N_K) sum_c chunk_c (groups in ascending order, chunks in
-// order inside each group); in group mode the group means (unweighted, App. B)
-// replace slot g (chunk index >= g, and every chunk of groups <= g is read first).
+// C: global mean (1/N_K) sum_j H_j, blocks in ascending order (Eq. 6, as the oracle);
+// in group mode the group means (unweighted, App. B) into slot g of part.
 template <int D>
 __global__ void __launch_bounds__(256) het_means_kernel(HetArgs a) {
     const int64_t bh = blockIdx.y;
     const int64_t e = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (e >= (int64_t)D * D) return;
-    double* p = a.part + bh * max(a.NC, a.NG) * (int64_t)D * D + e;
+    const double* hj = a.hj + bh * a.NK * (int64_t)D * D + e;
     double total = 0.0;
     for (int64_t g = 0; g < a.NG; ++g) {
         const int64_t jb = g * a.G, je = min(jb + a.G, a.NK);
         double s = 0.0;
-        for (int64_t c = jb / a.CB; c < (je + a.CB - 1) / a.CB; ++c) s += p[c * (int64_t)D * D];
-        total += s;
-        if (a.mode == PASA_PRIOR_GROUP) p[g * (int64_t)D * D] = s / (double)(je - jb);
+        for (int64_t j = jb; j < je; ++j) {
+            const double x = hj[j * (int64_t)D * D];
+            s += x;
+            total += x;
+        }
+        if (a.mode == PASA_PRIOR_GROUP)
+            a.part[(bh * a.NG + g) * (int64_t)D * D + e] = s / (double)(je - jb);
     }
     a.cglob[bh * (int64_t)D * D + e] = total / (double)a.NK;
 }
 
+// het_j = ||H_j - C||_F, log(het_j + eps): one CTA per (block, head), fixed-order
+// reduction (thread partials in ascending element order, warps in order).
+template <int D>
+__global__ void __launch_bounds__(256) het_norm_kernel(HetArgs a) {
+    const int64_t j = blockIdx.x, bh = blockIdx.y;
+    const double* Hj = a.hj + (bh * a.NK + j) * (int64_t)D * D;
+    const double* C = a.mode == PASA_PRIOR_GROUP ? a.part + (bh * a.NG + j / a.G) * (int64_t)D * D
+                                                 : a.cglob + bh * (int64_t)D * D;
+    __shared__ double red[8];
+    double p = 0.0;
+    for (int e = threadIdx.x; e < D * D; e += 256) {
+        const double d = Hj[e] - C[e];
+        p = fma(d, d, p);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) p += __shfl_xor_sync(0xffffffffu, p, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = p;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot = 0.0;
+        for (int w = 0; w < 8; ++w) tot += red[w];
+        const double hv = sqrt(tot);
+        a.het[bh * a.NK + j] = hv;
+        a.prior[bh * a.NK + j] = log(hv + a.eps);
+    }
+}
+
 template <typename T, int D>
 cudaError_t launch_d(const HetArgs& a, int64_t BH, cudaStream_t st) {
-    const size_t smem_sum = het_smem_units<T, D>();
-    const size_t smem_norm = smem_sum + (het_stage_c<T, D>() ? (size_t)D * D * sizeof(double) : 0);
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(het_kernel<T, D, false>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_sum)) != cudaSuccess)
-        return e;
-    if ((e = cudaFuncSetAttribute(het_kernel<T, D, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_norm)) != cudaSuccess)
-        return e;
-    const dim3 grid((unsigned)a.NC, (unsigned)BH);
-    het_kernel<T, D, false><<<grid, D * D / 64, smem_sum, st>>>(a);
+    const size_t smem = het_smem_units<T, D>();
+    cudaError_t e = cudaFuncSetAttribute(het_hj_kernel<T, D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    het_hj_kernel<T, D><<<dim3((unsigned)a.NC, (unsigned)BH), D * D / 64, smem, st>>>(a);
     het_means_kernel<D><<<dim3((unsigned)((D * D + 255) / 256), (unsigned)BH), 256, 0, st>>>(a);
-    het_kernel<T, D, true><<<grid, D * D / 64, smem_norm, st>>>(a);
+    het_norm_kernel<D><<<dim3((unsigned)a.NK, (unsigned)BH), 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
@@ -258,7 +239,7 @@ cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s*
     a.S = r->S; a.H = r->H; a.NK = r->NK; a.NG = r->NG; a.G = r->cfg.G;
     a.CB = het_chunk_blocks(a.G, a.NK);
     a.NC = (a.NK + a.CB - 1) / a.CB;
-    a.kbar = r->kbar; a.part = r->hgs; a.cglob = r->hglob;
+    a.kbar = r->kbar; a.hj = r->hj; a.part = r->hgs; a.cglob = r->hglob;
     a.mode = r->cfg.prior; a.eps = r->cfg.eps;
     a.het = r->het; a.prior = r->prior;
     const bool f32 = k.dtype == PASA_F32;

@@ -40,7 +40,8 @@ struct pasa_route_s {
     uint32_t* mask;                  // [BH][NQ][W]
     double* het;                     // [BH][NK] ||H_j - C||_F (prior-enabled handles only)
     double* prior;                   // [BH][NK] log(het + eps)
-    double* hgs;                     // [BH][NG][D][D] fp64 group sums / means of H_j
+    double* hj;                      // [BH][NK][D][D] fp64 H_j of every block (prior handles)
+    double* hgs;                     // [BH][NG][D][D] fp64 group means of H_j
     double* hglob;                   // [BH][D][D] fp64 global mean Hbar
     int32_t het_valid;               // a pasa_route_v has filled het
     int32_t route_dtype;             // dtype of the q/k the route was last built from (-1 = none)
