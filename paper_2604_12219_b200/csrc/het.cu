@@ -19,8 +19,7 @@
 //   3. het_norm_kernel:  ||H_j - C||_F^2 per block, fixed-order reduction.
 // Inside a het_hj_kernel CTA the K/V rows stream through shared memory in 32-token
 // units: cp.async copies the raw rows of unit u+1 while unit u is converted to fp64
-// (centred keys) and consumed.  D^2/64 threads, each owning a 4-row x 16-column
-// patch of H in fp64 registers; column reads are warp broadcasts.
+// (centred keys) and consumed by fp64 tensor-core MMAs (DMMA m8n8k4).
 #include <cuda_bf16.h>
 
 #include <cmath>
@@ -33,8 +32,8 @@ namespace {
 constexpr int kUnit = 32;       // tokens per pipeline unit (half a KV block)
 
 template <typename T, int D>
-constexpr size_t het_smem_units() {
-    return (size_t)2 * kUnit * D * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
+constexpr size_t het_smem_units() {   // fp64 units with padded rows + the raw double buffer
+    return (size_t)2 * kUnit * (D + 8) * sizeof(double) + (size_t)4 * kUnit * D * sizeof(T);
 }
 
 struct HetArgs {
@@ -64,18 +63,35 @@ __device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_g
 __device__ __forceinline__ double to_d(float x) { return (double)x; }
 __device__ __forceinline__ double to_d(__nv_bfloat16 x) { return (double)__bfloat162float(x); }
 
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// H_j = Kc^T V per block on the fp64 tensor core (DMMA m8n8k4, operands from registers:
+// ~14 fma per loaded double instead of ~3 with the register-tiled DFMA loop).  GEMM
+// view: M = N = D (rows r of Kc^T, columns c of V), K = the block's tokens.  Warp w owns
+// row tiles [w RTW, (w+1) RTW) x every column tile (32 8x8 tiles, 64 fp64 accumulators
+// per thread).  Fragments (PTX m8n8k4.f64): A[r][n] lane (r = lane/4, n = lane%4),
+// B[n][c] lane (n = lane%4, c = lane/4), C[r][c] lane (r = lane/4, c = 2(lane%4)+{0,1}).
+// The DMMA's internal rounding differs from a sequential fma chain by ~1e-16 relative:
+// the prior's tolerance against the oracle is 1e-10 (R-26).
 template <typename T, int D>
 __global__ void __launch_bounds__(D * D / 64, 1) het_hj_kernel(HetArgs a) {
-    constexpr int NT = D * D / 64;
-    constexpr int RT = D / 4;                        // row groups of 4
+    constexpr int NT = D * D / 64;                   // threads: 256 at d = 128, 64 at d = 64
+    constexpr int NW = NT / 32;
+    constexpr int CT = D / 8;                        // column tiles
+    constexpr int RTW = (D / 8) / NW;                // row tiles per warp (CT * RTW = 32)
+    constexpr int DP = D + 8;                        // padded fp64 row: conflict-free fragments
     constexpr int ROWB = D * (int)sizeof(T);         // bytes per raw row
     constexpr int RAWB = kUnit * ROWB;               // bytes per raw unit per tensor
     extern __shared__ __align__(16) uint8_t smem[];
-    double* kt = reinterpret_cast<double*>(smem);                      // [kUnit][D]
-    double* vt = kt + kUnit * D;                                        // [kUnit][D]
-    uint8_t* raw = reinterpret_cast<uint8_t*>(vt + kUnit * D);         // [2][K|V][RAWB]
-    const int tid = threadIdx.x;
-    const int r0 = 4 * (tid % RT), c0 = 16 * (tid / RT);
+    double* kt = reinterpret_cast<double*>(smem);                      // [kUnit][DP]
+    double* vt = kt + kUnit * DP;                                       // [kUnit][DP]
+    uint8_t* raw = reinterpret_cast<uint8_t*>(vt + kUnit * DP);        // [2][K|V][RAWB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fk = lane & 3;         // fragment row / k index
     const int64_t bh = blockIdx.y, chunk = blockIdx.x;
     const int64_t b = bh / a.H, h = bh % a.H;
     const T* K = reinterpret_cast<const T*>(a.k) + b * a.ksB + h * a.ksH;
@@ -98,11 +114,11 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_hj_kernel(HetArgs a) {
         cp_async_commit();
     };
 
-    double acc[4][16];
+    double acc[RTW][CT][2];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < RTW; ++i)
 #pragma unroll
-        for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
+        for (int c = 0; c < CT; ++c) acc[i][c][0] = acc[i][c][1] = 0.0;
     if (n_units > 0) issue(0);
     for (int u = 0; u < n_units; ++u) {
         const int64_t j = j_lo + u / 2;
@@ -120,39 +136,36 @@ __global__ void __launch_bounds__(D * D / 64, 1) het_hj_kernel(HetArgs a) {
                     kv = to_d(reinterpret_cast<const T*>(src)[n * D + col]) - kb[col];
                     vv = to_d(reinterpret_cast<const T*>(src + RAWB)[n * D + col]);
                 }
-                kt[n * D + col] = kv;
-                vt[n * D + col] = vv;
+                kt[n * DP + col] = kv;
+                vt[n * DP + col] = vv;
             }
         }
         __syncthreads();                              // fp64 unit ready; raw(u) consumed
         if (u + 1 < n_units) issue(u + 1);
-#pragma unroll 4
-        for (int n = 0; n < valid; ++n) {
-            const double2 k01 = *reinterpret_cast<const double2*>(&kt[n * D + r0]);
-            const double2 k23 = *reinterpret_cast<const double2*>(&kt[n * D + r0 + 2]);
-            const double kr[4] = {k01.x, k01.y, k23.x, k23.y};
-            double vr[16];
+        const int nsteps = (valid + 3) >> 2;          // zero rows past `valid` add nothing
+        for (int s4 = 0; s4 < nsteps; ++s4) {
+            const double* krow = kt + (4 * s4 + fk) * DP;
+            const double* vrow = vt + (4 * s4 + fk) * DP;
+            double av[RTW], bv[CT];
 #pragma unroll
-            for (int c = 0; c < 16; c += 2) {
-                const double2 t = *reinterpret_cast<const double2*>(&vt[n * D + c0 + c]);
-                vr[c] = t.x;
-                vr[c + 1] = t.y;
-            }
+            for (int i = 0; i < RTW; ++i) av[i] = krow[(warp * RTW + i) * 8 + fr];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int c = 0; c < CT; ++c) bv[c] = vrow[c * 8 + fr];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) acc[i][c] = fma(kr[i], vr[c], acc[i][c]);
+            for (int i = 0; i < RTW; ++i)
+#pragma unroll
+                for (int c = 0; c < CT; ++c) dmma_8x8x4(acc[i][c][0], acc[i][c][1], av[i], bv[c]);
         }
         if (u & 1) {                                  // block j complete: store H_j
             double* out = a.hj + (bh * a.NK + j) * (int64_t)D * D;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < RTW; ++i)
 #pragma unroll
-                for (int c = 0; c < 16; c += 2) {
-                    *reinterpret_cast<double2*>(&out[(r0 + i) * D + c0 + c]) =
-                        make_double2(acc[i][c], acc[i][c + 1]);
-                    acc[i][c] = 0.0;
-                    acc[i][c + 1] = 0.0;
+                for (int c = 0; c < CT; ++c) {
+                    const int r = (warp * RTW + i) * 8 + fr, col = c * 8 + 2 * fk;
+                    *reinterpret_cast<double2*>(&out[r * D + col]) =
+                        make_double2(acc[i][c][0], acc[i][c][1]);
+                    acc[i][c][0] = acc[i][c][1] = 0.0;
                 }
         }
     }
