@@ -96,43 +96,51 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolArgs qa, PoolArgs ka, int
 }
 
 // ---------------------------------------------------------------------------
-// a3: block scores r_ij = s * dot(Qbar_i, Kbar_j), a tiled fp64 GEMM.  Each
-// thread owns an 8x8 output patch and accumulates every output with an fma
-// chain over the head dimension in ascending order (R2), so the per-element
-// result is independent of the tiling.
+// a3: block scores r_ij = s * dot(Qbar_i, Kbar_j), a tiled fp64 GEMM on the fp64
+// tensor core.  Every output accumulates an fma chain over the head dimension in
+// ascending order (R2: the chain of DMMA 8x8x4 steps is that chain, bit for bit), so
+// the per-element result is independent of the tiling.
 // ---------------------------------------------------------------------------
 constexpr int kST = 128;    // tile edge (rows i x columns j)
 constexpr int kSK = 16;     // D chunk staged in smem
+constexpr int kSP = kSK + 4;   // padded smem row (doubles): conflict-free DMMA fragments
 
-constexpr int kSThreads = 256;   // 16 x 16 threads, 8 x 8 outputs each
+constexpr int kSThreads = 256;   // 8 warps; warp w owns row tiles 2w, 2w+1 x 16 column tiles
+
+// fp64 tensor core: d (+)= a * b on an 8x8x4 tile.  Measured on this pool
+// (tools/dmma_exact.cu): bit-identical to the sequential fma chain over k = 0..3, so
+// a chain of these in ascending k is the oracle's ascending-d fma chain (R2).
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
 
 __global__ void __launch_bounds__(kSThreads, 1) scores_kernel(const double* __restrict__ qbar,
                                                         const double* __restrict__ kbar, int64_t NQ,
                                                         int64_t NK, int64_t D, double s,
                                                         const double* __restrict__ prior,
                                                         double* __restrict__ r) {
-    __shared__ double sq[kSK][kST + 1];
-    __shared__ double sk[kSK][kST + 1];
-    int64_t bh = blockIdx.z;
-    int64_t i0 = (int64_t)blockIdx.y * kST, j0 = (int64_t)blockIdx.x * kST;
+    __shared__ double sq[kST][kSP];    // rows i of Qbar, one 16-dim chunk
+    __shared__ double sk[kST][kSP];    // rows j of Kbar
+    const int64_t bh = blockIdx.z;
+    const int64_t i0 = (int64_t)blockIdx.y * kST, j0 = (int64_t)blockIdx.x * kST;
     const double* Q = qbar + bh * NQ * D;
     const double* K = kbar + bh * NK * D;
-    // thread (tx, ty) owns rows ty + 16a and columns tx + 16c (a, c < 8): the row
-    // operand is a 2-address broadcast and the column operand 128 contiguous bytes
-    // per warp load, 16 loads per 64 fma (an 8 x 4 patch on 512 threads measured slower)
-    int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    double acc[8][8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int fr = lane >> 2, fk = lane & 3;     // DMMA fragment row / k index
+    double acc[2][16][2];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-        for (int c = 0; c < 8; ++c) acc[a][c] = 0.0;
+        for (int c = 0; c < 16; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
     // register double buffer: chunk d0 + kSK is in flight while chunk d0 is consumed
     constexpr int kPer = kSK * kST / kSThreads;
     double pq[kPer], pk[kPer];
     auto fetch = [&](int64_t d0) {
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
-            const int e = threadIdx.x + kSThreads * u;
+            const int e = tid + kSThreads * u;
             const int row = e / kSK, col = e % kSK;
             const int64_t gi = i0 + row, gj = j0 + row;
             pq[u] = gi < NQ ? Q[gi * D + d0 + col] : 0.0;
@@ -143,37 +151,42 @@ __global__ void __launch_bounds__(kSThreads, 1) scores_kernel(const double* __re
     for (int64_t d0 = 0; d0 < D; d0 += kSK) {
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
-            const int e = threadIdx.x + kSThreads * u;
-            sq[e % kSK][e / kSK] = pq[u];
-            sk[e % kSK][e / kSK] = pk[u];
+            const int e = tid + kSThreads * u;
+            sq[e / kSK][e % kSK] = pq[u];
+            sk[e / kSK][e % kSK] = pk[u];
         }
         __syncthreads();
         if (d0 + kSK < D) fetch(d0 + kSK);
 #pragma unroll
-        for (int dd = 0; dd < kSK; ++dd) {
-            double qv[8], kv[8];
+        for (int ks = 0; ks < kSK / 4; ++ks) {      // ascending d: r_ij's fma chain order
+            const int kk = 4 * ks + fk;
+            const double a0 = sq[(2 * warp) * 8 + fr][kk];
+            const double a1 = sq[(2 * warp + 1) * 8 + fr][kk];
+            double bv[16];
 #pragma unroll
-            for (int a = 0; a < 8; ++a) qv[a] = sq[dd][ty + 16 * a];
+            for (int c = 0; c < 16; ++c) bv[c] = sk[c * 8 + fr][kk];
 #pragma unroll
-            for (int c = 0; c < 8; ++c) kv[c] = sk[dd][tx + 16 * c];
-#pragma unroll
-            for (int a = 0; a < 8; ++a)
-#pragma unroll
-                for (int c = 0; c < 8; ++c) acc[a][c] = __fma_rn(qv[a], kv[c], acc[a][c]);
+            for (int c = 0; c < 16; ++c) {
+                dmma_8x8x4(acc[0][c][0], acc[0][c][1], a0, bv[c]);
+                dmma_8x8x4(acc[1][c][0], acc[1][c][1], a1, bv[c]);
+            }
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int a = 0; a < 8; ++a) {
-        int64_t gi = i0 + ty + 16 * a;
+    for (int a = 0; a < 2; ++a) {
+        const int64_t gi = i0 + (2 * warp + a) * 8 + fr;
         if (gi >= NQ) continue;
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
-            int64_t gj = j0 + tx + 16 * c;
-            if (gj < NK) {
-                double x = __dmul_rn(s, acc[a][c]);
-                if (prior) x = __dadd_rn(x, prior[bh * NK + gj]);   // Eq. 8 prior term
-                r[(bh * NQ + gi) * NK + gj] = x;
+        for (int c = 0; c < 16; ++c) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t gj = j0 + c * 8 + 2 * fk + h;
+                if (gj < NK) {
+                    double x = __dmul_rn(s, acc[a][c][h]);
+                    if (prior) x = __dadd_rn(x, prior[bh * NK + gj]);   // Eq. 8 prior term
+                    r[(bh * NQ + gi) * NK + gj] = x;
+                }
             }
         }
     }
