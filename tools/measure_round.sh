@@ -18,6 +18,8 @@ timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/b
 timeout 300 python tools/power_probe.py > gpurun_out/power_wan14b.txt 2>&1
 CFG=cogvideox5b SECS=3 timeout 200 python tools/power_probe.py > gpurun_out/power_cogvideox5b.txt 2>&1
 timeout 300 python tools/q256_time.py > gpurun_out/q256_wan14b.txt 2>&1
+timeout 400 python tools/energy_ablate.py > gpurun_out/energy_ablate.txt 2>&1
+timeout 400 python tools/scaling_emulate.py > gpurun_out/scaling_emulate.txt 2>&1
 # launch list (serialised, cold cache: only the shares are comparable with bench.py)
 timeout 400 ncu --metrics gpu__time_duration.sum --clock-control none \
   -k regex:'budget|pool|scores|select|stats|attn|rowstats' -c 16 --csv \
