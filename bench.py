@@ -35,7 +35,7 @@ METRIC = "PASA attn TFLOP/s-equiv & ms/layer at Wan2.1-14B 720p, 1/2/4/8 B200, %
 UNIT = "TFLOP/s-equiv"
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -65,7 +65,29 @@ def parse():
                          "the north-star path)")
     ap.add_argument("--cpu-qblocks", type=int, default=256,
                     help="oracle sample size (q-blocks of one head; ~10 s of CPU work)")
-    return ap.parse_args()
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1.  gloo is a debug mode: ranks may "
+                         "share one GPU (device = local_rank %% device_count) and every "
+                         "collective goes through host memory, so its timings say nothing; "
+                         "it exercises the multi-rank bookkeeping on a one-GPU box")
+    return ap.parse_args(argv)
+
+
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def torchrun_cmd(argv, n: int, port: int):
+    """`python bench.py --gpus N ...` outside torchrun re-launches itself as one process
+    per GPU (the driver's own form: torch.distributed.run, 127.0.0.1 rendezvous)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+            f"--nproc-per-node={n}", "--master-addr", "127.0.0.1", f"--master-port={port}",
+            os.path.abspath(__file__), *argv]
 
 
 def peaks():
@@ -224,7 +246,7 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": args.config, "S": S, "H": H, "D": D},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": desc},
+                         "sample": desc, "extrapolated": True},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -243,9 +265,14 @@ def run_pasa(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    gloo = args.dist_backend == "gloo"
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # gloo debug mode: ranks may share the box's one GPU
+        torch.cuda.set_device(local % torch.cuda.device_count() if gloo else local)
+        if gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     if rank == 0:
@@ -266,6 +293,28 @@ def run_pasa(args):
     except ValueError as exc:
         raise SystemExit(str(exc))
     dev = torch.device("cuda", torch.cuda.current_device())
+    cdev = torch.device("cpu") if gloo else dev      # where collective buffers live
+
+    def all_max(vals):
+        """MAX over ranks of a list of floats (device timings: max over ranks)."""
+        if world == 1:
+            return list(vals)
+        tt = torch.tensor(list(vals), device=cdev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return tt.cpu().tolist()
+
+    def all_sum(vals):
+        if world == 1:
+            return list(vals)
+        tt = torch.tensor(list(vals), device=cdev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.SUM)
+        return tt.cpu().tolist()
+
+    heads_all = [Hl]
+    if world > 1:
+        heads_all = [None] * world
+        dist.all_gather_object(heads_all, Hl)
+        assert sum(heads_all) == H, heads_all
     if seq_sharded and S % world:
         raise SystemExit(f"S = {S} does not split over {world} ranks")
     # every global head drawn from its own seed: the same data for any N
@@ -283,8 +332,14 @@ def run_pasa(args):
         # sequence-sharded input [B, S/P, H, D]: the step starts with the Ulysses
         # all-to-all to this rank's heads and ends with the inverse
         q_s, k_s, v_s = q, k, v
-        to_heads = (lambda t: pdist.seq_to_head(t)) if world > 1 else (lambda t: t)
-        to_seq = (lambda t: pdist.head_to_seq(t)) if world > 1 else (lambda t: t)
+        if world == 1:
+            to_heads = to_seq = (lambda t: t)
+        elif gloo:   # debug mode: the all-to-all through host memory
+            to_heads = lambda t: pdist.seq_to_head(t.cpu()).to(dev)  # noqa: E731
+            to_seq = lambda t: pdist.head_to_seq(t.cpu()).to(dev)    # noqa: E731
+        else:
+            to_heads = lambda t: pdist.seq_to_head(t)  # noqa: E731
+            to_seq = lambda t: pdist.head_to_seq(t)    # noqa: E731
         q, k, v = (to_heads(t) for t in (q_s, k_s, v_s))
     out = torch.empty_like(q)
     tp = synth.ThreePhase(shape=cfg["latent"], T=50, seed=7, device=dev)
@@ -363,16 +418,13 @@ def run_pasa(args):
         per_step.append(prev.elapsed_time(evs[it][3]))
     ph /= K
     step_p50, step_p90 = (float(np.percentile(per_step, q)) for q in (50, 90))
-    t_max = t_local
-    if world > 1:
-        tt = torch.tensor([t_local] + ph.tolist(), device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt[0])
-        ph = tt[1:].cpu().numpy()
+    mx = all_max([t_local] + ph.tolist())
+    t_max = float(mx[0])
+    ph = np.array(mx[1:])
 
     # ---------------- the same step captured once in a CUDA graph, replayed K times -----
     graph = None
-    if not args.no_graph and not (seq_sharded and world > 1):   # no NCCL inside a capture
+    if not args.no_graph and not (seq_sharded and world > 1):   # no collective inside a capture
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -388,11 +440,7 @@ def run_pasa(args):
                 g.replay()
             gb.record()
             torch.cuda.synchronize()
-            tg = ga.elapsed_time(gb) / K
-            if world > 1:
-                tt = torch.tensor([tg], device=dev, dtype=torch.float64)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                tg = float(tt[0])
+            tg = all_max([ga.elapsed_time(gb) / K])[0]
             graph = {"ms_per_step": tg, "value": 4.0 * S * S * D * B * H / (tg * 1e-3) / 1e12,
                      "unit": UNIT, "note": "budget+route+stats+attn captured once, replayed"}
         except Exception as exc:  # report, do not hide, a capture failure
@@ -440,11 +488,7 @@ def run_pasa(args):
             P.attn(q, k, v, route, out)
             eb.record(stream)
             torch.cuda.synchronize()
-            ms_t = ea.elapsed_time(eb)
-            if world > 1:
-                tt = torch.tensor([ms_t], device=dev, dtype=torch.float64)
-                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-                ms_t = float(tt[0])
+            ms_t = all_max([ea.elapsed_time(eb)])[0]
             ks.append(route.read()["k"])
             mss.append(ms_t)
         schedule = {"T": T, "budget": "online (three-phase synthetic trajectory, R-16)",
@@ -510,15 +554,8 @@ def run_pasa(args):
             e2e_step()
         bq.record(stream)
         torch.cuda.synchronize()
-        te = a.elapsed_time(bq) / n_e2e
-        h2d_all, d2h_all = h2d, d2h
-        if world > 1:
-            tt = torch.tensor([te], device=dev, dtype=torch.float64)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            te = float(tt[0])
-            nb = torch.tensor([h2d, d2h], device=dev, dtype=torch.float64)   # uneven heads
-            dist.all_reduce(nb, op=dist.ReduceOp.SUM)
-            h2d_all, d2h_all = float(nb[0]), float(nb[1])
+        te = all_max([a.elapsed_time(bq) / n_e2e])[0]
+        h2d_all, d2h_all = all_sum([h2d, d2h])          # uneven heads: sum over ranks
         # the e2e roofline: this rank's pinned-host -> device copy bandwidth, measured with
         # one contiguous 512 MB copy (best of 3), and the step's H2D bytes at that rate
         hb = torch.empty(1 << 28, dtype=torch.bfloat16, pin_memory=True)
@@ -577,7 +614,7 @@ def run_pasa(args):
         cv, secs, desc, _ = oracle_sample(cfg, args.cpu_qblocks)
         import oracle
         cpu = {"value": cv, "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
-               "sample": desc}
+               "sample": desc, "extrapolated": True}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": t_max, "ms_per_step_p50": step_p50,
@@ -585,6 +622,10 @@ def run_pasa(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {
             "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
+            "nranks": world, "heads_per_rank_all": heads_all,
+            "dist_backend": (args.dist_backend + (" (debug: ranks share GPUs, timings not "
+                                                  "meaningful)" if gloo else "")) if world > 1
+            else None,
             "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
             "step_t": t_step, "budget": args.budget, "prior": args.prior, "l1": rec["l1"], "alpha": rec["alpha"],
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
@@ -617,8 +658,15 @@ def run_pasa(args):
     return 0
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (rank 0 prints the JSON line)
+        return subprocess.call(torchrun_cmd(argv, args.gpus, free_port()))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE = {world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_pasa(args)

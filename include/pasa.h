@@ -76,7 +76,8 @@ typedef struct {
     double l1_mean;          /* l-bar of Eq. 9 from calibration; must be > 0                   */
     double h_t, h_tm1;       /* sigma_t - sigma_{t-1}, sigma_{t-1} - sigma_{t-2}; != 0 (R-16)   */
     double rho_max;          /* clip for rho_t (1.0, R-18)                                     */
-    const double* rho_table; /* HOST, optional length-T per-step rho_t (offline Eqs. 9-11), or NULL */
+    const double* rho_table; /* HOST, optional per-step rho_t (offline Eqs. 9-11), or NULL; when
+                                set it MUST hold at least T entries (only [step] is read)  */
     int32_t kind;            /* pasa_budget_input                                              */
     int32_t _pad;
 } pasa_schedule;
@@ -205,14 +206,6 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
 #define PASA_ATTN_FORCE_SIMT 1u
 #define PASA_ATTN_STATS_ONLY 2u
 #define PASA_ATTN_REUSE_STATS 4u
-/*   PASA_ATTN_PAIRED       use the paired-block tensor-core variant (one CTA per SM, kept
- *                          blocks processed two at a time; same results up to rounding) */
-#define PASA_ATTN_PAIRED 8u
-/*   PASA_ATTN_PINGPONG     use the one-CTA-per-SM variant (Q in TMEM, QK^T as a TS MMA, four
- *                          S/P buffers, two softmax warpgroups on alternate ops) where it
- *                          applies (d = 64 / 128, G = 32 / 64 or no grouped term); same
- *                          results up to the fp32 summation order of the denominator */
-#define PASA_ATTN_PINGPONG 16u
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 
@@ -258,16 +251,18 @@ pasa_status pasa_route_read(pasa_route_h route, int32_t* k, int32_t* idx, int32_
 pasa_status pasa_route_pooled_read(pasa_route_h route, double* qbar, double* kbar, void* stream);
 /* HOST outputs (may be NULL) of the last pasa_attn statistics pass, in the I/O dtype
  * (bf16 or fp32): kbar [B*H][N_K][D], vsum [B*H][N_K][D], ht [B*H][N_G][D][D]
- * (ht[.][g][n][k] = Hbar^(g)[k][n]).  Synchronises `stream`. */
+ * (ht[.][g][n][k] = Hbar^(g)[k][n]).  `dtype` declares the element type the caller
+ * sized its buffers for; it must equal the dtype of that pass (the q/k/v dtype of the
+ * last pasa_attn), else EDTYPE and nothing is written.  Synchronises `stream`. */
 pasa_status pasa_attn_stats_read(pasa_route_h route, void* kbar, void* vsum, void* ht,
-                                 void* stream);
+                                 int32_t dtype, void* stream);
 /* Geometry of a handle: dims[0..6] = {B, S, H, D, N_Q, N_K, N_G}. */
 pasa_status pasa_route_dims(pasa_route_h route, int64_t dims[7]);
 /* Synchronous: het [B*H][N_K] fp64 = ||H_j - C||_F of the last pasa_route_v
  * (HOST buffer).  EINVAL if the handle has no prior or it was never computed. */
 pasa_status pasa_route_het_read(pasa_route_h route, double* het, void* stream);
 /* Diagnostics: make the next tensor-core attention launches record a clock64()
- * timeline of CTA (x, y) into dev_buf (DEVICE, 13 x 4096 uint64: producer, MMA
+ * timeline of CTA (x, y) into dev_buf (DEVICE, 17 x 4096 uint64: producer, MMA
  * and softmax events per op); NULL disables.  Returns the element count. */
 int pasa_debug_trace(void* dev_buf, int x, int y);
 /* Diagnostics: performance ablations of the tensor-core attention kernel (1 = the

@@ -23,8 +23,6 @@ PASA_ATTN_FORCE_SIMT = 1
 PASA_ATTN_STATS_ONLY = 2
 PASA_ATTN_REUSE_STATS = 4
 PRIOR = {"none": 0, "global": 1, "group": 2}
-PASA_ATTN_PAIRED = 8
-PASA_ATTN_PINGPONG = 16
 
 # every symbol include/pasa.h declares (tests check the library exports them all)
 EXPORTS = [
@@ -112,7 +110,7 @@ def lib():
     L.pasa_route_read.argtypes = [P, P, P, P, P, P]
     L.pasa_route_pooled_read.argtypes = [P, P, P, P]
     L.pasa_route_dims.argtypes = [P, ctypes.POINTER(ctypes.c_int64)]
-    L.pasa_attn_stats_read.argtypes = [P, P, P, P, P]
+    L.pasa_attn_stats_read.argtypes = [P, P, P, P, I32, P]
     L.pasa_attn_stats_read.restype = ctypes.c_int
     L.pasa_last_launch_count.restype = I32
     L.pasa_last_launch_count.argtypes = []

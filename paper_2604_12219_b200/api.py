@@ -84,6 +84,8 @@ class Budget:
         c = latent_desc(x_tm2) if x_tm2 is not None else None
         tab = None
         if rho_table is not None:
+            if len(rho_table) < T:
+                raise ValueError(f"rho_table has {len(rho_table)} entries, needs T = {T}")
             self._tab = np.ascontiguousarray(np.asarray(rho_table, dtype=np.float64))
             tab = self._tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
         sc = _C.PasaSchedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, tab, kind_i, 0)
@@ -183,17 +185,21 @@ class Route:
                                           _stream_ptr(stream)), "pasa_route_read")
         return dict(k=int(k[0]), idx=idx, count=cnt, mask=mask)
 
-    def stats(self, dtype=torch.bfloat16, stream=None):
+    def stats(self, stream=None):
         """Statistics of the last pasa_attn: (kbar, vsum, ht) as float64 numpy arrays,
-        ht[bh, g, n, k] = Hbar^(g)[k][n]."""
+        ht[bh, g, n, k] = Hbar^(g)[k][n].  Stored in that call's I/O dtype, which the
+        binding recorded (pasa_attn_stats_read rejects a mismatched declaration)."""
         B, S, H, D = self.shape
+        dtype = getattr(self, "_stats_dtype", None)
+        if dtype is None:
+            raise _C.PasaError(_C.PASA_EINVAL, "Route.stats", "no pasa_attn has run on this route")
         t = torch.empty
         kb = t((B * H, self.NK, D), dtype=dtype)
         vs = t((B * H, self.NK, D), dtype=dtype)
         ht = t((B * H, self.NG, D, D), dtype=dtype)
         _C.check(_C.lib().pasa_attn_stats_read(self.handle, ctypes.c_void_p(kb.data_ptr()),
                                                ctypes.c_void_p(vs.data_ptr()),
-                                               ctypes.c_void_p(ht.data_ptr()),
+                                               ctypes.c_void_p(ht.data_ptr()), _DT[dtype],
                                                _stream_ptr(stream)), "pasa_attn_stats_read")
         return (kb.double().numpy(), vs.double().numpy(), ht.double().numpy())
 
@@ -208,19 +214,18 @@ class Route:
 
 
 def attn(q, k, v, route: Route, out=None, *, force_simt=False, stats_only=False,
-         reuse_stats=False, paired=False, pingpong=False, stream=None):
+         reuse_stats=False, stream=None):
     """pasa_attn: returns out ([B, S, H, D], q's dtype).  stats_only / reuse_stats
-    split the call into its statistics and attention kernels (PASA_ATTN_* flags);
-    pingpong selects the one-CTA-per-SM two-warpgroup variant (A/B)."""
+    split the call into its statistics and attention kernels (PASA_ATTN_* flags)."""
     if out is None:
         out = torch.empty_like(q)
     qd, kd, vd, od = tensor_desc(q), tensor_desc(k), tensor_desc(v), tensor_desc(out)
     flags = ((_C.PASA_ATTN_FORCE_SIMT if force_simt else 0)
              | (_C.PASA_ATTN_STATS_ONLY if stats_only else 0)
-             | (_C.PASA_ATTN_REUSE_STATS if reuse_stats else 0)
-             | (_C.PASA_ATTN_PAIRED if paired else 0)
-             | (_C.PASA_ATTN_PINGPONG if pingpong else 0))
+             | (_C.PASA_ATTN_REUSE_STATS if reuse_stats else 0))
     _C.check(_C.lib().pasa_attn_ex(ctypes.byref(qd), ctypes.byref(kd), ctypes.byref(vd),
                                    route.handle, ctypes.byref(od), flags, _stream_ptr(stream)),
              "pasa_attn")
+    if not reuse_stats:
+        route._stats_dtype = q.dtype   # the statistics pass ran in q's dtype
     return out

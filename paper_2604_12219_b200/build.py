@@ -24,7 +24,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
 # per-file extra flags: the route unit must not contract fp64 mul+add into fma
 EXTRA = {"route.cu": ["--fmad=false"]}
 SOURCES = ["api.cpp", "tmap.cpp", "budget.cu", "route.cu", "het.cu", "kv_stats.cu", "attn_simt.cu",
-           "attn_sm100.cu", "attn_sm100_pair.cu", "attn_sm100_pp.cu", "attn_sm100_q256.cu", "kv_stats_sm100.cu"]
+           "attn_sm100.cu", "attn_sm100_q256.cu", "kv_stats_sm100.cu"]
 HEADERS = ["pasa_internal.h", "philox.cuh", "sm100_ptx.cuh"]
 
 

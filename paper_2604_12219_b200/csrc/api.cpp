@@ -358,6 +358,8 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     if ((st = match_route(v, route, "v")) != PASA_OK) return st;
     if ((st = match_route(out, route, "out")) != PASA_OK) return st;
     if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route)");
+    if (flags & ~(PASA_ATTN_FORCE_SIMT | PASA_ATTN_STATS_ONLY | PASA_ATTN_REUSE_STATS))
+        return fail(PASA_EINVAL, "unknown pasa_attn_ex flags 0x%x", flags);
     int launches = 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (!(flags & PASA_ATTN_REUSE_STATS)) {
@@ -375,12 +377,11 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     const pasa_route_cfg& c = route->cfg;
     if (c.Bq == 256) {
         // Bq = 256 (NEXT 4 throughput variant) exists only as the tensor-core kernel
-        if (q->dtype != PASA_BF16 || (flags & (PASA_ATTN_FORCE_SIMT | PASA_ATTN_PAIRED |
-                                               PASA_ATTN_PINGPONG)) ||
+        if (q->dtype != PASA_BF16 || (flags & PASA_ATTN_FORCE_SIMT) ||
             !pasa::attn_sm100_q256_supported(route)) {
             g_launches = launches;
             return fail(PASA_EUNSUPPORTED, "Bq = 256 runs only the bf16 tensor-core kernel "
-                        "(d 64 / 128, G in {32, 64, k*128, >= N_K}, no FORCE_SIMT / PAIRED / PINGPONG)");
+                        "(d 64 / 128, G in {32, 64, k*128, >= N_K}, no FORCE_SIMT)");
         }
         char why[256] = {0};
         cudaError_t e = pasa::launch_attn_sm100_q256(*q, *k, *v, route, *out, s, &launches, why,
@@ -396,14 +397,7 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
         e = pasa::launch_attn_simt(*q, *k, *v, route, *out, s, &launches);
     } else {
         char why[256] = {0};
-        // diagnostics (pasa_debug_flags / pasa_debug_trace) live in the single-warpgroup kernel
-        const bool diag = (pasa::g_dbg & 63) != 0 || pasa::g_trace_buf != nullptr;
-        if (flags & PASA_ATTN_PAIRED)
-            e = pasa::launch_attn_sm100_pair(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
-        else if ((flags & PASA_ATTN_PINGPONG) && !diag && pasa::attn_sm100_pp_supported(route))
-            e = pasa::launch_attn_sm100_pp(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
-        else
-            e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
+        e = pasa::launch_attn_sm100(*q, *k, *v, route, *out, s, &launches, why, sizeof(why));
         if (e == cudaErrorNotSupported) {
             g_launches = launches;
             return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);
@@ -461,9 +455,14 @@ pasa_status pasa_route_pooled_read(pasa_route_h r, double* qbar, double* kbar, v
     return cuda_status(e, "pasa_route_pooled_read");
 }
 
-pasa_status pasa_attn_stats_read(pasa_route_h r, void* kbar, void* vsum, void* ht, void* stream) {
+pasa_status pasa_attn_stats_read(pasa_route_h r, void* kbar, void* vsum, void* ht, int32_t dtype,
+                                 void* stream) {
     if (!r) return fail(PASA_EINVAL, "NULL route");
     if (r->stats_dtype < 0) return fail(PASA_EINVAL, "no statistics pass has run on this route");
+    // the host buffers were sized for `dtype`: refuse to write wider elements into them
+    if (dtype != r->stats_dtype)
+        return fail(PASA_EDTYPE, "statistics are stored as dtype %d, buffers declared as %d",
+                    r->stats_dtype, dtype);
     const size_t es = r->stats_dtype == PASA_F32 ? 4 : 2;
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;

@@ -87,23 +87,12 @@ inline bool sm100_supports_group(int64_t G, int64_t NK) {
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                               int* launches, char* why, size_t why_len);
-// variant (PASA_ATTN_PINGPONG): one CTA per SM, Q in TMEM, two softmax warpgroups on
-// alternate ops (G = 32 / 64 or no grouped term, d = 64 / 128); attn_sm100_pp.cu
-bool attn_sm100_pp_supported(const pasa_route_s* r);
-cudaError_t launch_attn_sm100_pp(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
-                                 pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
-                                 int* launches, char* why, size_t why_len);
 // Bq = 256: one CTA per SM, two 128-row tiles sharing every
 // operand tile the op brings from L2; attn_sm100_q256.cu
 bool attn_sm100_q256_supported(const pasa_route_s* r);
 cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                                    pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                                    int* launches, char* why, size_t why_len);
-// variant: one CTA per SM, kept blocks processed in pairs (N = 128 QK^T), two
-// independent softmax warpgroups (PASA_ATTN_PAIRED)
-cudaError_t launch_attn_sm100_pair(const pasa_tensor& q, const pasa_tensor& k,
-                                   const pasa_tensor& v, pasa_route_s* r, const pasa_tensor& out,
-                                   cudaStream_t st, int* launches, char* why, size_t why_len);
 // tmap.cpp: TMA tensor-map encoding (bf16, 128-byte swizzle, zero OOB fill) and the
 // diagnostics state set by pasa_debug_trace / pasa_debug_flags
 bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,

@@ -25,3 +25,30 @@ def pytest_collection_modifyitems(config, items):
     for item in items:
         if "gpu" in item.keywords:
             item.add_marker(skip)
+
+
+# ---- achieved-error log of the GPU parity tests (record every case) ----
+_ERRORS = []
+
+
+@pytest.fixture
+def parity_log(request):
+    """Append one achieved-error record per compared output: the test id, the
+    case label, max|O_gpu - O_ref| / max|O_ref| and the relative Frobenius error.
+    Written at session end to $PASA_PARITY_LOG (default gpurun_out/parity_errors.json)
+    when any record exists; tools/parity_table.py turns it into profiles/ markdown."""
+    def log(label, max_rel, frob_rel, bound, ref="oracle"):
+        _ERRORS.append(dict(test=request.node.nodeid, case=label, max_rel=float(max_rel),
+                            frob_rel=float(frob_rel), bound=float(bound), ref=ref))
+    return log
+
+
+def pytest_sessionfinish(session, exitstatus):
+    if not _ERRORS:
+        return
+    import json
+    path = os.environ.get("PASA_PARITY_LOG", os.path.join(ROOT, "gpurun_out",
+                                                          "parity_errors.json"))
+    os.makedirs(os.path.dirname(path), exist_ok=True)
+    with open(path, "w") as f:
+        json.dump(_ERRORS, f, indent=1)

@@ -30,3 +30,43 @@ def test_reference_arm_json_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] == "oracle" and cb["cores"] >= 1 and cb["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+
+
+def _bench():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
+def test_gpus_n_relaunches_under_torchrun():
+    """`bench.py --gpus N` outside torchrun becomes one process per GPU: the driver's
+    own torch.distributed.run form, 127.0.0.1 rendezvous, the arguments passed on."""
+    b = _bench()
+    argv = ["--gpus", "4", "--steps", "7", "--dist-backend", "gloo"]
+    cmd = b.torchrun_cmd(argv, 4, 29555)
+    assert cmd[:3] == [sys.executable, "-m", "torch.distributed.run"]
+    assert "--nproc-per-node=4" in cmd and "--nnodes=1" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert "--master-port=29555" in cmd
+    assert cmd[-len(argv) - 1].endswith("bench.py") and cmd[-len(argv):] == argv
+    a = b.parse(argv)
+    assert a.gpus == 4 and a.dist_backend == "gloo" and a.steps == 7
+
+
+def test_gpus_must_match_world_size(monkeypatch):
+    b = _bench()
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    import pytest
+    with pytest.raises(SystemExit):
+        b.main(["--gpus", "4"])
+
+
+def test_reference_arm_world2_rank1_exits_without_work(monkeypatch):
+    """Under torchrun (N > 1) the reference arm runs on rank 0 only; the other ranks
+    exit 0 without work."""
+    b = _bench()
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setenv("RANK", "1")
+    assert b.main(["--gpus", "2", "--impl", "reference"]) == 0

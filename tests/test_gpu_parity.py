@@ -20,6 +20,12 @@ import synth
 pytestmark = pytest.mark.gpu
 
 TOL = {torch.bfloat16: 2e-2, torch.float32: 1e-5}
+# Regression bound on the achieved error, well inside the 2e-2 contract: SURVEY.md §8c
+# emulated the GPU's bf16 storage / rounding choices at 2.7e-3 (max) and round 1's
+# smoke measured 3.5e-3, so a bug that multiplies the error several-fold fails here
+# even though it would pass the contract.  Every achieved value is logged
+# (conftest.parity_log -> profiles/r02_parity_errors.md).
+REG = {torch.bfloat16: 8e-3, torch.float32: 1e-5}
 
 
 @pytest.fixture(scope="module")
@@ -75,15 +81,21 @@ def check_route(P, q, k, cfg, rho, seed=42, step=25, heads=None):
     return route, got, ties
 
 
-def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, pingpong=False):
-    out = P.attn(q, k, v, route, force_simt=force_simt, pingpong=pingpong)
+def errors(o, ref):
+    """(max|o - ref| / max|ref|, ||o - ref||_F / ||ref||_F) in fp64."""
+    d = o - ref
+    return (float(np.abs(d).max() / np.abs(ref).max()),
+            float(np.sqrt((d * d).sum() / (ref * ref).sum())))
+
+
+def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, log=None, label=""):
+    out = P.attn(q, k, v, route, force_simt=force_simt)
     torch.cuda.synchronize()
     B, S, H, D = q.shape
     if pairs is None:
         ref = oracle.attn_with_route(q, k, v, got["idx"], got["count"], Bq=cfg.Bq, Bk=cfg.Bk,
                                      G=cfg.G, comp=cfg.comp)
-        o = oracle.f64(out)
-        err = np.abs(o - ref).max() / np.abs(ref).max()
+        err, frob = errors(oracle.f64(out), ref)
     else:
         bhs = sorted({bh for bh, _ in pairs})
         sub = {bh: n for n, bh in enumerate(bhs)}
@@ -94,15 +106,18 @@ def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, pingpo
         lp = [(sub[bh], i) for bh, i in pairs]
         ref = oracle.attn_pairs(None, None, None, idx, cnt, lp, Bq=cfg.Bq, Bk=cfg.Bk, G=cfg.G,
                                 comp=cfg.comp, qh=qh, kh=kh, vh=vh)
-        err, mx = 0.0, 0.0
+        os_, rs = [], []
         for n, (bh, i) in enumerate(pairs):
             rows = min(cfg.Bq, S - i * cfg.Bq)
-            o = oracle.f64(out[bh // H, i * cfg.Bq:i * cfg.Bq + rows, bh % H])
-            err = max(err, np.abs(o - ref[n, :rows]).max())
-            mx = max(mx, np.abs(ref[n, :rows]).max())
-        err /= mx
+            os_.append(oracle.f64(out[bh // H, i * cfg.Bq:i * cfg.Bq + rows, bh % H]))
+            rs.append(ref[n, :rows])
+        err, frob = errors(np.concatenate(os_), np.concatenate(rs))
     assert np.isfinite(oracle.f64(out)).all()
+    if log is not None:
+        log(label or f"B{B} S{S} H{H} D{D} Bq{cfg.Bq} G{cfg.G} {cfg.comp} {str(q.dtype)[6:]}"
+            + (f" sampled {len(pairs)} (head, q-block)" if pairs else ""), err, frob, REG[q.dtype])
     assert err <= TOL[q.dtype], err
+    assert err <= REG[q.dtype], f"achieved error {err:.3e} above the regression bound"
     return out, err
 
 
@@ -222,37 +237,15 @@ ATTN_CASES = [
 
 
 @pytest.mark.parametrize("case", ATTN_CASES, ids=[c[0] for c in ATTN_CASES])
-def test_attn_parity(pasa, case):
+def test_attn_parity(pasa, case, parity_log):
     name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
     q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=11)
     cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
     route, got, _ = check_route(pasa, q, k, cfg, rho)
-    out, err = check_attn(pasa, q, k, v, route, got, cfg)
+    out, err = check_attn(pasa, q, k, v, route, got, cfg, log=parity_log, label=name)
     # determinism: no atomics on the output path -> bitwise reproducible
     out2 = pasa.attn(q, k, v, route)
     assert torch.equal(out, out2)
-
-
-PINGPONG_CASES = [c for c in ATTN_CASES if c[0] in (
-    "tc_d128_1000", "tc_d128_4100_g32", "tc_d64_4100_g32", "tc_d128_4100_g64",
-    "tc_d128_4100_zeroth", "tc_d64_4100_none", "tc_d64_20000_g64", "tc_d128_odd_k")]
-
-
-@pytest.mark.parametrize("case", PINGPONG_CASES, ids=[c[0] for c in PINGPONG_CASES])
-def test_attn_parity_pingpong(pasa, case):
-    """The one-CTA-per-SM variant (PASA_ATTN_PINGPONG: Q in TMEM, two softmax
-    warpgroups on alternate ops) against the oracle, and against the default kernel:
-    the same running-max decisions and PV order, so they differ only by the fp32
-    summation order of the denominator (a few bf16 ulps of the output)."""
-    name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
-    q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=11)
-    cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
-    route, got, _ = check_route(pasa, q, k, cfg, rho)
-    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pingpong=True)
-    ref = pasa.attn(q, k, v, route)
-    rel = (out.float() - ref.float()).abs().max().item() / ref.float().abs().max().item()
-    assert rel <= 1e-2, rel
-    assert torch.equal(out, pasa.attn(q, k, v, route, pingpong=True))
 
 
 Q256_CASES = [
@@ -271,14 +264,14 @@ Q256_CASES = [
 
 
 @pytest.mark.parametrize("case", Q256_CASES, ids=[c[0] for c in Q256_CASES])
-def test_attn_parity_q256(pasa, case):
+def test_attn_parity_q256(pasa, case, parity_log):
     """Bq = 256 routing (bit-exact against the oracle's route at Bq = 256) and the
     two-tile tensor-core kernel against the oracle's attention at Bq = 256."""
     name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
     q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=13)
     cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
     route, got, _ = check_route(pasa, q, k, cfg, rho)
-    out, _ = check_attn(pasa, q, k, v, route, got, cfg)
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, log=parity_log, label=name)
     assert torch.equal(out, pasa.attn(q, k, v, route))
 
 
@@ -315,9 +308,8 @@ EDGE_CASES = [
 ]
 
 
-@pytest.mark.parametrize("pingpong", [False, True], ids=["default", "pingpong"])
 @pytest.mark.parametrize("case", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
-def test_attn_edge_cases(pasa, case, pingpong):
+def test_attn_edge_cases(pasa, case, parity_log):
     """Single partial blocks (S < Bk, S < Bq), one-token sequences, lengths one past a
     block edge, k = 1 (the floor of R-14) and k = N_K - 1: route bit-exact, output
     within the tolerance of the dtype."""
@@ -325,7 +317,7 @@ def test_attn_edge_cases(pasa, case, pingpong):
     q, k, v = synth.iid_qkv(1, S, 2, D, seed=S + D, dtype=dtype, device="cuda")
     cfg = pasa.RouteCfg(Bq=Bq, G=32, beta=0.1)
     route, got, _ = check_route(pasa, q, k, cfg, rho)
-    check_attn(pasa, q, k, v, route, got, cfg, pingpong=pingpong)
+    check_attn(pasa, q, k, v, route, got, cfg, log=parity_log, label="edge " + name)
 
 
 def test_tensor_core_matches_simt_kernel(pasa):
@@ -386,37 +378,93 @@ def test_strided_output_and_inputs(pasa):
 
 
 # ----------------------------------------------- full BASELINE configs --
-def _pairs(H, NQ, heads, nq):
+def _pairs(heads, NQ, nq=16):
+    """nq q-blocks per head, evenly spread, always q-block 0 and the ragged last one."""
     qs = sorted({0, NQ - 1, *np.linspace(0, NQ - 1, nq).astype(int).tolist()})
     return [(h, int(i)) for h in heads for i in qs]
 
 
-@pytest.mark.parametrize("name,gen,heads,nq", [
-    ("wan13b_480p", "video", [0, 5, 11], 12),
-    ("wan14b_720p", "iid", [0, 39], 6),
-    ("cogvideox5b", "video", [0, 23, 47], 8),
-    ("hunyuan_720p", "iid", [0, 23], 4),
-])
-def test_full_config_sampled(pasa, name, gen, heads, nq):
-    """BASELINE.json configs at full size, in the launch configuration bench.py
-    times: route bit-exact on sampled heads, attention on sampled (head, q-block)
-    pairs always including q-block 0 and the ragged last one."""
-    c = synth.CONFIGS[name]
+def _attn_heads(H):
+    """4 heads spread over the layer, first and last included."""
+    return sorted({0, H - 1, *np.linspace(0, H - 1, 4).round().astype(int).tolist()})
+
+
+def _full_inputs(c, gen, seed):
     B, S, H, D = c["B"], c["S"], c["H"], c["D"]
     if gen == "video":
-        q, k, v = synth.video_qkv(B, c["grid"], H, D, seed=1003, dtype=torch.bfloat16,
-                                  device="cuda")
-    else:
-        q, k, v = synth.iid_qkv(B, S, H, D, seed=1003, dtype=torch.bfloat16, device="cuda")
+        return synth.video_qkv(B, c["grid"], H, D, seed=seed, dtype=torch.bfloat16,
+                               device="cuda")
+    return synth.iid_qkv(B, S, H, D, seed=seed, dtype=torch.bfloat16, device="cuda")
+
+
+@pytest.mark.parametrize("name,gen", [
+    ("wan13b_480p", "video"),
+    ("cogvideox5b", "video"),
+    ("wan14b_720p", "iid"),
+    ("wan14b_720p", "video"),
+    ("hunyuan_720p", "iid"),
+])
+def test_full_config_sampled(pasa, name, gen, parity_log):
+    """SURVEY.md §8c coverage at every BASELINE.json config at full size, in the launch
+    configuration bench.py times: route (k, count, idx, mask) against the oracle on ALL
+    heads, attention on 4 heads x 16 q-blocks always including q-block 0 and the ragged
+    last one (Eq. 7 with App. B grouping)."""
+    c = synth.CONFIGS[name]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    q, k, v = _full_inputs(c, gen, 1003)
     cfg = pasa.RouteCfg(Bq=c["Bq"], G=c["G"], beta=0.1)
     route, got, ties = check_route(pasa, q, k, cfg, c["rho"], seed=pasa.layer_seed(42, 0),
-                                   step=25, heads=heads)
+                                   step=25, heads=None)
     assert ties <= 4
-    NQ = route.NQ
-    check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, NQ, heads, nq))
+    pairs = _pairs(_attn_heads(B * H), route.NQ, 16)
+    assert len(pairs) >= 4 * 16
+    check_attn(pasa, q, k, v, route, got, cfg, pairs=pairs, log=parity_log,
+               label=f"{name} {gen} full size, 4 heads x 16 q-blocks")
 
 
-@pytest.mark.parametrize("variant", ["default", "pingpong", "q256"])
+@pytest.mark.parametrize("name", ["wan13b_480p", "cogvideox5b", "wan14b_720p", "hunyuan_720p"])
+def test_full_config_constant_key_blocks_equal_dense(pasa, name, parity_log):
+    """Oracle-free end-to-end check at full size: with keys constant inside every
+    64-token block, every centroid logit is exact and H_j = 0, so PASA equals dense
+    softmax attention (Eq. 1) for ANY route -- including the ragged
+    last block's true-length weight n_j (R-2, R-7).  Reference: fp32 dense attention
+    computed with torch matmuls, chunked over queries, on 4 heads."""
+    c = synth.CONFIGS[name]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    q, k, v = synth.iid_qkv(B, S, H, D, seed=1006, dtype=torch.bfloat16, device="cuda")
+    NK = (S + 63) // 64
+    first = torch.arange(NK, device="cuda").repeat_interleave(64)[:S] * 64
+    k = k[:, first].contiguous()                  # K_n = K of the block's first token
+    for rho in (c["rho"], 0.4):
+        cfg = pasa.RouteCfg(Bq=c["Bq"], G=c["G"], beta=0.1)
+        route = pasa.Route(B, S, H, D, cfg)
+        route(q, k, make_budget(pasa, rho), pasa.layer_seed(42, 0), 25)
+        out = pasa.attn(q, k, v, route)
+        torch.cuda.synchronize()
+        assert 0 < route.read()["k"] < NK
+        err, frob, mx = 0.0, 0.0, 0.0
+        num = den = 0.0
+        for bh in _attn_heads(B * H):
+            b, h = divmod(bh, H)
+            qh, kh, vh = (t[b, :, h].float() for t in (q, k, v))
+            s = 1.0 / math.sqrt(D)
+            for r0 in range(0, S, 8192):
+                p = torch.softmax((qh[r0:r0 + 8192] @ kh.T) * s, dim=-1)
+                ref = (p @ vh).double()
+                o = out[b, r0:r0 + 8192, h].double()
+                err = max(err, (o - ref).abs().max().item())
+                mx = max(mx, ref.abs().max().item())
+                num += ((o - ref) ** 2).sum().item()
+                den += (ref ** 2).sum().item()
+        err /= mx
+        frob = math.sqrt(num / den)
+        parity_log(f"{name} constant-key blocks rho={rho} vs dense fp32 (4 heads)", err, frob,
+                   REG[torch.bfloat16], ref="dense")
+        assert err <= TOL[torch.bfloat16], err
+        assert err <= REG[torch.bfloat16], err
+
+
+@pytest.mark.parametrize("variant", ["default", "q256"])
 @pytest.mark.parametrize("name", ["wan13b_480p", "cogvideox5b", "wan14b_720p", "hunyuan_720p"])
 def test_full_config_repeat_finite_bitwise(pasa, name, variant):
     """Every BASELINE config at full size in bench.py's launch configuration, three
@@ -432,7 +480,7 @@ def test_full_config_repeat_finite_bitwise(pasa, name, variant):
     first = None
     for _ in range(3):
         out = torch.full_like(q, float("nan"))
-        pasa.attn(q, k, v, route, out, pingpong=variant == "pingpong")
+        pasa.attn(q, k, v, route, out)
         torch.cuda.synchronize()
         assert bool(torch.isfinite(out).all())
         if first is None:
@@ -441,18 +489,18 @@ def test_full_config_repeat_finite_bitwise(pasa, name, variant):
             assert torch.equal(out, first)
 
 
-def test_full_config_q256_sampled(pasa):
-    """Wan 2.1-14B 720p at full size with Bq = 256: route bit-exact on two heads,
-    attention on sampled (head, q-block) pairs incl. the ragged last one, whole output
-    finite and bitwise reproducible."""
+def test_full_config_q256_sampled(pasa, parity_log):
+    """Wan 2.1-14B 720p at full size with Bq = 256: route bit-exact on all heads,
+    attention on 4 heads x 16 q-blocks incl. the ragged last one, whole output finite
+    and bitwise reproducible."""
     c = synth.CONFIGS["wan14b_720p"]
     B, S, H, D = c["B"], c["S"], c["H"], c["D"]
     q, k, v = synth.iid_qkv(B, S, H, D, seed=1005, dtype=torch.bfloat16, device="cuda")
     cfg = pasa.RouteCfg(Bq=256, G=c["G"], beta=0.1)
-    heads = [0, 39]
     route, got, ties = check_route(pasa, q, k, cfg, c["rho"], seed=pasa.layer_seed(42, 0),
-                                   step=25, heads=heads)
+                                   step=25)
     assert ties <= 4
-    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(H, route.NQ, heads, 5))
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(_attn_heads(H), route.NQ),
+                        log=parity_log, label="wan14b_720p Bq=256 full size, 4 heads x 16 q-blocks")
     assert bool(torch.isfinite(out).all())
     assert torch.equal(out, pasa.attn(q, k, v, route))

@@ -1,5 +1,5 @@
 """GPU <-> oracle parity of the K/V statistics pass (Kbar, Vsum, grouped Hbar) and
-of the paired-block attention variant.  Tolerances: Kbar is the bf16 rounding of
+of the attention kernels built on it.  Tolerances: Kbar is the bf16 rounding of
 the oracle's fp64 mean (exact comparison after the same rounding); Vsum and Hbar
 are fp32-accumulated and stored in bf16 (reading R-21): max abs error <= 1e-2 of
 the oracle's max |value| (bf16 storage alone contributes <= 2^-8 relative)."""
@@ -21,14 +21,14 @@ def pasa():
     return P
 
 
-def _run(P, q, k, v, G, rho=0.15, paired=False, Bq=128):
+def _run(P, q, k, v, G, rho=0.15, Bq=128):
     B, S, H, D = q.shape
     route = P.Route(B, S, H, D, P.RouteCfg(Bq=Bq, G=G))
     bud = P.Budget()
     z = torch.zeros(64, device="cuda")
     bud(z, z, z, T=50, step=25, rho_table=[rho] * 50)
     route(q, k, bud, 7, 25)
-    out = P.attn(q, k, v, route, paired=paired)
+    out = P.attn(q, k, v, route)
     torch.cuda.synchronize()
     return route, out
 
@@ -67,7 +67,7 @@ def test_kv_stats_kernels_agree(pasa, D, G):
     assert np.abs(a - b).max() <= 1e-2 * np.abs(b).max()
 
 
-@pytest.mark.parametrize("variant", ["paired", "prefetch"])
+@pytest.mark.parametrize("variant", ["default"])
 @pytest.mark.parametrize("S,H,D,G,rho", [(4100, 2, 128, 32, 0.15), (4100, 2, 64, 64, 0.2),
                                          (20000, 1, 128, 128, 0.15), (1000, 2, 128, 1000, 0.11),
                                          (9000, 2, 128, 32, 0.05), (9000, 1, 64, 4096, 0.3)])
@@ -76,7 +76,7 @@ def test_variant_parity(pasa, S, H, D, G, rho, variant):
     from paper_2604_12219_b200 import _C
     old = _C.lib().pasa_debug_flags(0)
     try:
-        route, out = _run(pasa, q, k, v, G, rho=rho, paired=variant == "paired")
+        route, out = _run(pasa, q, k, v, G, rho=rho)
     finally:
         _C.lib().pasa_debug_flags(old)
     got = route.read()

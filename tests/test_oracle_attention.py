@@ -125,6 +125,36 @@ def test_constant_key_blocks_exact_for_any_route(comp):
     assert np.abs(o[0, :, 0] - ref).max() < 1e-12
 
 
+@pytest.mark.parametrize("G", [1, 4, 13])
+@pytest.mark.parametrize("comp", ["grouped", "zeroth"])
+def test_constant_key_blocks_exact_ragged(comp, G):
+    """Reading R-7's true block lengths, pinned without the NumPy twin: S = 203, Bk = 16
+    leaves a last KV block of n_j = 11 tokens and a last q-block of 11 rows.  With
+    constant keys per block every centroid logit is exact and H_j = 0, so Eq. 7 equals
+    dense attention (Eq. 1) for any route -- but only if a dropped
+    block enters the denominator with its true weight n_j (R-2).  Weighting the ragged
+    block by Bk = 16 instead of 11 (or padding it with zero keys) breaks the equality,
+    and the routes below drop the ragged block in some rows and keep it in others."""
+    rng = np.random.default_rng(12)
+    S, D, Bk, Bq = 203, 8, 16, 32
+    NK, NQ = (S + Bk - 1) // Bk, (S + Bq - 1) // Bq
+    kb = rng.standard_normal((NK, D))
+    k = np.repeat(kb, Bk, 0)[:S][None, :, None, :]
+    q = 1.5 * rng.standard_normal((1, S, 1, D))
+    v = rng.standard_normal((1, S, 1, D))
+    idx = random_route(3, 1, NQ, NK, 4)
+    assert (idx[0] == NK - 1).any(axis=1).any() and not (idx[0] == NK - 1).any(axis=1).all()
+    o = oracle.attn_with_route(q, k, v, idx, Bq=Bq, Bk=Bk, G=G, comp=comp)
+    ref = brute.dense_attention(q[0, :, 0], k[0, :, 0], v[0, :, 0])
+    assert np.abs(o[0, :, 0] - ref).max() < 1e-12
+    # the same check fails if the ragged block is weighted as a full block: the
+    # denominator weight is what the equality pins
+    ref_bad = brute.dense_attention(np.vstack([q[0, :, 0]]),
+                                    np.vstack([k[0, :, 0], np.repeat(kb[-1:], Bk - S % Bk, 0)]),
+                                    np.vstack([v[0, :, 0], np.zeros((Bk - S % Bk, D))]))
+    assert np.abs(o[0, :, 0] - ref_bad).max() > 1e-6
+
+
 @pytest.mark.parametrize("G", [1, 3, 4, 100])
 @pytest.mark.parametrize("comp", ["grouped", "zeroth", "none"])
 def test_c_oracle_matches_numpy_brute(G, comp):

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Time the tensor-core attention kernels (default and paired variant) under
+"""Time the tensor-core attention kernel under
 diagnostic ablations (pasa_debug_flags).  REPS > 1 interleaves the
 configurations and reports min / median (the pool's clocks drift under power cap)."""
 import os
@@ -25,16 +25,15 @@ out = P.attn(q, k, v, route, stats_only=True)
 REPS = int(os.environ.get("REPS", "1"))
 results = {}
 for rep in range(REPS):
-  for variant in os.environ.get("VARIANTS", "default,paired").split(","):
-    paired = variant == "paired"
+  for variant in os.environ.get("VARIANTS", "default").split(","):
     for flags in [int(f) for f in os.environ.get("FLAGS", "0,1,3").split(",")]:
         _C.lib().pasa_debug_flags(flags)
         for _ in range(2):
-            P.attn(q, k, v, route, out, reuse_stats=True, paired=paired)
+            P.attn(q, k, v, route, out, reuse_stats=True)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(5):
-            P.attn(q, k, v, route, out, reuse_stats=True, paired=paired)
+            P.attn(q, k, v, route, out, reuse_stats=True)
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5

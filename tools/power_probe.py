@@ -34,7 +34,6 @@ for bq in (128, 256):
     out = P.attn(q, k, v, r)
     if bq == 128:
         variants["default (Bq 128, 2 CTAs/SM)"] = (r, out, {})
-        variants["pingpong (Bq 128, 1 CTA/SM, Q in TMEM)"] = (r, out, {"pingpong": True})
     else:
         variants["q256 (Bq 256, 1 CTA/SM, 2 tiles)"] = (r, out, {})
 

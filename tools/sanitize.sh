@@ -1,18 +1,20 @@
 #!/usr/bin/env bash
-# compute-sanitizer memcheck / racecheck over a subset of the GPU parity tests (run on the
-# B200 box from the repo root):  /usr/local/graft/bin/gpurun --timeout 1800 -- 'bash tools/sanitize.sh'
+# compute-sanitizer memcheck / racecheck / synccheck over the GPU parity tests (run on the
+# B200 box from the repo root):  /usr/local/graft/bin/gpurun --timeout 2400 -- 'bash tools/sanitize.sh'
+# SURVEY.md §4.2 T6.  Small shapes only: the sanitizers slow kernels down ~100x.
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
 export PYTEST_ADDOPTS="-p no:cacheprovider"
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 --log-file gpurun_out/san_memcheck.txt \
-  python -m pytest tests/test_gpu_parity.py -q -x -k "tc_d128_4100_g32 or tc_d64_4100_g32 or tc_d128_g8 or tc_d64_g16 or ragged1000 or iid16k or tc_d128_20000_g128 or budget" > gpurun_out/san_memcheck.log 2>&1
-tail -3 gpurun_out/san_memcheck.log; grep -c "Invalid\|ERROR SUMMARY" gpurun_out/san_memcheck.txt; grep "ERROR SUMMARY" gpurun_out/san_memcheck.txt | head
-timeout 900 compute-sanitizer --tool memcheck --print-limit 20 --log-file gpurun_out/san_memcheck2.txt \
-  python -m pytest tests/test_gpu_prior.py tests/test_gpu_stats.py -q -x > gpurun_out/san_memcheck2.log 2>&1
-tail -3 gpurun_out/san_memcheck2.log; grep "ERROR SUMMARY" gpurun_out/san_memcheck2.txt | head
-timeout 900 compute-sanitizer --tool racecheck --print-limit 20 --log-file gpurun_out/san_race.txt \
-  python -m pytest tests/test_gpu_parity.py -q -x -k "ragged1000 or iid16k or clustered" > gpurun_out/san_race.log 2>&1
-tail -3 gpurun_out/san_race.log; grep "ERROR SUMMARY\|RACECHECK SUMMARY" gpurun_out/san_race.txt | head
-# the round's attention variants: ping-pong (one CTA/SM, Q in TMEM) and Bq = 256 (two tiles)
-timeout 1200 compute-sanitizer --tool memcheck --print-limit 20 --log-file gpurun_out/san_memcheck3.txt \
-  python -m pytest tests/test_gpu_parity.py -q -x -k "pingpong and (tc_d128_4100_g32 or tc_d64_4100_g32 or S65 or k1) or q256_d128_4100_g32 or q256_d64_4100_g32 or q256_d128_20000 or test_attn_q256_edges" > gpurun_out/san_memcheck3.log 2>&1
-tail -3 gpurun_out/san_memcheck3.log; grep "ERROR SUMMARY" gpurun_out/san_memcheck3.txt | head
+ATTN="tc_d128_1000 or tc_d128_4100_g32 or tc_d64_4100_g32 or tc_d128_g8 or tc_d64_g16 or tc_d128_4100_zeroth or tc_d64_4100_none or S65 or k1 or q256_d128_4100_g32 or q256_d64_4100_g32"
+ROUTE="ragged1000 or iid16k or clustered or budget"
+run() {  # tool, log-stem, pytest -k expression, files...
+  local tool=$1 stem=$2 expr=$3; shift 3
+  timeout 1500 compute-sanitizer --tool "$tool" --print-limit 20 --log-file "gpurun_out/san_${stem}.txt" \
+    python -m pytest "$@" -q -x -k "$expr" > "gpurun_out/san_${stem}.log" 2>&1
+  echo "== $tool $stem rc=$?"; tail -2 "gpurun_out/san_${stem}.log"
+  grep "ERROR SUMMARY\|RACECHECK SUMMARY\|SYNCCHECK SUMMARY" "gpurun_out/san_${stem}.txt" | sort | uniq -c | head
+}
+run memcheck  memcheck_attn  "$ATTN or $ROUTE" tests/test_gpu_parity.py
+run racecheck racecheck_attn "$ATTN" tests/test_gpu_parity.py
+run synccheck synccheck_attn "$ATTN" tests/test_gpu_parity.py
+run racecheck racecheck_route "$ROUTE" tests/test_gpu_parity.py
+run memcheck  memcheck_stats "kv_stats" tests/test_gpu_stats.py
