@@ -241,6 +241,7 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->vsum_lp = w + L.off_vsum;
     r->ht = w + L.off_ht;
     r->idx = reinterpret_cast<int32_t*>(w + L.off_idx);
+    r->idx_ld = L.NK;
     r->count = reinterpret_cast<int32_t*>(w + L.off_count);
     r->mask = reinterpret_cast<uint32_t*>(w + L.off_mask);
     const bool pr = cfg->prior != PASA_PRIOR_NONE;

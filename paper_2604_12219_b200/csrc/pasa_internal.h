@@ -35,7 +35,8 @@ struct pasa_route_s {
     void* vsum_lp;                   // [BH][NK][D]
     void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)
     float* part;                     // [BH][ceil(NK/32)][D][D] fp32 chunk sums (G > 64)
-    int32_t* idx;                    // [BH][NQ][NK]
+    int32_t* idx;                    // [BH][NQ][idx_ld] (first count entries valid, ascending)
+    int64_t idx_ld;                  // row stride of idx (entries)
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]
     double* het;                     // [BH][NK] ||H_j - C||_F (prior-enabled handles only)

@@ -253,6 +253,16 @@ __device__ __forceinline__ void bar_sync(uint32_t id, uint32_t n) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// per-warpgroup register budget (all 128 threads of the warpgroup execute it)
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_inc() {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(N));
+}
+template <uint32_t N>
+__device__ __forceinline__ void setmaxnreg_dec() {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(N));
+}
+
 // ------------------------------------------------------------ descriptors --
 // UMMA shared-memory descriptor, SWIZZLE_128B, Blackwell version bits = 1.
 // K-major (rows of 128 B, 8-row groups 1024 B apart):  lbo = 16 B (unused), sbo = 1024 B.
@@ -297,6 +307,21 @@ __device__ __forceinline__ float ex2_poly(float x) {
     p = fmaf(p, f, 1.0f);
     return __int_as_float(__float_as_int(p) + (ji << 23));
 }
+// Same 2^x with no ALU-pipe integer step except the clamp: the exponent insert
+// bits(p) + (j << 23) is one integer multiply-add bits(t) * 2^23 + bits(p) (IMAD, FMA
+// pipe), because bits(t) = 0x4B400000 + j and 0x4B400000 << 23 == 0 (mod 2^32).  x is
+// clamped at -125 so 2^j * p stays a normal number.
+__device__ __forceinline__ float ex2_fma(float x) {
+    x = fmaxf(x, -125.f);
+    const float t = x + 12582912.0f;
+    const float f = x - (t - 12582912.0f);
+    float p = fmaf(0.05500868998260835f, f, 0.2422106313698579f);
+    p = fmaf(p, f, 0.6932829170291438f);
+    p = fmaf(p, f, 1.0f);
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 8388608, %2;" : "=r"(r) : "r"(__float_as_uint(t)), "r"(__float_as_uint(p)));
+    return __uint_as_float(r);
+}
 // packed fp32 pairs (sm_100 FFMA2 / FADD2): two lanes per instruction, each rounded
 // exactly as the scalar fma.rn / add.rn
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
@@ -316,6 +341,23 @@ __device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
         : "=f"(d.x), "=f"(d.y)
         : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
     return d;
+}
+// ex2_fma on a pair, the floating-point steps as packed FADD2 / FFMA2 (FMA pipe), the clamp
+// (FMNMX) and exponent insert (IMAD) per element: 5 issue slots per element, no MUFU.
+__device__ __forceinline__ float2 ex2_fma2(float2 x) {
+    x.x = fmaxf(x.x, -125.f);
+    x.y = fmaxf(x.y, -125.f);
+    const float2 t = fadd2(x, make_float2(12582912.0f, 12582912.0f));
+    const float2 j = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+    const float2 f = ffma2(j, make_float2(-1.f, -1.f), x);                 // x - j in [-1/2, 1/2]
+    float2 p = ffma2(make_float2(0.05500868998260835f, 0.05500868998260835f), f,
+                     make_float2(0.2422106313698579f, 0.2422106313698579f));
+    p = ffma2(p, f, make_float2(0.6932829170291438f, 0.6932829170291438f));
+    p = ffma2(p, f, make_float2(1.0f, 1.0f));
+    uint32_t r0, r1;
+    asm("mad.lo.u32 %0, %1, 8388608, %2;" : "=r"(r0) : "r"(__float_as_uint(t.x)), "r"(__float_as_uint(p.x)));
+    asm("mad.lo.u32 %0, %1, 8388608, %2;" : "=r"(r1) : "r"(__float_as_uint(t.y)), "r"(__float_as_uint(p.y)));
+    return make_float2(__uint_as_float(r0), __uint_as_float(r1));
 }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
     float r;
