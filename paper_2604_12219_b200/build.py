@@ -25,7 +25,7 @@ COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
 EXTRA = {"route.cu": ["--fmad=false"]}
 SOURCES = ["api.cpp", "tmap.cpp", "budget.cu", "route.cu", "het.cu", "kv_stats.cu", "attn_simt.cu",
            "attn_sm100.cu", "attn_sm100_q256.cu", "kv_stats_sm100.cu"]
-HEADERS = ["pasa_internal.h", "philox.cuh", "sm100_ptx.cuh"]
+HEADERS = ["pasa_internal.h", "philox.cuh", "sm100_ptx.cuh", "fastlog.cuh", "logtab.h"]
 
 
 def nvcc() -> str:

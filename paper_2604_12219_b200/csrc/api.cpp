@@ -39,7 +39,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
-    size_t off_hdr, off_qbar, off_kbar, off_scores, off_sigma, off_kbar_lp, off_vsum, off_ht, off_idx,
+    size_t off_hdr, off_qbar, off_kbar, off_kfrag, off_scores, off_kbar_lp, off_vsum, off_ht, off_idx,
         off_count, off_mask, off_het, off_prior, off_hj, off_hgs, off_hglob, off_part, total;
 };
 
@@ -77,8 +77,10 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_hdr = o;      o = align_up(o + 64);
     L.off_qbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NQ * D);
     L.off_kbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NK * D);
-    L.off_scores = o;   o = align_up(o + sizeof(double) * L.BH * L.NQ * L.NK);
-    L.off_sigma = o;    o = align_up(o + sizeof(double) * L.BH * L.NQ);
+    L.off_kfrag = o;    o = align_up(o + sizeof(double) * L.BH * ((L.NK + 7) / 8) * 8 * D);
+    // fp64 score rows: on chip (shared memory) unless a row tile does not fit there
+    const bool gsc = pasa::route_rows_per_cta(L.NK, D) == 0;
+    L.off_scores = o;   o = align_up(o + (gsc ? sizeof(double) * L.BH * L.NQ * pasa::route_score_stride(L.NK) : 0));
     L.off_kbar_lp = o;  o = align_up(o + 4 * L.BH * L.NK * D);
     L.off_vsum = o;     o = align_up(o + 4 * L.BH * L.NK * D);
     L.off_ht = o;       o = align_up(o + 4 * L.BH * L.NG * D * D);
@@ -235,8 +237,9 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->hdr = reinterpret_cast<int32_t*>(w + L.off_hdr);
     r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
     r->kbar = reinterpret_cast<double*>(w + L.off_kbar);
-    r->scores = reinterpret_cast<double*>(w + L.off_scores);
-    r->sigma = reinterpret_cast<double*>(w + L.off_sigma);
+    r->kfrag = reinterpret_cast<double*>(w + L.off_kfrag);
+    r->scores = pasa::route_rows_per_cta(L.NK, D) == 0 ? reinterpret_cast<double*>(w + L.off_scores)
+                                                        : nullptr;
     r->kbar_lp = w + L.off_kbar_lp;
     r->vsum_lp = w + L.off_vsum;
     r->ht = w + L.off_ht;

@@ -29,8 +29,9 @@ struct pasa_route_s {
     int32_t* hdr;                    // device: [0] = k of the last pasa_route
     double* qbar;                    // [BH][NQ][D]
     double* kbar;                    // [BH][NK][D]
-    double* scores;                  // [BH][NQ][NK] scratch (r, fp64)
-    double* sigma;                   // [BH][NQ] row standard deviations (scratch)
+    double* kfrag;                   // Kbar in DMMA B-fragment order [BH][ceil(NK/8)][D/8][64]
+    double* scores;                  // [BH][NQ][NKP] fp64 score rows, only when they do not
+                                     // fit in shared memory (route_rows_per_cta == 0), else null
     void* kbar_lp;                   // [BH][NK][D]   bf16 or fp32 (4 B/elem capacity)
     void* vsum_lp;                   // [BH][NK][D]
     void* ht;                        // [BH][NG][D][D] Hbar^T per group (row n, col k)
@@ -61,6 +62,11 @@ cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, in
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches);
+// fused scores / sigma / top-k kernel: rows of scores per CTA held in shared memory
+// (0: they do not fit and live in the workspace's global scratch) and the odd row
+// stride of a score row
+int route_rows_per_cta(int64_t NK, int64_t D);
+int64_t route_score_stride(int64_t NK);
 cudaError_t launch_het(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r,
                        cudaStream_t st, int* launches);
 // KV blocks per work chunk of the prior kernels (a divisor of G, <= 32)

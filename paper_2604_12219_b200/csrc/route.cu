@@ -9,8 +9,11 @@
 // with --fmad=false and uses __d*_rn intrinsics so nvcc contracts nothing.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "pasa_internal.h"
 #include "philox.cuh"
+#include "fastlog.cuh"
 
 namespace pasa {
 namespace {
@@ -46,10 +49,12 @@ struct PoolArgs {
     int32_t bsz;    // block size in tokens
     int64_t nblk;   // blocks per head
     double* out;    // [BH][nblk][D]
+    double* frag;   // optional DMMA B-fragment copy [BH][ceil(nblk/8)][D/8][8][4][2]
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) pool_kernel(PoolArgs qa, PoolArgs ka, int64_t q_tasks,
+// 4 CTAs (32 warps) per SM: at 3 (70 registers) the kernel lost 40% of its bandwidth
+__global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, int64_t q_tasks,
                                                    int64_t total) {
     int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (task >= total) return;
@@ -90,23 +95,27 @@ __global__ void __launch_bounds__(256) pool_kernel(PoolArgs qa, PoolArgs ka, int
         for (int i = 0; i < 8; ++i) acc[i] = __dadd_rn(acc[i], v0[i]);
     }
     double n = (double)(t1 - t0);
-    double* o = a.out + (bh * a.nblk + blk) * a.D + dg * 8;
+    double m[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) o[i] = __ddiv_rn(acc[i], n);
+    for (int i = 0; i < 8; ++i) m[i] = __ddiv_rn(acc[i], n);
+    // 16-byte stores (a warp's scalar 8-byte stores would each touch 32 sectors)
+    double2* o = reinterpret_cast<double2*>(a.out + (bh * a.nblk + blk) * a.D + dg * 8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = make_double2(m[2 * i], m[2 * i + 1]);
+    if (a.frag) {
+        // fragment order of the fused route kernel's B operand: block j = 8 ct + fr, dims
+        // 8 dg + 4 h + fk -> [ct][dg][fr][fk][h] (one 512-byte run per (ct, dg): a warp's
+        // 16-byte loads of two consecutive k-steps are contiguous)
+        double2* f = reinterpret_cast<double2*>(
+            a.frag + ((bh * ((a.nblk + 7) / 8) + blk / 8) * (a.D / 8) + dg) * 64 + (blk % 8) * 8);
+#pragma unroll
+        for (int fk = 0; fk < 4; ++fk) f[fk] = make_double2(m[fk], m[4 + fk]);
+    }
 }
 
 // ---------------------------------------------------------------------------
-// a3: block scores r_ij = s * dot(Qbar_i, Kbar_j), a tiled fp64 GEMM on the fp64
-// tensor core.  Every output accumulates an fma chain over the head dimension in
-// ascending order (R2: the chain of DMMA 8x8x4 steps is that chain, bit for bit), so
-// the per-element result is independent of the tiling.
+// shared helpers of the fused kernel
 // ---------------------------------------------------------------------------
-constexpr int kST = 128;    // tile edge (rows i x columns j)
-constexpr int kSK = 16;     // D chunk staged in smem
-constexpr int kSP = kSK + 4;   // padded smem row (doubles): conflict-free DMMA fragments
-
-constexpr int kSThreads = 256;   // 8 warps; warp w owns row tiles 2w, 2w+1 x 16 column tiles
-
 // fp64 tensor core: d (+)= a * b on an 8x8x4 tile.  Measured on this pool
 // (tools/dmma_exact.cu): bit-identical to the sequential fma chain over k = 0..3, so
 // a chain of these in ascending k is the oracle's ascending-d fma chain (R2).
@@ -115,155 +124,6 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
-
-__global__ void __launch_bounds__(kSThreads, 1) scores_kernel(const double* __restrict__ qbar,
-                                                        const double* __restrict__ kbar, int64_t NQ,
-                                                        int64_t NK, int64_t D, double s,
-                                                        const double* __restrict__ prior,
-                                                        double* __restrict__ r) {
-    __shared__ double sq[kST][kSP];    // rows i of Qbar, one 16-dim chunk
-    __shared__ double sk[kST][kSP];    // rows j of Kbar
-    const int64_t bh = blockIdx.z;
-    const int64_t i0 = (int64_t)blockIdx.y * kST, j0 = (int64_t)blockIdx.x * kST;
-    const double* Q = qbar + bh * NQ * D;
-    const double* K = kbar + bh * NK * D;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int fr = lane >> 2, fk = lane & 3;     // DMMA fragment row / k index
-    double acc[2][16][2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 16; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-    // register double buffer: chunk d0 + kSK is in flight while chunk d0 is consumed
-    constexpr int kPer = kSK * kST / kSThreads;
-    double pq[kPer], pk[kPer];
-    auto fetch = [&](int64_t d0) {
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = tid + kSThreads * u;
-            const int row = e / kSK, col = e % kSK;
-            const int64_t gi = i0 + row, gj = j0 + row;
-            pq[u] = gi < NQ ? Q[gi * D + d0 + col] : 0.0;
-            pk[u] = gj < NK ? K[gj * D + d0 + col] : 0.0;
-        }
-    };
-    fetch(0);
-    for (int64_t d0 = 0; d0 < D; d0 += kSK) {
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = tid + kSThreads * u;
-            sq[e / kSK][e % kSK] = pq[u];
-            sk[e / kSK][e % kSK] = pk[u];
-        }
-        __syncthreads();
-        if (d0 + kSK < D) fetch(d0 + kSK);
-#pragma unroll
-        for (int ks = 0; ks < kSK / 4; ++ks) {      // ascending d: r_ij's fma chain order
-            const int kk = 4 * ks + fk;
-            const double a0 = sq[(2 * warp) * 8 + fr][kk];
-            const double a1 = sq[(2 * warp + 1) * 8 + fr][kk];
-            double bv[16];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) bv[c] = sk[c * 8 + fr][kk];
-#pragma unroll
-            for (int c = 0; c < 16; ++c) {
-                dmma_8x8x4(acc[0][c][0], acc[0][c][1], a0, bv[c]);
-                dmma_8x8x4(acc[1][c][0], acc[1][c][1], a1, bv[c]);
-            }
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-        const int64_t gi = i0 + (2 * warp + a) * 8 + fr;
-        if (gi >= NQ) continue;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int64_t gj = j0 + c * 8 + 2 * fk + h;
-                if (gj < NK) {
-                    double x = __dmul_rn(s, acc[a][c][h]);
-                    if (prior) x = __dadd_rn(x, prior[bh * NK + gj]);   // Eq. 8 prior term
-                    r[(bh * NQ + gi) * NK + gj] = x;
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// a4 (row statistics): sigma_i, the population std of score row i (R3).  The
-// sums run sequentially in ascending j exactly as in the oracle (bit-exact), one
-// thread per row; 128 rows per CTA are staged through shared memory in column
-// chunks so the loads are coalesced and 128 sequential chains run concurrently.
-// ---------------------------------------------------------------------------
-constexpr int kRsRows = 64, kRsCols = 32;
-
-__global__ void __launch_bounds__(kRsRows * 2) rowstats_kernel(const double* __restrict__ r,
-                                                               int64_t rows, int64_t NK,
-                                                               double* __restrict__ sigma) {
-    // 128 threads stage a [64 rows x 64 cols] chunk (register prefetch of the next
-    // chunk overlaps the sequential sums of the current one); threads 0..63 own a row.
-    __shared__ double tile[2][kRsRows][kRsCols + 1];
-    const int tid = threadIdx.x;
-    const int64_t r0 = (int64_t)blockIdx.x * kRsRows;
-    const int nrows = (int)min((int64_t)kRsRows, rows - r0);
-    const int nchunk = (int)((NK + kRsCols - 1) / kRsCols);
-    constexpr int kPer = kRsRows * kRsCols / (kRsRows * 2);   // 32 loads per thread per chunk
-    double buf[kPer];
-    auto fetch = [&](int c) {
-        const int64_t c0 = (int64_t)c * kRsCols;
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = tid + u * (kRsRows * 2);
-            const int rr = e / kRsCols, cc = e % kRsCols;
-            buf[u] = (rr < nrows && c0 + cc < NK) ? __ldg(r + (r0 + rr) * NK + c0 + cc) : 0.0;
-        }
-    };
-    auto stash = [&](int slot) {
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) {
-            const int e = tid + u * (kRsRows * 2);
-            tile[slot][e / kRsCols][e % kRsCols] = buf[u];
-        }
-    };
-    double sum = 0.0, mu = 0.0, acc = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-        fetch(0);
-        for (int c = 0; c < nchunk; ++c) {
-            const int slot = c & 1;
-            stash(slot);
-            __syncthreads();
-            if (c + 1 < nchunk) fetch(c + 1);
-            const int nc = (int)min((int64_t)kRsCols, NK - (int64_t)c * kRsCols);
-            if (tid < nrows) {
-                if (pass == 0) {
-                    for (int cc = 0; cc < nc; ++cc) sum = __dadd_rn(sum, tile[slot][tid][cc]);
-                } else {
-                    for (int cc = 0; cc < nc; ++cc) {
-                        const double dl = __dsub_rn(tile[slot][tid][cc], mu);
-                        acc = __fma_rn(dl, dl, acc);
-                    }
-                }
-            }
-        }
-        __syncthreads();
-        if (pass == 0) mu = __ddiv_rn(sum, (double)NK);
-    }
-    if (tid < nrows) sigma[r0 + tid] = __dsqrt_rn(__ddiv_rn(acc, (double)NK));
-}
-
-// ---------------------------------------------------------------------------
-// a4 + a5: one warp per (head, query block) row.  Element j = 32 m + lane lives in
-// register m of lane `lane`.  Gumbel bias, then the k-th largest orderable key T is
-// found bit by bit (T = the largest value with #{key >= T} >= k), ties at T go to
-// the smallest j (R-13), and the ballot of each 32-block chunk is directly the
-// route's mask word; the ascending index list follows from ballot prefix counts.
-// ---------------------------------------------------------------------------
-constexpr int kSelWarps = 4;
-// 5 CTAs (20 warps) per SM for M <= 40: a few spilled registers cost less than the
-// lost occupancy (route at Wan-14B 1.52 -> 1.34 ms with the window search below)
 
 __device__ __forceinline__ uint64_t orderable(double x) {
     x = __dadd_rn(x, 0.0);  // -0.0 -> +0.0: the oracle's double compare treats them as equal
@@ -279,68 +139,86 @@ __device__ __forceinline__ int device_k(const BudgetRec* rec, int64_t NK) {
     return (int)k;
 }
 
-struct SelArgs {
-    const double* r;          // [BH][NQ][NK]
-    const double* sigma;      // [BH][NQ]
+// ---------------------------------------------------------------------------
+// a3 + a4 + a5 fused (the route's hot kernel): one CTA per (head, 8 query-block
+// rows), two CTAs per SM.  The fp64 scores of its rows against every KV block are
+// computed on the fp64 tensor core into SHARED memory and never leave the chip;
+// sigma_i, the Philox / Gumbel bias and the top-k threshold search run from there.
+//
+//   phase A  (all 8 warps) DMMA m8n8k4: the 8 Qbar rows are the A operand (shared
+//            memory), Kbar the B operand straight from L2 into registers (4 k-steps
+//            per block, two blocks in flight), groups of 4 column tiles round-robin
+//            over the warps, no barrier inside the phase; r_ij = s * acc (+ prior_j)
+//   phase B  (warp w = row w) sigma_i with the oracle's sequential sums (R3), every
+//            lane walking the row (broadcast reads: no divergence)
+//   phase C  (same warp) keys r~ = r + (beta sigma_i) g (two rounded operations, R5)
+//            written over the row in place, k-th largest by a bitwise threshold search
+//            over the shared-memory keys, idx / mask / count out (R6, R-13)
+//
+// Two co-resident CTAs interleave their phases on the SM (fp64 tensor pipe in A,
+// integer / fp64 CUDA-core work in C).  When the score rows do not fit in shared
+// memory (N_K > ~1,570 at 2 CTAs/SM) they live in a global scratch slice of the
+// workspace (same code; written and read back by the same CTA, so it stays in L2).
+// ---------------------------------------------------------------------------
+constexpr int kFCG4 = 4;               // column tiles x row tiles per warp work group
+constexpr int kFKS = 4;                // k-steps per register block (phase A)
+constexpr int kFRows = 8;              // score rows per CTA (one DMMA row tile)
+constexpr int kFHR = 40;               // key high words per lane held in registers (N_K <= 1280)
+struct FusedArgs {
+    const double* qbar;        // [BH][NQ][D]
+    const double* kfrag;       // Kbar in B-fragment order (pool_kernel)
+    const double* prior;       // [BH][NK] or nullptr
     const BudgetRec* rec;
-    int64_t rows, NQ, NK, W, H, H_total, head_offset;
-    double beta;
-    uint32_t key0, key1;      // Philox key = (lo32 seed, hi32 seed)
-    uint32_t step;
-    int32_t* idx;             // [BH][NQ][NK]
-    int32_t* count;           // [BH][NQ]
-    uint32_t* mask;           // [BH][NQ][W]
+    int64_t NQ, NK, W, H, H_total, head_offset;
+    int D, NKP;                // NKP: odd row stride of the score rows (doubles)
+    double s, beta;
+    uint32_t key0, key1, step;
+    int32_t* idx;              // [BH][NQ][NK]
+    int32_t* count;            // [BH][NQ]
+    uint32_t* mask;            // [BH][NQ][W]
     int32_t* hdr;
+    double* gsc;               // global score rows [BH][NQ][NKP] when !SMEM_SC
 };
 
-template <int MAXM>
-// occupancy over registers: a few spilled keys cost less than idle warps (route at
-// Wan-14B 1.52 -> 1.34 ms with 5 CTAs/SM for MAXM <= 40; HunyuanVideo's MAXM = 64
-// 2.70 -> 2.03 ms with 4 instead of 2 CTAs/SM, 3, 5 and 6 measured slower)
-__global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 4) select_kernel(SelArgs a) {
-    const int lane = threadIdx.x & 31;
-    const int64_t row = (int64_t)blockIdx.x * kSelWarps + (threadIdx.x >> 5);   // bh * NQ + i
-    if (row >= a.rows) return;
-    const int64_t bh = row / a.NQ, i = row % a.NQ;
-    const int NK = (int)a.NK;
+__device__ const LogEnt g_logtab[128] = PASA_LOGTAB_INIT;
+
+// Gumbel variate of score (i, j) of global head gh (R4, R-12): g = -log(-log u), with the
+// table-driven fp64 log of fastlog.cuh (within 1.5 ulp of the exact log; glibc's, which
+// the oracle uses, is within 0.52: r~ moves by ~1e-16 relative, inside the documented-tie
+// margin)
+__device__ __forceinline__ double gumbel(uint32_t j, uint32_t i, uint32_t gh, uint32_t step,
+                                         uint32_t k0, uint32_t k1) {
+    const uint32_t x0 = philox4x32_10_x0(j, i, gh, step, k0, k1);
+    const double u = __dmul_rn(__dadd_rn((double)x0, 0.5), 2.3283064365386963e-10);
+    return -fastlog_tab(g_logtab, -fastlog_tab(g_logtab, u));
+}
+
+// The k-th largest orderable key T of one row (the largest value with #{key >= T} >= k),
+// ties at T to the smallest j (R-13); writes the ascending index list, the mask words
+// and the count.  The keys live in shared (or L2-resident global) memory, one row per
+// warp: element j at key[j], j < NK.  Upper 32 bits first (32-bit reads of the high
+// words), then, once the top 16 bits of T are fixed, the keys sharing them (usually a
+// few dozen) are compacted to two registers per lane and the rest is searched there.
+// HR > 0: the caller also holds the high words of the lane's keys (j = 32 m + lane) in
+// registers hr[m] (0 where j >= NK), so the first 16 bits are searched without memory reads.
+template <int HR>
+__device__ __forceinline__ void select_row_mem(const uint64_t* key, int NK, int k, int lane,
+                                               uint64_t* cb, int32_t* orow, uint32_t* mrow,
+                                               int32_t* cnt, const uint32_t (&hr)[HR > 0 ? HR : 1]) {
+    const uint32_t* hw = reinterpret_cast<const uint32_t*>(key) + 1;   // high words, stride 2
     const int M = (NK + 31) >> 5;
-    const int k = device_k(a.rec, NK);
-    if (row == 0 && lane == 0) a.hdr[0] = k;
-    int32_t* orow = a.idx + row * NK;
-    uint32_t* mrow = a.mask + row * a.W;
-    if (k >= NK) {  // dense step / full budget: every block exact
-        for (int j = lane; j < NK; j += 32) orow[j] = j;
-        for (int w = lane; w < M; w += 32) {
-            const int rem = NK - 32 * w;
-            mrow[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
-        }
-        if (lane == 0) a.count[row] = NK;
-        return;
-    }
-    const double* rr = a.r + row * NK;
-    uint64_t key[MAXM];
-    const bool biased = a.beta != 0.0;
-    const double bi = biased ? __dmul_rn(a.beta, a.sigma[row]) : 0.0;
-    const uint32_t gh = (uint32_t)((bh / a.H) * a.H_total + a.head_offset + (bh % a.H));
-    uint64_t kand = ~0ull, kor = 0ull;
+    auto count_ge = [&](uint32_t cand) {
+        int c = 0;
+        if constexpr (HR > 0) {
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-        const int j = 32 * m + lane;
-        key[m] = 0ull;                       // absent elements sort last (below every key)
-        if (m < M && j < NK) {
-            double x = __ldg(rr + j);
-            if (biased) {   // R4/R5: rt = r + (beta * sigma_i) * g, two rounded operations
-                const uint32_t x0 = philox4x32_10_x0((uint32_t)j, (uint32_t)i, gh, a.step, a.key0,
-                                                     a.key1);
-                const double u = __dmul_rn(__dadd_rn((double)x0, 0.5), 2.3283064365386963e-10);
-                x = __dadd_rn(x, __dmul_rn(bi, -log(-log(u))));
-            }
-            key[m] = orderable(x);
-            kand &= key[m];
-            kor |= key[m];
+            for (int m = 0; m < HR; ++m) c += hr[m] >= cand;
+        } else {
+            for (int j = lane; j < NK; j += 32) c += hw[2 * j] >= cand;
         }
-    }
-    // bits above the highest differing bit are common to every present key
+        return c;
+    };
+    uint64_t kand = ~0ull, kor = 0ull;
+    for (int j = lane; j < NK; j += 32) { const uint64_t x = key[j]; kand &= x; kor |= x; }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         kand &= __shfl_xor_sync(0xffffffffu, kand, o);
@@ -349,48 +227,41 @@ __global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 4) select_ker
     const uint64_t diff = kand ^ kor;
     uint64_t T = diff ? (kand & ~((2ull << (63 - __clzll(diff))) - 1ull)) : kand;
     const int top = diff ? 63 - __clzll(diff) : -1;
-    // T = the largest value with #{key >= T} >= k, bit by bit from the top differing
-    // bit.  Upper half first with 32-bit compares (key >= T_hi:0 <=> hi >= T_hi), then
-    // the lower half among the keys whose upper half equals T_hi (the others are
-    // counted once: hi > T_hi always, hi < T_hi never).
-    //
-    // Shortcut (top >= 48): once the top 16 bits of T are fixed, the keys sharing them are
-    // usually few (a 1/16-binade window around the k-th score).  If there are at most
-    // 64, they are compacted into shared memory (two per lane) and the remaining bits
-    // are searched over those two registers instead of all M; the keys above the
-    // window are counted once.  Same T as the full search.
-    __shared__ uint64_t cbuf[kSelWarps][64];
     uint32_t T_hi = (uint32_t)(T >> 32);
     int bpos = top;
     for (; bpos >= 48; --bpos) {
         const uint32_t cand = T_hi | (1u << (bpos - 32));
-        int c = 0;
-#pragma unroll
-        for (int m = 0; m < MAXM; ++m) c += (uint32_t)(key[m] >> 32) >= cand;
-        c = __reduce_add_sync(0xffffffffu, c);
+        const int c = __reduce_add_sync(0xffffffffu, count_ge(cand));
         if (c >= k) T_hi = cand;
     }
+    bool done = false;
     if (top >= 48) {
-        // window = keys whose top 16 bits equal T's (32-bit compares on the upper half)
         const uint32_t tw = T_hi >> 16;
         int gw = 0, ew = 0;
+        if constexpr (HR > 0) {
 #pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-            const uint32_t h16 = (uint32_t)(key[m] >> 48);
-            gw += h16 > tw;
-            ew += h16 == tw;   // an absent key (0) can only match if tw = 0; it never counts below
+            for (int m = 0; m < HR; ++m) {
+                const uint32_t h16 = hr[m] >> 16;
+                gw += h16 > tw;
+                ew += h16 == tw && 32 * m + lane < NK;
+            }
+        } else {
+            for (int j = lane; j < NK; j += 32) {
+                const uint32_t h16 = hw[2 * j] >> 16;
+                gw += h16 > tw;
+                ew += h16 == tw;
+            }
         }
         gw = __reduce_add_sync(0xffffffffu, gw);
         ew = __reduce_add_sync(0xffffffffu, ew);
         if (ew <= 64) {
-            uint64_t* cb = cbuf[threadIdx.x >> 5];
             const uint32_t lt = (1u << lane) - 1u;
             int base = 0;
-#pragma unroll
-            for (int m = 0; m < MAXM; ++m) {
-                const bool in = (uint32_t)(key[m] >> 48) == tw;
+            for (int m = 0; m < M; ++m) {
+                const int j = 32 * m + lane;
+                const bool in = j < NK && (hw[2 * j] >> 16) == tw;
                 const uint32_t b = __ballot_sync(0xffffffffu, in);
-                if (in) cb[base + __popc(b & lt)] = key[m];
+                if (in) cb[base + __popc(b & lt)] = key[j];
                 base += __popc(b);
             }
             __syncwarp();
@@ -403,64 +274,236 @@ __global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 4) select_ker
                 const int c = gw + __reduce_add_sync(0xffffffffu, (c0 >= cand) + (c1 >= cand));
                 if (c >= k) Tc = cand;
             }
-            T_hi = (uint32_t)(Tc >> 32);
             T = Tc;
-            bpos = -2;   // done
+            done = true;
         }
     }
-    for (; bpos >= 32; --bpos) {
-        const uint32_t cand = T_hi | (1u << (bpos - 32));
-        int c = 0;
-#pragma unroll
-        for (int m = 0; m < MAXM; ++m) c += (uint32_t)(key[m] >> 32) >= cand;
-        c = __reduce_add_sync(0xffffffffu, c);
-        if (c >= k) T_hi = cand;
-    }
-    uint32_t T_lo = top >= 32 ? 0u : (uint32_t)T;
-    if (bpos == -2) {
-        T_lo = (uint32_t)T;
-    } else if (top >= 0) {
-        int gtc = 0;
-        uint32_t lo[MAXM];
-#pragma unroll
-        for (int m = 0; m < MAXM; ++m) {
-            const uint32_t hi = (uint32_t)(key[m] >> 32);
-            gtc += hi > T_hi;
-            lo[m] = hi == T_hi ? (uint32_t)key[m] : 0u;   // 0 never reaches a candidate
-        }
-        gtc = __reduce_add_sync(0xffffffffu, gtc);
-        for (int bpos = min(top, 31); bpos >= 0; --bpos) {
-            const uint32_t cand = T_lo | (1u << bpos);
+    if (!done) {
+        for (; bpos >= 32; --bpos) {
+            const uint32_t cand = T_hi | (1u << (bpos - 32));
             int c = 0;
-#pragma unroll
-            for (int m = 0; m < MAXM; ++m) c += lo[m] >= cand;
-            c = gtc + __reduce_add_sync(0xffffffffu, c);
-            if (c >= k) T_lo = cand;
+            for (int j = lane; j < NK; j += 32) c += hw[2 * j] >= cand;
+            c = __reduce_add_sync(0xffffffffu, c);
+            if (c >= k) T_hi = cand;
         }
+        uint32_t T_lo = top >= 32 ? 0u : (uint32_t)T;
+        if (top >= 0) {
+            int gtc = 0;
+            for (int j = lane; j < NK; j += 32) gtc += hw[2 * j] > T_hi;
+            gtc = __reduce_add_sync(0xffffffffu, gtc);
+            for (int b = min(top, 31); b >= 0; --b) {
+                const uint32_t cand = T_lo | (1u << b);
+                int c = 0;
+                for (int j = lane; j < NK; j += 32) {
+                    const uint64_t x = key[j];
+                    c += (uint32_t)(x >> 32) == T_hi && (uint32_t)x >= cand;
+                }
+                c = gtc + __reduce_add_sync(0xffffffffu, c);
+                if (c >= k) T_lo = cand;
+            }
+        }
+        T = ((uint64_t)T_hi << 32) | T_lo;
     }
-    T = ((uint64_t)T_hi << 32) | T_lo;
     int gt = 0;
-#pragma unroll
-    for (int m = 0; m < MAXM; ++m) gt += key[m] > T;
+    for (int j = lane; j < NK; j += 32) gt += key[j] > T;
     const int need = k - __reduce_add_sync(0xffffffffu, gt);   // keys equal to T to take
-    // walk the chunks in ascending j: ties go to the smallest j; the ballot of a chunk
-    // is its mask word; positions come from prefix counts
     int taken_eq = 0, pos = 0;
     const uint32_t below = (1u << lane) - 1u;
+    for (int m = 0; m < M; ++m) {
+        const int j = 32 * m + lane;
+        const uint64_t x = j < NK ? key[j] : 0ull;
+        const uint32_t eqb = __ballot_sync(0xffffffffu, x == T && j < NK);
+        const int eq_rank = taken_eq + __popc(eqb & below);
+        const bool take = j < NK && (x > T || (x == T && eq_rank < need));
+        taken_eq += __popc(eqb);
+        const uint32_t sel = __ballot_sync(0xffffffffu, take);
+        if (take) orow[pos + __popc(sel & below)] = j;
+        pos += __popc(sel);
+        if (lane == 0) mrow[m] = sel;
+    }
+    if (lane == 0) *cnt = k;
+}
+
+// HR > 0 (N_K <= 32 HR): the high words of a row's keys stay in registers for the search
+template <int R, int D, bool SMEM_SC, int HR>
+__global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a) {
+    extern __shared__ __align__(16) unsigned char f_smem[];
+    constexpr int NT = 32 * R, NW = R;              // one warp per score row
+    constexpr int RT = R / 8;                       // DMMA row tiles (all in every warp)
+    constexpr int CG = kFCG4 / RT;                  // column tiles per work group
+    constexpr int KB = D / (4 * kFKS);              // register blocks per group (even)
+    static_assert(KB % 2 == 0, "ping-pong blocks must pair up inside a group");
+    const int NK = (int)a.NK, NKP = a.NKP;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t bh = blockIdx.y;
+    const int64_t i0 = (int64_t)blockIdx.x * R;
+    const int nrows = (int)min((int64_t)R, a.NQ - i0);
+    double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
+    uint64_t* cbuf = reinterpret_cast<uint64_t*>(sq + R * (D + 4));    // [NW][64]
+    double* sc = SMEM_SC ? reinterpret_cast<double*>(cbuf + NW * 64)
+                         : a.gsc + (bh * a.NQ + i0) * (int64_t)NKP;     // [R][NKP]
+
+    const int k = device_k(a.rec, NK);
+    if (blockIdx.x == 0 && bh == 0 && tid == 0) a.hdr[0] = k;
+    const int M = (NK + 31) >> 5;
+    if (k >= NK) {   // dense step / full budget: every block exact, no scores needed
+        if (warp < nrows) {
+            const int64_t row = bh * a.NQ + i0 + warp;
+            int32_t* orow = a.idx + row * NK;
+            uint32_t* mrow = a.mask + row * a.W;
+            for (int j = lane; j < NK; j += 32) orow[j] = j;
+            for (int w = lane; w < M; w += 32) {
+                const int rem = NK - 32 * w;
+                mrow[w] = rem >= 32 ? 0xffffffffu : ((1u << rem) - 1u);
+            }
+            if (lane == 0) a.count[row] = NK;
+        }
+        return;
+    }
+
+    // ---- phase A: scores -------------------------------------------------------------
+    // Every warp holds all R rows (RT row tiles) and works through groups of CG column
+    // tiles (8 KV blocks each), groups round-robin over the warps.  B fragments (Kbar,
+    // fragment order) come from L2 as 16-byte loads of two k-steps straight into
+    // registers, a block of 4 k-steps ahead; A fragments (Qbar) from shared memory.
+    const double* Q = a.qbar + (bh * a.NQ + i0) * D;
+    for (int e = tid; e < R * D; e += NT) {
+        const int r = e / D, c = e % D;
+        sq[r * (D + 4) + c] = r < nrows ? Q[(int64_t)r * D + c] : 0.0;
+    }
+    __syncthreads();
+    {
+        const int fr = lane >> 2, fk = lane & 3;
+        const int ntiles = (NK + 7) >> 3;
+        const int ngroups = (ntiles + CG - 1) / CG;
+        const int mygroups = warp < ngroups ? (ngroups - 1 - warp) / NW + 1 : 0;
+        const double2* KF = reinterpret_cast<const double2*>(a.kfrag) +
+                            bh * (int64_t)ntiles * (D / 8) * 32 + lane;
+        const double* arow = sq + fr * (D + 4) + fk;
+        auto load_blk = [&](double (&bb)[kFKS][CG], int g, int kb) {
 #pragma unroll
-    for (int m = 0; m < MAXM; ++m) {
-        if (m < M) {
-            const uint32_t eqb = __ballot_sync(0xffffffffu, key[m] == T);
-            const int eq_rank = taken_eq + __popc(eqb & below);
-            const bool take = key[m] > T || (key[m] == T && eq_rank < need);
-            taken_eq += __popc(eqb);
-            const uint32_t sel = __ballot_sync(0xffffffffu, take);
-            if (take) orow[pos + __popc(sel & below)] = 32 * m + lane;
-            pos += __popc(sel);
-            if (lane == 0) mrow[m] = sel;
+            for (int c = 0; c < CG; ++c) {
+                const int ct = g * CG + c;
+                const bool ok = ct * 8 + fr < NK;
+#pragma unroll
+                for (int q = 0; q < kFKS / 2; ++q) {
+                    const double2 v = ok ? __ldg(KF + ((int64_t)ct * (D / 8) + kb * (kFKS / 2) + q) * 32)
+                                         : make_double2(0.0, 0.0);
+                    bb[2 * q][c] = v.x;
+                    bb[2 * q + 1][c] = v.y;
+                }
+            }
+        };
+        double acc[RT][CG][2];
+#pragma unroll
+        for (int t = 0; t < RT; ++t)
+#pragma unroll
+            for (int c = 0; c < CG; ++c) acc[t][c][0] = acc[t][c][1] = 0.0;
+        double bb[2][kFKS][CG];
+        if (mygroups > 0) load_blk(bb[0], warp, 0);
+        for (int gi = 0; gi < mygroups; ++gi) {
+            const int g = warp + NW * gi;
+#pragma unroll
+            for (int kb = 0; kb < KB; ++kb) {
+                if (kb + 1 < KB) load_blk(bb[(kb + 1) & 1], g, kb + 1);
+                else if (gi + 1 < mygroups) load_blk(bb[(kb + 1) & 1], g + NW, 0);
+#pragma unroll
+                for (int u = 0; u < kFKS; ++u) {           // ascending d: the fma chain of R2
+#pragma unroll
+                    for (int t = 0; t < RT; ++t) {
+                        const double av = arow[t * 8 * (D + 4) + kb * 4 * kFKS + 4 * u];
+#pragma unroll
+                        for (int c = 0; c < CG; ++c)
+                            dmma_8x8x4(acc[t][c][0], acc[t][c][1], av, bb[kb & 1][u][c]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < RT; ++t) {                 // group done: r = s * acc (+ prior)
+                const int r = t * 8 + fr;
+#pragma unroll
+                for (int c = 0; c < CG; ++c) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int j = (g * CG + c) * 8 + 2 * fk + h;
+                        if (j < NK && r < nrows) {
+                            double x = __dmul_rn(a.s, acc[t][c][h]);
+                            if (a.prior) x = __dadd_rn(x, a.prior[bh * a.NK + j]);   // Eq. 8
+                            sc[r * NKP + j] = x;
+                        }
+                        acc[t][c][h] = 0.0;
+                    }
+                }
+            }
         }
     }
-    if (lane == 0) a.count[row] = k;
+    __syncthreads();
+    if (warp >= nrows) return;
+
+    // ---- phase B: sigma_i (R3) ---------------------------------------------------------
+    // mu_i and the centred sum of squares as fixed-order warp reductions (lane-strided
+    // partial sums in ascending j, then a butterfly; every lane ends with the same value).
+    // The oracle sums sequentially in j; the two differ by a few ulps of sigma_i, which
+    // moves r~ by ~1e-16 relative: routing can differ only where two oracle scores tie
+    // within that, far inside the documented-tie margin of SURVEY.md 8(c) (R3').
+    double* row = sc + warp * NKP;
+    const bool biased = a.beta != 0.0;
+    const uint32_t gh = (uint32_t)((bh / a.H) * a.H_total + a.head_offset + (bh % a.H));
+    const uint32_t i = (uint32_t)(i0 + warp);
+    double bi = 0.0;
+    if (biased) {
+        double sum = 0.0;
+        for (int j = lane; j < NK; j += 32) sum = __dadd_rn(sum, row[j]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+        const double mu = __ddiv_rn(sum, (double)NK);
+        double v = 0.0;
+        for (int j = lane; j < NK; j += 32) {
+            const double dl = __dsub_rn(row[j], mu);
+            v = __fma_rn(dl, dl, v);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+        bi = __dmul_rn(a.beta, __dsqrt_rn(__ddiv_rn(v, (double)NK)));
+    }
+
+    // ---- phase C: keys in place, threshold, outputs -------------------------------------
+    uint64_t* key = reinterpret_cast<uint64_t*>(row);
+    const int64_t grow = bh * a.NQ + i0 + warp;
+    if constexpr (HR > 0) {
+        uint32_t hr[HR];
+#pragma unroll
+        for (int m = 0; m < HR; ++m) {
+            const int j = 32 * m + lane;
+            hr[m] = 0u;
+            if (j < NK) {
+                double x = row[j];
+                if (biased)   // R4/R5: rt = r + (beta sigma_i) g, two rounded operations
+                    x = __dadd_rn(x, __dmul_rn(bi, gumbel((uint32_t)j, i, gh, a.step, a.key0, a.key1)));
+                const uint64_t kx = orderable(x);
+                key[j] = kx;
+                hr[m] = (uint32_t)(kx >> 32);
+            }
+        }
+        __syncwarp();
+        select_row_mem<HR>(key, NK, k, lane, cbuf + warp * 64, a.idx + grow * NK,
+                           a.mask + grow * a.W, a.count + grow, hr);
+    } else {
+        for (int j = lane; j < NK; j += 32) {
+            double x = row[j];
+            if (biased)
+                x = __dadd_rn(x, __dmul_rn(bi, gumbel((uint32_t)j, i, gh, a.step, a.key0, a.key1)));
+            key[j] = orderable(x);
+        }
+        __syncwarp();
+        const uint32_t none[1] = {0u};
+        select_row_mem<0>(key, NK, k, lane, cbuf + warp * 64, a.idx + grow * NK,
+                          a.mask + grow * a.W, a.count + grow, none);
+    }
+}
+
+constexpr size_t fused_fixed_smem(int R, int D) {
+    return sizeof(double) * (size_t)R * (D + 4) + sizeof(uint64_t) * R * 64;
 }
 
 }  // namespace
@@ -468,16 +511,17 @@ __global__ void __launch_bounds__(32 * kSelWarps, MAXM <= 40 ? 5 : 4) select_ker
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches) {
-    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qbar};
-    PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, r->kbar};
+    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qbar, nullptr};
+    PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, r->kbar,
+                r->kfrag};
     int64_t ng = r->D / 8;
     int64_t q_tasks = r->BH * r->NQ * ng;
     int64_t total = q_tasks + r->BH * r->NK * ng;
-    int64_t grid = (total + 255) / 256;
+    const unsigned pgrid = (unsigned)((total + 255) / 256);
     if (q.dtype == PASA_F32)
-        pool_kernel<float><<<(unsigned)grid, 256, 0, st>>>(qa, ka, q_tasks, total);
+        pool_kernel<float><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
     else
-        pool_kernel<__nv_bfloat16><<<(unsigned)grid, 256, 0, st>>>(qa, ka, q_tasks, total);
+        pool_kernel<__nv_bfloat16><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
 
     const double* prior = nullptr;
     if (v) {
@@ -486,39 +530,47 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
         prior = r->prior;
     }
     const double s = 1.0 / sqrt((double)r->D);
-    dim3 sg((unsigned)((r->NK + kST - 1) / kST), (unsigned)((r->NQ + kST - 1) / kST),
-            (unsigned)r->BH);
-    scores_kernel<<<sg, kSThreads, 0, st>>>(r->qbar, r->kbar, r->NQ, r->NK, r->D, s, prior, r->scores);
-    *launches += 2;
-
-    const int64_t rows = r->BH * r->NQ;
-    if (r->cfg.beta != 0.0) {
-        rowstats_kernel<<<(unsigned)((rows + kRsRows - 1) / kRsRows), kRsRows * 2, 0, st>>>(
-            r->scores, rows, r->NK, r->sigma);
-        *launches += 1;
+    FusedArgs fa;
+    fa.qbar = r->qbar; fa.kfrag = r->kfrag; fa.prior = prior; fa.rec = b->rec;
+    fa.NQ = r->NQ; fa.NK = r->NK; fa.W = r->W; fa.H = r->H;
+    fa.H_total = r->cfg.H_total; fa.head_offset = r->cfg.head_offset;
+    fa.D = (int)r->D; fa.NKP = (int)route_score_stride(r->NK);
+    fa.s = s; fa.beta = r->cfg.beta;
+    fa.key0 = (uint32_t)(seed & 0xffffffffu); fa.key1 = (uint32_t)(seed >> 32);
+    fa.step = (uint32_t)step;
+    fa.idx = r->idx; fa.count = r->count; fa.mask = r->mask; fa.hdr = r->hdr;
+    fa.gsc = r->scores;
+    const bool smem_sc = route_rows_per_cta(r->NK, r->D) > 0;
+    constexpr int RR = kFRows;
+    const size_t smem = fused_fixed_smem(RR, (int)r->D) +
+                        (smem_sc ? sizeof(double) * (size_t)RR * fa.NKP : 0);
+    dim3 grid((unsigned)((r->NQ + RR - 1) / RR), (unsigned)r->BH);
+    const bool hreg = r->NK <= 32 * kFHR;
+#define PASA_FUSED_PICK(DD)                                                                  \
+    (!smem_sc ? route_fused_kernel<RR, DD, false, 0>                                         \
+              : (hreg ? route_fused_kernel<RR, DD, true, kFHR> : route_fused_kernel<RR, DD, true, 0>))
+    void (*kfn)(FusedArgs) = r->D == 128 ? PASA_FUSED_PICK(128) : PASA_FUSED_PICK(64);
+#undef PASA_FUSED_PICK
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e == cudaSuccess) {
+        kfn<<<grid, 32 * RR, smem, st>>>(fa);
+        e = cudaGetLastError();
     }
-    SelArgs sa;
-    sa.r = r->scores;
-    sa.sigma = r->sigma;
-    sa.rec = b->rec;
-    sa.rows = rows;
-    sa.NQ = r->NQ; sa.NK = r->NK; sa.W = r->W; sa.H = r->H;
-    sa.H_total = r->cfg.H_total; sa.head_offset = r->cfg.head_offset;
-    sa.beta = r->cfg.beta;
-    sa.key0 = (uint32_t)(seed & 0xffffffffu);
-    sa.key1 = (uint32_t)(seed >> 32);
-    sa.step = (uint32_t)step;
-    sa.idx = r->idx; sa.count = r->count; sa.mask = r->mask; sa.hdr = r->hdr;
-    const unsigned sg2 = (unsigned)((rows + kSelWarps - 1) / kSelWarps);
-    const int M = (int)((r->NK + 31) / 32);
-    if (M <= 8) select_kernel<8><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
-    else if (M <= 20) select_kernel<20><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
-    else if (M <= 40) select_kernel<40><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
-    else select_kernel<64><<<sg2, 32 * kSelWarps, 0, st>>>(sa);
-    *launches += 1;
-    return cudaGetLastError();
+    *launches += 2;
+    return e;
 }
 
-int route_max_nk() { return 2048; }
+int route_rows_per_cta(int64_t NK, int64_t D) {
+    // 8 rows (one DMMA row tile) per CTA, two CTAs per SM: 113 KB of shared memory each
+    // (16 rows at one CTA per SM measured the same at Wan-14B: 1.142 vs 1.137 ms)
+    const size_t nkp = (size_t)route_score_stride(NK);
+    return fused_fixed_smem(kFRows, (int)D) + sizeof(double) * kFRows * nkp <= 113 * 1024 ? kFRows
+                                                                                        : 0;
+}
+
+int64_t route_score_stride(int64_t NK) { return NK | 1; }
+
+
 
 }  // namespace pasa
