@@ -65,6 +65,13 @@ def parse(argv=None):
                          "the north-star path)")
     ap.add_argument("--cpu-qblocks", type=int, default=256,
                     help="oracle sample size (q-blocks of one head; ~10 s of CPU work)")
+    ap.add_argument("--partition", default="auto", choices=["auto", "heads", "flat"],
+                    help="work split over ranks: contiguous heads, or the flattened (head, "
+                         "q-block) list (SURVEY.md §8e; auto: flat when the heads do not divide "
+                         "the rank count, e.g. Wan-1.3B's 12 heads over 8 GPUs)")
+    ap.add_argument("--ulysses-chunks", type=int, default=0,
+                    help="head groups of the sequence-sharded Ulysses all-to-all (attention on "
+                         "arrived heads overlaps the rest; 0 = auto, up to 4)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1.  gloo is a debug mode: ranks may "
                          "share one GPU (device = local_rank %% device_count) and every "
@@ -286,12 +293,25 @@ def run_pasa(args):
     from paper_2604_12219_b200 import dist as pdist
     seq_sharded = (args.seq_sharded == "yes"
                    or (args.seq_sharded == "auto" and args.config == "hunyuan_720p"))
-    # contiguous head partition (uneven allowed, e.g. 12 heads over 8 ranks); the
-    # Ulysses all-to-all of sequence-sharded input needs equal head chunks
+    NQ = -(-S // cfg["Bq"])
+    partition = args.partition
+    if partition == "auto":
+        partition = "flat" if (not seq_sharded and H % world) else "heads"
+    if seq_sharded and partition == "flat":
+        raise SystemExit("the Ulysses path splits whole heads (--partition heads)")
+    # contiguous head partition (uneven allowed, e.g. 12 heads over 8 ranks) or the
+    # flattened (head, q-block) split; the Ulysses all-to-all needs equal head chunks
     try:
-        off, Hl = pdist.head_range(H, world, rank, even=seq_sharded)
+        if partition == "flat":
+            segs = pdist.flat_partition(H, NQ, world, rank)
+            off, Hl = pdist.partition_heads(segs)     # the heads whose K/V this rank reads
+        else:
+            off, Hl = pdist.head_range(H, world, rank, even=seq_sharded)
+            segs = [(off, Hl, 0, 0)]
     except ValueError as exc:
         raise SystemExit(str(exc))
+    # head-equivalents of attention work on this rank ((head, q-block) items / N_Q)
+    work_heads = sum(n * ((b - a) if (a, b) != (0, 0) else NQ) for _, n, a, b in segs) / NQ
     dev = torch.device("cuda", torch.cuda.current_device())
     cdev = torch.device("cpu") if gloo else dev      # where collective buffers live
 
@@ -310,11 +330,11 @@ def run_pasa(args):
         dist.all_reduce(tt, op=dist.ReduceOp.SUM)
         return tt.cpu().tolist()
 
-    heads_all = [Hl]
+    heads_all = [work_heads]
     if world > 1:
         heads_all = [None] * world
-        dist.all_gather_object(heads_all, Hl)
-        assert sum(heads_all) == H, heads_all
+        dist.all_gather_object(heads_all, work_heads)
+        assert abs(sum(heads_all) - H) < 1e-9, heads_all
     if seq_sharded and S % world:
         raise SystemExit(f"S = {S} does not split over {world} ranks")
     # every global head drawn from its own seed: the same data for any N
@@ -328,56 +348,109 @@ def run_pasa(args):
     q = torch.cat(qs, 2).contiguous(); k = torch.cat(ks, 2).contiguous()
     v = torch.cat(vs, 2).contiguous()
     del qs, ks, vs
-    if seq_sharded:
-        # sequence-sharded input [B, S/P, H, D]: the step starts with the Ulysses
-        # all-to-all to this rank's heads and ends with the inverse
-        q_s, k_s, v_s = q, k, v
-        if world == 1:
-            to_heads = to_seq = (lambda t: t)
-        elif gloo:   # debug mode: the all-to-all through host memory
-            to_heads = lambda t: pdist.seq_to_head(t.cpu()).to(dev)  # noqa: E731
-            to_seq = lambda t: pdist.head_to_seq(t.cpu()).to(dev)    # noqa: E731
-        else:
-            to_heads = lambda t: pdist.seq_to_head(t)  # noqa: E731
-            to_seq = lambda t: pdist.head_to_seq(t)    # noqa: E731
-        q, k, v = (to_heads(t) for t in (q_s, k_s, v_s))
     out = torch.empty_like(q)
     tp = synth.ThreePhase(shape=cfg["latent"], T=50, seed=7, device=dev)
     t_step = args.step_t
     x_t, x_tm1, x_tm2 = (x.contiguous() for x in tp.latents(t_step))
     lbar = tp.expected_l1_mean()
-    rcfg = P.RouteCfg(Bq=cfg["Bq"], Bk=cfg["Bk"], G=cfg["G"], comp="grouped", beta=0.1,
-                      H_total=H, head_offset=off, prior=args.prior)
     use_v = args.prior != "none"
     budget = P.Budget(dev)
-    route = P.Route(B, S, Hl, D, rcfg, dev)
     seed = P.layer_seed(42, 0)
     stream = torch.cuda.current_stream()
     launches = [0]
-
     table = [cfg["rho"]] * 50 if args.budget == "table" else None
+    bkw = dict(T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar, h_t=1 / 50, h_tm1=1 / 50,
+               rho_table=table)
+
+    def rcfg_for(h, a=0, b=0):
+        return P.RouteCfg(Bq=cfg["Bq"], Bk=cfg["Bk"], G=cfg["G"], comp="grouped", beta=0.1,
+                          H_total=H, head_offset=h, prior=args.prior, qb_begin=a, qb_end=b)
+
+    rcfg = rcfg_for(off)
+    if seq_sharded:
+        # sequence-sharded input [B, S/P, H, D] and latents: the step is the sharded budget
+        # (one fp64 partial per rank, all_gather) and the chunked Ulysses all-to-all with
+        # PASA per head chunk
+        q_s, k_s, v_s = q, k, v
+        out_s = torch.empty_like(q_s)
+        n_lat = x_t.numel()
+        la = (rank * n_lat // world) // 4 * 4
+        lb = n_lat if rank == world - 1 else ((rank + 1) * n_lat // world) // 4 * 4
+        xs_sh = [x.reshape(-1)[la:lb] for x in (x_t, x_tm1, x_tm2)]
+        n_chunks_u = args.ulysses_chunks or max(c for c in (1, 2, 3, 4) if (H // world) % c == 0)
+        uly = pdist.Ulysses(B, S, H, D, q.dtype, dev, chunks=n_chunks_u)
+        chunk_routes = {}
+        chunk_ev = []   # per chunk: [before route, after route, after stats, after attn]
+
+        def compute(c, qh, kh, vh, oh, hoff):
+            r = chunk_routes.get(c)
+            if r is None:
+                r = chunk_routes[c] = P.Route(B, S, qh.shape[2], D, rcfg_for(hoff), dev)
+            evs = chunk_ev[-1][c] if chunk_ev and chunk_ev[-1] is not None else None
+            if evs:
+                evs[0].record(stream)
+            r(qh, kh, budget, seed, t_step, v=vh if use_v else None)
+            launches[0] += P.last_launch_count()
+            if evs:
+                evs[1].record(stream)
+            P.attn(qh, kh, vh, r, oh, stats_only=True)
+            launches[0] += P.last_launch_count()
+            if evs:
+                evs[2].record(stream)
+            P.attn(qh, kh, vh, r, oh, reuse_stats=True)
+            launches[0] += P.last_launch_count()
+            if evs:
+                evs[3].record(stream)
+        # the first call builds the chunk handles (outside any timed region)
+        chunk_ev.append(None)
+        uly(q_s, k_s, v_s, out_s, compute)
+        route = chunk_routes[0]
+        # this rank's head-sharded tensors (dense-attention context): chunk 0 as received
+        q, k, v = ((q_s, k_s, v_s) if world == 1 else
+                   tuple(uly._heads(uly.recv[n][0]) for n in "qkv"))
+    else:
+        units = []
+        for h, n, a, b in segs:
+            sl = slice(h - off, h - off + n)
+            units.append((P.Route(B, S, n, D, rcfg_for(h, a, b), dev),
+                          q[:, :, sl], k[:, :, sl], v[:, :, sl], out[:, :, sl]))
+        route = units[0][0]
+
+    def do_budget():
+        if seq_sharded:
+            pdist.sharded_budget(budget, *xs_sh, n_total=x_t.numel(), **bkw)
+        else:
+            budget(x_t, x_tm1, x_tm2, **bkw)
+        launches[0] += P.last_launch_count()
 
     def step(ev=None):
-        nonlocal q, k, v
-        budget(x_t, x_tm1, x_tm2, T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
-               h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
-        launches[0] += P.last_launch_count()
-        if seq_sharded:
-            q, k, v = (to_heads(t) for t in (q_s, k_s, v_s))
+        do_budget()
         if ev is not None:
             ev[0].record(stream)
-        route(q, k, budget, seed, t_step, v=v if use_v else None)
-        launches[0] += P.last_launch_count()
+        if seq_sharded:
+            if ev is not None:
+                chunk_ev.append([[torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                                 for _ in range(uly.C)])
+            else:
+                chunk_ev.append(None)
+            uly(q_s, k_s, v_s, out_s, compute)
+            if ev is not None:
+                for j in (1, 2, 3):
+                    ev[j].record(stream)
+            return
+        for r, qu, ku, vu, ou in units:
+            r(qu, ku, budget, seed, t_step, v=vu if use_v else None)
+            launches[0] += P.last_launch_count()
         if ev is not None:
             ev[1].record(stream)
-        P.attn(q, k, v, route, out, stats_only=True)
-        launches[0] += P.last_launch_count()
+        for r, qu, ku, vu, ou in units:
+            P.attn(qu, ku, vu, r, ou, stats_only=True)
+            launches[0] += P.last_launch_count()
         if ev is not None:
             ev[2].record(stream)
-        P.attn(q, k, v, route, out, reuse_stats=True)
-        launches[0] += P.last_launch_count()
-        if seq_sharded:
-            to_seq(out)
+        for r, qu, ku, vu, ou in units:
+            P.attn(qu, ku, vu, r, ou, reuse_stats=True)
+            launches[0] += P.last_launch_count()
         if ev is not None:
             ev[3].record(stream)
 
@@ -413,8 +486,13 @@ def run_pasa(args):
     for it in range(K):
         prev = e_start if it == 0 else evs[it - 1][3]
         ph[0] += prev.elapsed_time(evs[it][0])
-        for j in range(1, 4):
-            ph[j] += evs[it][j - 1].elapsed_time(evs[it][j])
+        if seq_sharded:   # route / stats / attention summed over the Ulysses chunks
+            for ce in chunk_ev[-K + it]:
+                for j in range(1, 4):
+                    ph[j] += ce[j - 1].elapsed_time(ce[j])
+        else:
+            for j in range(1, 4):
+                ph[j] += evs[it][j - 1].elapsed_time(evs[it][j])
         per_step.append(prev.elapsed_time(evs[it][3]))
     ph /= K
     step_p50, step_p90 = (float(np.percentile(per_step, q)) for q in (50, 90))
@@ -508,19 +586,38 @@ def run_pasa(args):
         # the GPU and hide the per-chunk launches; Wan-14B 20, CogVideoX / Wan-1.3B 12)
         n_chunks = args.e2e_chunks or max(4, min(20, round(t_max / 0.12)))
         if seq_sharded and world > 1:
-            # host shards -> device -> all-to-all -> PASA -> all-to-all -> host shard
+            # host shards -> device -> sharded budget -> chunked Ulysses + PASA -> host shard
             dsq, dsk, dsv = (torch.empty_like(t) for t in src)
-            dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
+            dx = [torch.empty_like(x) for x in xs_sh]
+            hx = [x.cpu().pin_memory() for x in xs_sh]
+            h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
+            dout = torch.empty_like(out_s)
 
             def e2e_step():
                 for d, hsrc in zip((dsq, dsk, dsv, *dx), (hq, hk, hv, *hx)):
                     d.copy_(hsrc, non_blocking=True)
-                budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
-                       h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
-                qh, kh, vh = (to_heads(t) for t in (dsq, dsk, dsv))
-                route(qh, kh, budget, seed, t_step, v=vh if use_v else None)
-                P.attn(qh, kh, vh, route, out)
-                hout.copy_(to_seq(out), non_blocking=True)
+                pdist.sharded_budget(budget, *dx, n_total=x_t.numel(), **bkw)
+                chunk_ev.append(None)
+                uly(dsq, dsk, dsv, dout, compute)
+                hout.copy_(dout, non_blocking=True)
+        elif partition == "flat":
+            # the rank's heads to the device, its (head, q-block) segments, its rows back
+            dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            dx = [torch.empty_like(x) for x in (x_t, x_tm1, x_tm2)]
+            dout = torch.empty_like(out)
+            dunits = []
+            for (r, *_), (h, n, a, b) in zip(units, segs):
+                sl = slice(h - off, h - off + n)
+                dunits.append((r, dq[:, :, sl], dk[:, :, sl], dv[:, :, sl], dout[:, :, sl]))
+
+            def e2e_step():
+                for d, hsrc in zip((dq, dk, dv, *dx), (hq, hk, hv, *hx)):
+                    d.copy_(hsrc, non_blocking=True)
+                budget(dx[0], dx[1], dx[2], **bkw)
+                for r, qu, ku, vu, ou in dunits:
+                    r(qu, ku, budget, seed, t_step, v=vu if use_v else None)
+                    P.attn(qu, ku, vu, r, ou)
+                hout.copy_(dout, non_blocking=True)
         elif n_chunks > 1:
             # public API for host-resident tensors: head chunks on copy-in / compute /
             # copy-out streams (paper_2604_12219_b200.pipeline)
@@ -584,7 +681,7 @@ def run_pasa(args):
     pk, which = peaks()
     NK, NG = route.NK, route.NG
     flops_head = algorithmic_flops_per_head(S, D, NK, NG, kk)
-    attn_flops = flops_head * B * Hl           # per launch, this rank
+    attn_flops = flops_head * B * work_heads   # per step, this rank (all its launches)
     t_attn = float(ph[3])
     achieved = attn_flops / (t_attn * 1e-3) / 1e12
     peak = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
@@ -592,7 +689,7 @@ def run_pasa(args):
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
             tr = json.load(f)
-            if tr.get("config") == args.config and tr.get("heads") == Hl:
+            if tr.get("config") == args.config and tr.get("heads") == work_heads:
                 traffic = tr.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
@@ -602,7 +699,7 @@ def run_pasa(args):
     # being every 64-block chunk with a dropped block -- all of them at these densities)
     clocks = clk.summary()
     n_c = 0 if kk >= NK else (NK + 63) // 64
-    n_exp = B * Hl * route.NQ * (kk + n_c) * 128 * 64
+    n_exp = int(B * work_heads * route.NQ * (kk + n_c) * 128 * 64)
     f_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
     mufu = {"bound": "mufu", "achieved": n_exp / (t_attn * 1e-3) / 1e12,
             "peak": 16 * 148 * f_hz / 1e12, "unit": "Tex2/s",
@@ -621,8 +718,10 @@ def run_pasa(args):
         "ms_per_step_p90": step_p90, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
         "config": {
-            "workload": args.config, "B": B, "S": S, "H": H, "D": D, "heads_per_rank": Hl,
-            "nranks": world, "heads_per_rank_all": heads_all,
+            "workload": args.config, "B": B, "S": S, "H": H, "D": D,
+            "heads_per_rank": work_heads, "nranks": world, "heads_per_rank_all": heads_all,
+            "partition": partition, "segments": segs if partition == "flat" else None,
+            "ulysses_chunks": uly.C if seq_sharded else None,
             "dist_backend": (args.dist_backend + (" (debug: ranks share GPUs, timings not "
                                                   "meaningful)" if gloo else "")) if world > 1
             else None,
@@ -631,12 +730,14 @@ def run_pasa(args):
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
-            "parallelism": (f"sequence-sharded input, Ulysses all-to-all x{world} "
-                            "(ms_layer.budget includes the all-to-all of q, k, v)")
-                           if seq_sharded else f"head-partition x{world}",
+            "parallelism": (f"sequence-sharded input and latents, chunked Ulysses all-to-all "
+                            f"x{world} (ms_layer route/kv_stats/attn summed over the chunks)")
+                           if seq_sharded else
+                           (f"(head, q-block) partition x{world}" if partition == "flat"
+                            else f"head-partition x{world}"),
         },
         "ms_layer": {"budget": float(ph[0]), "route": float(ph[1]), "kv_stats": float(ph[2]),
-                     "attn": float(ph[3])},
+                     "attn": float(ph[3]), "other": float(t_max - ph.sum())},
         "tflops_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12,
         "pct_of_peak_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12 / peak,
         "roofline": {"kernel": "attn_sm100_kernel", "bound": "tensor", "achieved": achieved,

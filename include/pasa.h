@@ -103,6 +103,12 @@ typedef struct {
     int32_t prior;           /* pasa_prior (PASA_PRIOR_NONE = the north star's route)          */
     int32_t _pad;
     double eps;              /* epsilon of the prior's log (1e-6); > 0 if prior on */
+    int32_t qb_begin;        /* this handle routes and attends query blocks [qb_begin, qb_end)  */
+    int32_t qb_end;          /* of every head only; (0, 0) = all N_Q.  The flattened (head,
+                              * q-block) partition of SURVEY.md §8e for head counts that do not
+                              * divide the GPU count: K/V statistics still cover whole heads,
+                              * Philox keys on the global block index i, and rows outside the
+                              * range of idx / count / mask / out are not written.            */
 } pasa_route_cfg;
 
 typedef struct pasa_budget_s* pasa_budget_h;
@@ -144,6 +150,23 @@ void pasa_route_fini(pasa_route_h h);
  *   EDEGENERATE (l1_mean <= 0). */
 pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
                         const pasa_schedule* schedule, pasa_budget_h budget, void* stream);
+
+/* Sharded latents ("all_gather of one fp64 partial per rank, summed
+ * in rank order"), for callers whose latents are split across ranks (sequence-
+ * sharded DiT inference).  Two steps around the caller's all_gather:
+ *   pasa_budget_local_sum: dev_sum[0] (DEVICE fp64) = sum over THIS rank's elements of
+ *     |dv| (the numerator of pasa_budget's l; same element formula, fixed-order tree);
+ *   pasa_budget_from_sums: l = (sums[0] + sums[1] + ... + sums[n-1], in that order) /
+ *     n_total, then alpha, rho_t exactly as pasa_budget.  dev_sums: DEVICE, nsums fp64
+ *     (the gathered per-rank sums, rank order); n_total: the element count of the full
+ *     latent.
+ * Errors: as pasa_budget; EINVAL for nsums < 1 or n_total < 1. */
+pasa_status pasa_budget_local_sum(const pasa_latent* x_t, const pasa_latent* x_tm1,
+                                  const pasa_latent* x_tm2, const pasa_schedule* schedule,
+                                  pasa_budget_h budget, double* dev_sum, void* stream);
+pasa_status pasa_budget_from_sums(const double* dev_sums, int32_t nsums, int64_t n_total,
+                                  const pasa_schedule* schedule, pasa_budget_h budget,
+                                  void* stream);
 
 /* pasa_route -- PAPER.md:189-193 (block partition, top-k per query block),
  * Eq. 8 pooled-logit term, stochastic bias

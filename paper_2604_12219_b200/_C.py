@@ -32,6 +32,7 @@ EXPORTS = [
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
     "pasa_version", "pasa_debug_trace", "pasa_debug_flags", "pasa_attn_stats_read",
     "pasa_route_v", "pasa_route_het_read", "pasa_calibrate", "pasa_copy2d",
+    "pasa_budget_local_sum", "pasa_budget_from_sums",
 ]
 
 
@@ -59,7 +60,8 @@ class PasaRouteCfg(ctypes.Structure):
     _fields_ = [("Bq", ctypes.c_int32), ("Bk", ctypes.c_int32), ("G", ctypes.c_int32),
                 ("comp", ctypes.c_int32), ("beta", ctypes.c_double),
                 ("H_total", ctypes.c_int64), ("head_offset", ctypes.c_int64),
-                ("prior", ctypes.c_int32), ("_pad", ctypes.c_int32), ("eps", ctypes.c_double)]
+                ("prior", ctypes.c_int32), ("_pad", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("qb_begin", ctypes.c_int32), ("qb_end", ctypes.c_int32)]
 
 
 class PasaError(RuntimeError):
@@ -96,6 +98,8 @@ def lib():
     L.pasa_route_fini.argtypes = [P]
     L.pasa_route_fini.restype = None
     L.pasa_budget.argtypes = [LT, LT, LT, ctypes.POINTER(PasaSchedule), P, P]
+    L.pasa_budget_local_sum.argtypes = [LT, LT, LT, ctypes.POINTER(PasaSchedule), P, P, P]
+    L.pasa_budget_from_sums.argtypes = [P, I32, I64, ctypes.POINTER(PasaSchedule), P, P]
     L.pasa_route.argtypes = [T, T, P, U64, I32, P, P]
     L.pasa_route_v.argtypes = [T, T, T, P, U64, I32, P, P]
     L.pasa_route_het_read.argtypes = [P, P, P]
@@ -123,6 +127,7 @@ def lib():
     L.pasa_debug_flags.restype = ctypes.c_int
     L.pasa_debug_flags.argtypes = [ctypes.c_int]
     for name in ("pasa_budget_init", "pasa_route_init", "pasa_budget", "pasa_route",
+                 "pasa_budget_local_sum", "pasa_budget_from_sums",
                  "pasa_attn", "pasa_attn_ex", "pasa_budget_read", "pasa_route_read",
                  "pasa_route_pooled_read", "pasa_route_dims"):
         getattr(L, name).restype = ctypes.c_int

@@ -76,23 +76,55 @@ class Budget:
         except Exception:  # pragma: no cover - interpreter shutdown
             pass
 
-    def __call__(self, x_t, x_tm1, x_tm2=None, *, T=50, step=25, rho=0.15, dense_frac=0.2,
-                 l1_mean=1.0, h_t=1.0, h_tm1=1.0, rho_max=1.0, rho_table=None, kind="latent",
-                 stream=None):
+    def _schedule(self, T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, rho_table, kind):
         kind_i = _C.PASA_IN_VELOCITY if kind == "velocity" else _C.PASA_IN_LATENT
-        a, b = latent_desc(x_t), latent_desc(x_tm1)
-        c = latent_desc(x_tm2) if x_tm2 is not None else None
         tab = None
         if rho_table is not None:
             if len(rho_table) < T:
                 raise ValueError(f"rho_table has {len(rho_table)} entries, needs T = {T}")
             self._tab = np.ascontiguousarray(np.asarray(rho_table, dtype=np.float64))
             tab = self._tab.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
-        sc = _C.PasaSchedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, tab, kind_i, 0)
+        return _C.PasaSchedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, tab, kind_i,
+                               0)
+
+    def __call__(self, x_t, x_tm1, x_tm2=None, *, T=50, step=25, rho=0.15, dense_frac=0.2,
+                 l1_mean=1.0, h_t=1.0, h_tm1=1.0, rho_max=1.0, rho_table=None, kind="latent",
+                 stream=None):
+        a, b = latent_desc(x_t), latent_desc(x_tm1)
+        c = latent_desc(x_tm2) if x_tm2 is not None else None
+        sc = self._schedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, rho_table, kind)
         st = _C.lib().pasa_budget(ctypes.byref(a), ctypes.byref(b),
                                   ctypes.byref(c) if c is not None else None, ctypes.byref(sc),
                                   self.handle, _stream_ptr(stream))
         _C.check(st, "pasa_budget")
+        return self
+
+    def local_sum(self, x_t, x_tm1, x_tm2=None, out=None, *, T=50, step=25, rho=0.15,
+                  dense_frac=0.2, l1_mean=1.0, h_t=1.0, h_tm1=1.0, rho_max=1.0, rho_table=None,
+                  kind="latent", stream=None) -> torch.Tensor:
+        """pasa_budget_local_sum: this rank's fp64 sum of |dv| (a 1-element device tensor)
+        for latents sharded across ranks."""
+        if out is None:
+            out = torch.empty(1, dtype=torch.float64, device=x_t.device)
+        a, b = latent_desc(x_t), latent_desc(x_tm1)
+        c = latent_desc(x_tm2) if x_tm2 is not None else None
+        sc = self._schedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, rho_table, kind)
+        _C.check(_C.lib().pasa_budget_local_sum(
+            ctypes.byref(a), ctypes.byref(b), ctypes.byref(c) if c is not None else None,
+            ctypes.byref(sc), self.handle, ctypes.c_void_p(out.data_ptr()), _stream_ptr(stream)),
+            "pasa_budget_local_sum")
+        return out
+
+    def from_sums(self, sums: torch.Tensor, n_total: int, *, T=50, step=25, rho=0.15,
+                  dense_frac=0.2, l1_mean=1.0, h_t=1.0, h_tm1=1.0, rho_max=1.0, rho_table=None,
+                  kind="latent", stream=None):
+        """pasa_budget_from_sums: l = (sums in rank order) / n_total, then Eqs. 10-11."""
+        if sums.dtype != torch.float64 or not sums.is_cuda or not sums.is_contiguous():
+            raise ValueError("sums must be a contiguous float64 CUDA tensor")
+        sc = self._schedule(T, step, rho, dense_frac, l1_mean, h_t, h_tm1, rho_max, rho_table, kind)
+        _C.check(_C.lib().pasa_budget_from_sums(ctypes.c_void_p(sums.data_ptr()), sums.numel(),
+                                                n_total, ctypes.byref(sc), self.handle,
+                                                _stream_ptr(stream)), "pasa_budget_from_sums")
         return self
 
     def read(self, stream=None) -> dict:
@@ -114,11 +146,13 @@ class RouteCfg:
     head_offset: int = 0
     prior: str = "none"          # Eq. 8 heterogeneity prior: "none" | "global" | "group"
     eps: float = 1e-6
+    qb_begin: int = 0            # query blocks [qb_begin, qb_end) only; (0, 0) = all
+    qb_end: int = 0              # (flattened (head, q-block) partition)
 
     def to_c(self, H: int) -> _C.PasaRouteCfg:
         return _C.PasaRouteCfg(self.Bq, self.Bk, self.G, _C.COMP[self.comp], self.beta,
                                self.H_total if self.H_total is not None else H, self.head_offset,
-                               _C.PRIOR[self.prior], 0, self.eps)
+                               _C.PRIOR[self.prior], 0, self.eps, self.qb_begin, self.qb_end)
 
 
 class Route:

@@ -63,6 +63,11 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
         return fail(PASA_EINVAL, "prior eps must be finite and > 0");
     const int64_t NK = (S + c->Bk - 1) / c->Bk;
     if (NK > 2048) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 2048 (S too long)", (long long)NK);
+    const int64_t NQ = (S + c->Bq - 1) / c->Bq;
+    if ((c->qb_begin != 0 || c->qb_end != 0) &&
+        !(c->qb_begin >= 0 && c->qb_begin < c->qb_end && c->qb_end <= NQ))
+        return fail(PASA_EINVAL, "q-block range [%d, %d) outside [0, N_Q=%lld)", c->qb_begin,
+                    c->qb_end, (long long)NQ);
     return PASA_OK;
 }
 
@@ -124,6 +129,31 @@ pasa_status match_route(const pasa_tensor* t, const pasa_route_s* r, const char*
                     name, (long long)t->B, (long long)t->S, (long long)t->H, (long long)t->D,
                     (long long)r->B, (long long)r->S, (long long)r->H, (long long)r->D);
     return PASA_OK;
+}
+
+pasa_status check_schedule(const pasa_schedule* sc) {
+    const bool vel = sc->kind == PASA_IN_VELOCITY;
+    if (sc->T < 1 || sc->step < 0 || sc->step >= sc->T)
+        return fail(PASA_EINVAL, "step=%d outside [0, T=%d)", sc->step, sc->T);
+    if (!vel && (sc->h_t == 0.0 || sc->h_tm1 == 0.0)) return fail(PASA_EINVAL, "h == 0");
+    if (!(sc->l1_mean > 0.0)) return fail(PASA_EDEGENERATE, "l1_mean must be > 0 (Eq. 10)");
+    if (!(sc->rho >= 0.0) || !(sc->rho_max > 0.0) || !(sc->dense_frac >= 0.0))
+        return fail(PASA_EINVAL, "rho / rho_max / dense_frac out of range");
+    return PASA_OK;
+}
+
+pasa::BudgetParams budget_params(const pasa_schedule* sc) {
+    pasa::BudgetParams p;
+    p.rht = 1.0 / sc->h_t;
+    p.rh1 = 1.0 / sc->h_tm1;
+    p.step = sc->step;
+    p.dense_steps = (int32_t)std::floor(sc->dense_frac * (double)sc->T + 0.5);
+    p.rho = sc->rho;
+    p.l1_mean = sc->l1_mean;
+    p.rho_max = sc->rho_max;
+    p.use_table = sc->rho_table != nullptr;
+    p.table_val = p.use_table ? sc->rho_table[sc->step] : 0.0;
+    return p;
 }
 
 }  // namespace
@@ -196,7 +226,8 @@ pasa_status pasa_copy2d(void* dst, size_t dpitch, const void* src, size_t spitch
 }
 
 size_t pasa_budget_workspace_bytes(void) {
-    return sizeof(pasa::BudgetRec) + sizeof(double) * pasa::kBudgetParts;
+    // record, one fp64 partial per reduction CTA, the CTAs' completion ticket
+    return sizeof(pasa::BudgetRec) + sizeof(double) * pasa::kBudgetParts + 64;
 }
 
 size_t pasa_route_workspace_bytes(const pasa_route_cfg* cfg, int64_t B, int64_t S, int64_t H,
@@ -216,6 +247,8 @@ pasa_status pasa_budget_init(void* dev_ws, size_t bytes, pasa_budget_h* out) {
     h->rec = reinterpret_cast<pasa::BudgetRec*>(dev_ws);
     h->partials = reinterpret_cast<double*>(reinterpret_cast<char*>(dev_ws) +
                                             sizeof(pasa::BudgetRec));
+    h->ticket = reinterpret_cast<unsigned int*>(h->partials + pasa::kBudgetParts);
+    h->ticket_ready = 0;   // zeroed on the handle's first launch (the kernel then resets it)
     *out = h;
     return PASA_OK;
 }
@@ -234,6 +267,9 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->cfg = *cfg;
     r->B = B; r->S = S; r->H = H; r->D = D;
     r->NQ = L.NQ; r->NK = L.NK; r->NG = L.NG; r->W = L.W; r->BH = L.BH;
+    const bool all = cfg->qb_begin == 0 && cfg->qb_end == 0;
+    r->qb0 = all ? 0 : cfg->qb_begin;
+    r->qb1 = all ? L.NQ : cfg->qb_end;
     r->hdr = reinterpret_cast<int32_t*>(w + L.off_hdr);
     r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
     r->kbar = reinterpret_cast<double*>(w + L.off_kbar);
@@ -264,20 +300,17 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
 void pasa_budget_fini(pasa_budget_h h) { delete h; }
 void pasa_route_fini(pasa_route_h h) { delete h; }
 
-pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
-                        const pasa_schedule* sc, pasa_budget_h budget, void* stream) {
-    g_launches = 0;
+namespace {
+// validation shared by pasa_budget and pasa_budget_local_sum; fills xs[3]
+pasa_status check_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
+                         const pasa_schedule* sc, pasa_budget_h budget, const pasa_latent* xs[3]) {
     if (!budget || !sc || !x_t || !x_tm1) return fail(PASA_EINVAL, "NULL argument");
     const bool vel = sc->kind == PASA_IN_VELOCITY;
     if (sc->kind != PASA_IN_LATENT && !vel) return fail(PASA_EINVAL, "kind=%d", sc->kind);
     if (!vel && !x_tm2) return fail(PASA_EINVAL, "x_tm2 is NULL for latent input");
-    if (sc->T < 1 || sc->step < 0 || sc->step >= sc->T)
-        return fail(PASA_EINVAL, "step=%d outside [0, T=%d)", sc->step, sc->T);
-    if (!vel && (sc->h_t == 0.0 || sc->h_tm1 == 0.0)) return fail(PASA_EINVAL, "h == 0");
-    if (!(sc->l1_mean > 0.0)) return fail(PASA_EDEGENERATE, "l1_mean must be > 0 (Eq. 10)");
-    if (!(sc->rho >= 0.0) || !(sc->rho_max > 0.0) || !(sc->dense_frac >= 0.0))
-        return fail(PASA_EINVAL, "rho / rho_max / dense_frac out of range");
-    const pasa_latent* xs[3] = {x_t, x_tm1, vel ? x_tm1 : x_tm2};
+    pasa_status st = check_schedule(sc);
+    if (st != PASA_OK) return st;
+    xs[0] = x_t; xs[1] = x_tm1; xs[2] = vel ? x_tm1 : x_tm2;
     for (int i = 0; i < 3; ++i) {
         if (!xs[i]->data) return fail(PASA_EINVAL, "latent %d data is NULL", i);
         if (xs[i]->dtype != x_t->dtype) return fail(PASA_EDTYPE, "latent dtypes differ");
@@ -288,16 +321,53 @@ pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const 
             return fail(PASA_ESHAPE, "latent %d not 16-byte aligned", i);
     }
     if (x_t->numel < 1) return fail(PASA_ESHAPE, "empty latent");
-    const int32_t dense_steps = (int32_t)std::floor(sc->dense_frac * (double)sc->T + 0.5);
-    const int use_table = sc->rho_table != nullptr;
-    const double tv = use_table ? sc->rho_table[sc->step] : 0.0;
+    return PASA_OK;
+}
+}  // namespace
+
+pasa_status pasa_budget(const pasa_latent* x_t, const pasa_latent* x_tm1, const pasa_latent* x_tm2,
+                        const pasa_schedule* sc, pasa_budget_h budget, void* stream) {
+    g_launches = 0;
+    const pasa_latent* xs[3];
+    pasa_status st = check_budget(x_t, x_tm1, x_tm2, sc, budget, xs);
+    if (st != PASA_OK) return st;
     int launches = 0;
-    cudaError_t e = pasa::launch_budget(
-        x_t->data, x_tm1->data, xs[2]->data, x_t->numel, x_t->dtype, vel ? 1 : 0, sc->h_t,
-        sc->h_tm1, sc->step, dense_steps, sc->rho, sc->l1_mean, sc->rho_max, use_table, tv,
-        budget, (cudaStream_t)stream, &launches);
+    cudaError_t e = pasa::launch_budget(xs[0]->data, xs[1]->data, xs[2]->data, x_t->numel,
+                                        x_t->dtype, sc->kind == PASA_IN_VELOCITY, budget_params(sc),
+                                        budget, nullptr, (cudaStream_t)stream, &launches);
     g_launches = launches;
     return cuda_status(e, "pasa_budget launch");
+}
+
+pasa_status pasa_budget_local_sum(const pasa_latent* x_t, const pasa_latent* x_tm1,
+                                  const pasa_latent* x_tm2, const pasa_schedule* sc,
+                                  pasa_budget_h budget, double* dev_sum, void* stream) {
+    g_launches = 0;
+    if (!dev_sum) return fail(PASA_EINVAL, "dev_sum is NULL");
+    const pasa_latent* xs[3];
+    pasa_status st = check_budget(x_t, x_tm1, x_tm2, sc, budget, xs);
+    if (st != PASA_OK) return st;
+    int launches = 0;
+    cudaError_t e = pasa::launch_budget(xs[0]->data, xs[1]->data, xs[2]->data, x_t->numel,
+                                        x_t->dtype, sc->kind == PASA_IN_VELOCITY, budget_params(sc),
+                                        budget, dev_sum, (cudaStream_t)stream, &launches);
+    g_launches = launches;
+    return cuda_status(e, "pasa_budget_local_sum launch");
+}
+
+pasa_status pasa_budget_from_sums(const double* dev_sums, int32_t nsums, int64_t n_total,
+                                  const pasa_schedule* sc, pasa_budget_h budget, void* stream) {
+    g_launches = 0;
+    if (!budget || !sc || !dev_sums) return fail(PASA_EINVAL, "NULL argument");
+    if (nsums < 1 || n_total < 1) return fail(PASA_EINVAL, "nsums=%d n_total=%lld", nsums,
+                                              (long long)n_total);
+    pasa_status st = check_schedule(sc);
+    if (st != PASA_OK) return st;
+    int launches = 0;
+    cudaError_t e = pasa::launch_budget_from_sums(dev_sums, nsums, n_total, budget_params(sc),
+                                                  budget, (cudaStream_t)stream, &launches);
+    g_launches = launches;
+    return cuda_status(e, "pasa_budget_from_sums launch");
 }
 
 namespace {

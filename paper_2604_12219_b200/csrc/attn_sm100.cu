@@ -64,6 +64,7 @@ struct Geo {
 
 struct Params {
     int64_t S, H, NQ, NK, NG, W;
+    int64_t qb0;        // first query block of the handle's range (grid.x covers the range)
     int32_t G, comp;
     float scale_log2;   // s * log2(e)
     float s;            // 1/sqrt(D)
@@ -126,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     const bool spin = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
     const bool tracing = p.trace != nullptr && (int)blockIdx.x == p.trace_x &&
                          (int)blockIdx.y == p.trace_y;
-    const int64_t i = blockIdx.x, bh = blockIdx.y;
+    const int64_t i = p.qb0 + blockIdx.x, bh = blockIdx.y;
     const int64_t b = bh / p.H, h = bh % p.H;
     const int64_t row = bh * p.NQ + i;
     const int32_t cnt = p.count[row];
@@ -650,7 +651,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
                              : (diag ? attn_sm100_kernel<D, true, 0> : attn_sm100_kernel<D, false, 0>);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)r->NQ, (unsigned)r->BH);
+    prm.qb0 = r->qb0;
+    dim3 grid((unsigned)(r->qb1 - r->qb0), (unsigned)r->BH);
     kern<<<grid, kThreads, smem, st>>>(mQ, mK, mV, mKb, mVs, mHt, prm);
     return cudaGetLastError();
 }

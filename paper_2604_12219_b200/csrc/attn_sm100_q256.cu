@@ -65,6 +65,7 @@ struct Geo {
 
 struct Params {
     int32_t S, H, NQ, NK, W, G, comp;
+    int32_t qb0;        // first query block of the handle's range (grid.x covers the range)
     float scale_log2;   // s * log2(e)
     float s;            // 1/sqrt(D)
     const int32_t* idx;
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ Ctl ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int i = blockIdx.x, bh = blockIdx.y;
+    const int i = p.qb0 + (int)blockIdx.x, bh = blockIdx.y;
     const int b = bh / p.H, h = bh % p.H;
     const int64_t row = (int64_t)bh * p.NQ + i;
     const int32_t cnt = p.count[row];
@@ -527,7 +528,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     auto kern = attn_sm100_q256_kernel<D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)r->NQ, (unsigned)r->BH);
+    prm.qb0 = (int32_t)r->qb0;
+    dim3 grid((unsigned)(r->qb1 - r->qb0), (unsigned)r->BH);
     kern<<<grid, kThreads, smem, st>>>(mQ, mK, mV, mKb, mVs, mHt, prm);
     return cudaGetLastError();
 }

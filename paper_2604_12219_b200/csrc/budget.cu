@@ -52,17 +52,39 @@ __device__ __forceinline__ double accel(double xt, double x1, double x2, int kin
     return fabs(__dsub_rn(__dmul_rn(a, rht), __dmul_rn(b, rh1)));
 }
 
+// Eq. 10 alpha = l / l-bar; Eq. 11 rho_t = rho * alpha (or the table entry),
+// clipped at rho_max (R-18); dense prefix (R-15) -> rho_t = 1.
+__device__ __forceinline__ void finish_record(double l, const BudgetParams& p, BudgetRec* rec) {
+    const double alpha = l / p.l1_mean;
+    double rho_t, dense = 0.0, clipped = 0.0;
+    if (p.step < p.dense_steps || p.step < 2) {
+        rho_t = 1.0;
+        dense = 1.0;
+    } else {
+        const double rp = p.use_table ? p.table_val : __dmul_rn(p.rho, alpha);
+        if (rp > p.rho_max) { rho_t = p.rho_max; clipped = 1.0; }
+        else rho_t = rp;
+    }
+    rec->l1 = l; rec->alpha = alpha; rec->rho_t = rho_t; rec->dense = dense;
+    rec->clipped = clipped;
+}
+
+// One launch: a fixed grid of kBudgetParts CTAs each reduce one contiguous chunk in
+// fp64 with a fixed shuffle tree; the last CTA to finish (completion ticket) sums the
+// partials in a fixed tree and writes the record (or, for sharded latents, the local
+// sum), then resets the ticket.  Bit-identical run to run.
 template <typename T>
-__global__ void __launch_bounds__(kThreads) budget_partial_kernel(
+__global__ void __launch_bounds__(kThreads) budget_kernel(
     const T* __restrict__ xt, const T* __restrict__ x1, const T* __restrict__ x2, int64_t n,
-    int kind, double rht, double rh1, double* __restrict__ partials) {
+    int kind, BudgetParams p, double* __restrict__ partials, unsigned int* ticket,
+    BudgetRec* __restrict__ rec, double* __restrict__ local_sum) {
     // chunk of a multiple of 4 elements per CTA (vector loads stay aligned)
-    int64_t chunk = ((n + kBudgetParts - 1) / kBudgetParts + 3) & ~int64_t(3);
-    int64_t e0 = (int64_t)blockIdx.x * chunk;
-    int64_t e1 = min(e0 + chunk, n);
+    const int64_t chunk = ((n + kBudgetParts - 1) / kBudgetParts + 3) & ~int64_t(3);
+    const int64_t e0 = (int64_t)blockIdx.x * chunk;
+    const int64_t e1 = min(e0 + chunk, n);
     double acc = 0.0;
     if (e0 < e1) {
-        int64_t nv = (e1 - e0) & ~int64_t(3);
+        const int64_t nv = (e1 - e0) & ~int64_t(3);
         for (int64_t e = e0 + 4 * (int64_t)threadIdx.x; e < e0 + nv; e += 4 * kThreads) {
             double a[4], b[4], c[4];
             load4<T>(xt, e, a);
@@ -70,14 +92,15 @@ __global__ void __launch_bounds__(kThreads) budget_partial_kernel(
             if (kind == 0) load4<T>(x2, e, c);
             else { c[0] = c[1] = c[2] = c[3] = 0.0; }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) acc += accel(a[u], b[u], c[u], kind, rht, rh1);
+            for (int u = 0; u < 4; ++u) acc += accel(a[u], b[u], c[u], kind, p.rht, p.rh1);
         }
         for (int64_t e = e0 + nv + threadIdx.x; e < e1; e += kThreads)
             acc += accel(load1<T>(xt, e), load1<T>(x1, e), kind == 0 ? load1<T>(x2, e) : 0.0,
-                         kind, rht, rh1);
+                         kind, p.rht, p.rh1);
     }
     // fixed-order reduction: warp shuffle tree, then warp 0 over the warp sums
     __shared__ double warp_sum[kThreads / 32];
+    __shared__ bool last;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) warp_sum[threadIdx.x >> 5] = acc;
@@ -86,57 +109,69 @@ __global__ void __launch_bounds__(kThreads) budget_partial_kernel(
         double v = threadIdx.x < kThreads / 32 ? warp_sum[threadIdx.x] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (threadIdx.x == 0) partials[blockIdx.x] = v;
+        if (threadIdx.x == 0) {
+            partials[blockIdx.x] = v;
+            __threadfence();
+            last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        }
     }
-}
-
-// Eq. 10 alpha = l / l-bar; Eq. 11 rho_t = rho * alpha (or the table entry),
-// clipped at rho_max (R-18); dense prefix (R-15) -> rho_t = 1.
-__global__ void budget_finalize_kernel(const double* __restrict__ partials, int64_t n,
-                                       int32_t step, int32_t dense_steps, double rho,
-                                       double l1_mean, double rho_max, int use_table,
-                                       double table_val, BudgetRec* __restrict__ rec) {
+    __syncthreads();
+    if (!last) return;
+    // the last CTA: every other CTA's partial is visible (fence before its ticket)
+    __threadfence();
     __shared__ double s[kBudgetParts];
-    for (int i = threadIdx.x; i < kBudgetParts; i += blockDim.x) s[i] = partials[i];
+    for (int i = threadIdx.x; i < kBudgetParts; i += blockDim.x)
+        s[i] = __ldcg(partials + i);
     __syncthreads();
     for (int w = kBudgetParts / 2; w > 0; w >>= 1) {
         for (int i = threadIdx.x; i < w; i += blockDim.x) s[i] = s[i] + s[i + w];
         __syncthreads();
     }
     if (threadIdx.x == 0) {
-        double l = n > 0 ? s[0] / (double)n : 0.0;
-        double alpha = l / l1_mean;
-        double rho_t, dense = 0.0, clipped = 0.0;
-        if (step < dense_steps || step < 2) {
-            rho_t = 1.0;
-            dense = 1.0;
-        } else {
-            double rp = use_table ? table_val : __dmul_rn(rho, alpha);
-            if (rp > rho_max) { rho_t = rho_max; clipped = 1.0; }
-            else rho_t = rp;
-        }
-        rec->l1 = l; rec->alpha = alpha; rec->rho_t = rho_t; rec->dense = dense;
-        rec->clipped = clipped;
+        *ticket = 0u;
+        if (local_sum) *local_sum = s[0];
+        else finish_record(n > 0 ? s[0] / (double)n : 0.0, p, rec);
     }
+}
+
+// sharded latents: l = (sum of the ranks' local sums, in rank order) / n_total
+__global__ void budget_from_sums_kernel(const double* __restrict__ sums, int32_t nsums,
+                                        int64_t n_total, BudgetParams p,
+                                        BudgetRec* __restrict__ rec) {
+    double acc = 0.0;
+    for (int32_t r = 0; r < nsums; ++r) acc += sums[r];
+    finish_record(acc / (double)n_total, p, rec);
 }
 
 }  // namespace
 
 cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, int64_t n, int dtype,
-                          int kind, double h_t, double h_tm1, int32_t step, int32_t dense_steps,
-                          double rho, double l1_mean, double rho_max, int use_table,
-                          double table_val, pasa_budget_s* b, cudaStream_t st, int* launches) {
+                          int kind, const BudgetParams& p, pasa_budget_s* b, double* local_sum,
+                          cudaStream_t st, int* launches) {
+    // the completion ticket starts at 0: zeroed once, on the handle's first launch (stream
+    // ordered, graph capturable); every launch's last CTA resets it afterwards
+    if (!b->ticket_ready) {
+        const cudaError_t e = cudaMemsetAsync(b->ticket, 0, sizeof(unsigned int), st);
+        if (e != cudaSuccess) return e;
+        b->ticket_ready = 1;
+    }
     if (dtype == PASA_F32)
-        budget_partial_kernel<float><<<kBudgetParts, kThreads, 0, st>>>(
-            (const float*)xt, (const float*)xtm1, (const float*)xtm2, n, kind, 1.0 / h_t,
-            1.0 / h_tm1, b->partials);
+        budget_kernel<float><<<kBudgetParts, kThreads, 0, st>>>(
+            (const float*)xt, (const float*)xtm1, (const float*)xtm2, n, kind, p, b->partials,
+            b->ticket, b->rec, local_sum);
     else
-        budget_partial_kernel<__nv_bfloat16><<<kBudgetParts, kThreads, 0, st>>>(
+        budget_kernel<__nv_bfloat16><<<kBudgetParts, kThreads, 0, st>>>(
             (const __nv_bfloat16*)xt, (const __nv_bfloat16*)xtm1, (const __nv_bfloat16*)xtm2, n,
-            kind, 1.0 / h_t, 1.0 / h_tm1, b->partials);
-    budget_finalize_kernel<<<1, 256, 0, st>>>(b->partials, n, step, dense_steps, rho, l1_mean,
-                                              rho_max, use_table, table_val, b->rec);
-    *launches += 2;
+            kind, p, b->partials, b->ticket, b->rec, local_sum);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_budget_from_sums(const double* sums, int32_t nsums, int64_t n_total,
+                                    const BudgetParams& p, pasa_budget_s* b, cudaStream_t st,
+                                    int* launches) {
+    budget_from_sums_kernel<<<1, 1, 0, st>>>(sums, nsums, n_total, p, b->rec);
+    *launches += 1;
     return cudaGetLastError();
 }
 

@@ -16,16 +16,27 @@ struct BudgetRec {                    // device record, 64 bytes
     double l1, alpha, rho_t, dense, clipped, pad0, pad1, pad2;
 };
 
+struct BudgetParams {                 // host-derived scalars of one budget call
+    double rht, rh1;                  // 1 / h_t, 1 / h_{t-1}
+    int32_t step, dense_steps;
+    double rho, l1_mean, rho_max;
+    int32_t use_table;
+    double table_val;
+};
+
 }  // namespace pasa
 
 struct pasa_budget_s {
     pasa::BudgetRec* rec;            // device
     double* partials;                // device [kBudgetParts]
+    unsigned int* ticket;            // device: CTAs of the running reduction that finished
+    int ticket_ready;                // host: the ticket has been zeroed on a stream
 };
 
 struct pasa_route_s {
     pasa_route_cfg cfg;
     int64_t B, S, H, D, NQ, NK, NG, W, BH;
+    int64_t qb0, qb1;                // query blocks this handle routes / attends: [qb0, qb1)
     int32_t* hdr;                    // device: [0] = k of the last pasa_route
     double* qbar;                    // [BH][NQ][D]
     double* kbar;                    // [BH][NK][D]
@@ -53,10 +64,13 @@ struct pasa_route_s {
 namespace pasa {
 
 // ---- launchers (each returns cudaGetLastError() after its launches) -------
+// local_sum != nullptr: store the fp64 sum of |dv| there instead of finishing the record
 cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, int64_t n, int dtype,
-                          int kind, double h_t, double h_tm1, int32_t step, int32_t dense_steps,
-                          double rho, double l1_mean, double rho_max, int use_table,
-                          double table_val, pasa_budget_s* b, cudaStream_t st, int* launches);
+                          int kind, const BudgetParams& p, pasa_budget_s* b, double* local_sum,
+                          cudaStream_t st, int* launches);
+cudaError_t launch_budget_from_sums(const double* sums, int32_t nsums, int64_t n_total,
+                                    const BudgetParams& p, pasa_budget_s* b, cudaStream_t st,
+                                    int* launches);
 
 // v != nullptr: Eq. 8 prior (het.cu) between pooling and scoring
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,

@@ -48,6 +48,7 @@ struct PoolArgs {
     int64_t S, H, D;
     int32_t bsz;    // block size in tokens
     int64_t nblk;   // blocks per head
+    int64_t blk0, ntask;   // blocks [blk0, blk0 + ntask) of every head are pooled
     double* out;    // [BH][nblk][D]
     double* frag;   // optional DMMA B-fragment copy [BH][ceil(nblk/8)][D/8][8][4][2]
 };
@@ -63,8 +64,8 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
     int64_t ng = a.D / 8;
     int64_t dg = task % ng;
     int64_t rest = task / ng;
-    int64_t blk = rest % a.nblk;
-    int64_t bh = rest / a.nblk;
+    int64_t blk = a.blk0 + rest % a.ntask;
+    int64_t bh = rest / a.ntask;
     int64_t b = bh / a.H, h = bh % a.H;
     int64_t t0 = blk * a.bsz;
     int64_t t1 = min(t0 + (int64_t)a.bsz, a.S);
@@ -170,6 +171,7 @@ struct FusedArgs {
     const double* prior;       // [BH][NK] or nullptr
     const BudgetRec* rec;
     int64_t NQ, NK, W, H, H_total, head_offset;
+    int64_t qb0, qb1;          // query blocks routed: [qb0, qb1)
     int D, NKP;                // NKP: odd row stride of the score rows (doubles)
     double s, beta;
     uint32_t key0, key1, step;
@@ -336,8 +338,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     const int NK = (int)a.NK, NKP = a.NKP;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t bh = blockIdx.y;
-    const int64_t i0 = (int64_t)blockIdx.x * R;
-    const int nrows = (int)min((int64_t)R, a.NQ - i0);
+    const int64_t i0 = a.qb0 + (int64_t)blockIdx.x * R;
+    const int nrows = (int)min((int64_t)R, a.qb1 - i0);
     double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(sq + R * (D + 4));    // [NW][64]
     double* sc = SMEM_SC ? reinterpret_cast<double*>(cbuf + NW * 64)
@@ -347,7 +349,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     if (blockIdx.x == 0 && bh == 0 && tid == 0) a.hdr[0] = k;
     const int M = (NK + 31) >> 5;
     if (k >= NK) {   // dense step / full budget: every block exact, no scores needed
-        if (warp < nrows) {
+        if (warp < nrows) {   // (one row per warp: R = 8)
             const int64_t row = bh * a.NQ + i0 + warp;
             int32_t* orow = a.idx + row * NK;
             uint32_t* mrow = a.mask + row * a.W;
@@ -511,11 +513,13 @@ constexpr size_t fused_fixed_smem(int R, int D) {
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches) {
-    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qbar, nullptr};
-    PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, r->kbar,
+    // Q only for this handle's query blocks [qb0, qb1); K for every block (all are scored)
+    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qb0,
+                r->qb1 - r->qb0, r->qbar, nullptr};
+    PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, 0, r->NK, r->kbar,
                 r->kfrag};
     int64_t ng = r->D / 8;
-    int64_t q_tasks = r->BH * r->NQ * ng;
+    int64_t q_tasks = r->BH * (r->qb1 - r->qb0) * ng;
     int64_t total = q_tasks + r->BH * r->NK * ng;
     const unsigned pgrid = (unsigned)((total + 255) / 256);
     if (q.dtype == PASA_F32)
@@ -533,6 +537,7 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     FusedArgs fa;
     fa.qbar = r->qbar; fa.kfrag = r->kfrag; fa.prior = prior; fa.rec = b->rec;
     fa.NQ = r->NQ; fa.NK = r->NK; fa.W = r->W; fa.H = r->H;
+    fa.qb0 = r->qb0; fa.qb1 = r->qb1;
     fa.H_total = r->cfg.H_total; fa.head_offset = r->cfg.head_offset;
     fa.D = (int)r->D; fa.NKP = (int)route_score_stride(r->NK);
     fa.s = s; fa.beta = r->cfg.beta;
@@ -544,7 +549,7 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     constexpr int RR = kFRows;
     const size_t smem = fused_fixed_smem(RR, (int)r->D) +
                         (smem_sc ? sizeof(double) * (size_t)RR * fa.NKP : 0);
-    dim3 grid((unsigned)((r->NQ + RR - 1) / RR), (unsigned)r->BH);
+    dim3 grid((unsigned)((r->qb1 - r->qb0 + RR - 1) / RR), (unsigned)r->BH);
     const bool hreg = r->NK <= 32 * kFHR;
 #define PASA_FUSED_PICK(DD)                                                                  \
     (!smem_sc ? route_fused_kernel<RR, DD, false, 0>                                         \

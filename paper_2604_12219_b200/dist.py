@@ -1,5 +1,7 @@
-"""Multi-GPU plumbing for PASA: head partitioning and, only for
-sequence-sharded input, a Ulysses all-to-all.
+"""Multi-GPU plumbing for PASA: head partitioning (or, when the head
+count does not divide the GPU count, a flattened (head, q-block) partition), the
+sharded-latent budget and, only for sequence-sharded input, a Ulysses all-to-all
+chunked by head group so attention on arrived heads overlaps the transfer of the rest.
 
 Every (batch, head) is an independent unit of the method (its own pooled
 statistics, groups, route and output), so the hot path needs no collective:
@@ -14,7 +16,7 @@ the local heads and moves the output back with one more all-to-all.
 """
 from __future__ import annotations
 
-from typing import Callable
+from typing import Callable, List, Optional, Tuple
 
 import torch
 import torch.distributed as dist
@@ -78,3 +80,161 @@ def ulysses_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor,
     qh, kh, vh = (seq_to_head(t, group) for t in (q, k, v))
     oh = local_attn(qh, kh, vh, off, H)
     return head_to_seq(oh, group)
+
+
+# ------------------------------------------------- flattened (head, q-block) split --
+def flat_partition(H: int, NQ: int, world: int, rank: int) -> List[Tuple[int, int, int, int]]:
+    """Rank r owns the flattened work items [floor(r N / P), floor((r+1) N / P)) of the
+    N = H * NQ (head, q-block) items, head-major (Wan-1.3B's 12 heads over
+    8 ranks is capped at 75% efficiency by the head split; 3,072 items split to 384 each).
+    Returns segments (head_offset, n_heads, qb_begin, qb_end): one route handle each, with
+    (0, 0) = all N_Q q-blocks of n_heads whole heads, else one head's q-block range."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"rank {rank} of world {world}")
+    N = H * NQ
+    a, b = N * rank // world, N * (rank + 1) // world
+    if a >= b:
+        return []
+    segs = []
+    ha, ia = divmod(a, NQ)
+    hb, ib = divmod(b - 1, NQ)
+    ib += 1
+    if ha == hb:
+        return [(ha, 1, 0, 0) if (ia, ib) == (0, NQ) else (ha, 1, ia, ib)]
+    if ia > 0:
+        segs.append((ha, 1, ia, NQ))
+        ha += 1
+    full_end = hb if ib < NQ else hb + 1
+    if full_end > ha:
+        segs.append((ha, full_end - ha, 0, 0))
+    if ib < NQ:
+        segs.append((hb, 1, 0, ib))
+    return segs
+
+
+def partition_heads(segs) -> Tuple[int, int]:
+    """(first global head, number of heads) a rank's segments touch (its K/V slice)."""
+    if not segs:
+        return 0, 0
+    h0 = segs[0][0]
+    h1 = max(h + n for h, n, _, _ in segs)
+    return h0, h1 - h0
+
+
+# ------------------------------------------------------------ collectives -----------
+def _backend(group=None) -> str:
+    return dist.get_backend(group)
+
+
+def all_to_all(recv: torch.Tensor, send: torch.Tensor, group=None, async_op: bool = False):
+    """all_to_all_single; NCCL asynchronously on its stream (the returned work's wait()
+    makes the current stream wait), gloo through host memory (debug mode: ranks that
+    share one GPU)."""
+    if _backend(group) == "nccl" or not send.is_cuda:
+        return dist.all_to_all_single(recv, send, group=group, async_op=async_op)
+    r = torch.empty(send.shape, dtype=send.dtype)
+    dist.all_to_all_single(r, send.cpu(), group=group)
+    recv.copy_(r)
+    return None
+
+
+def all_gather_sums(local: torch.Tensor, group=None) -> torch.Tensor:
+    """[P] float64 on local's device: every rank's 1-element local sum, rank order."""
+    P = dist.get_world_size(group)
+    if _backend(group) == "nccl" or not local.is_cuda:
+        out = torch.empty(P, dtype=local.dtype, device=local.device)
+        dist.all_gather_into_tensor(out, local, group=group)
+        return out
+    parts = [torch.empty(1, dtype=local.dtype) for _ in range(P)]
+    dist.all_gather(parts, local.cpu(), group=group)
+    return torch.cat(parts).to(local.device)
+
+
+def sharded_budget(budget, x_t, x_tm1, x_tm2, n_total: int, group=None, **schedule):
+    """Budget over latents split across ranks: pasa_budget_local_sum on
+    this rank's shard, all_gather of the fp64 sums, pasa_budget_from_sums in rank order."""
+    local = budget.local_sum(x_t, x_tm1, x_tm2, **schedule)
+    sums = all_gather_sums(local, group) if dist.is_initialized() else local
+    return budget.from_sums(sums, n_total, **schedule)
+
+
+# ------------------------------------------------- chunked Ulysses all-to-all ----
+class Ulysses:
+    """Sequence-sharded attention input [B, S/P, H, D] per rank -> this rank's heads
+    [B, S, H/P, D] -> PASA -> output back to [B, S/P, H, D], in `chunks` head groups:
+    all chunks' all-to-alls are issued up front (NCCL, asynchronous, on its own stream);
+    chunk c's attention starts once chunk c has arrived and its output is sent back at
+    once, so transfers overlap attention.  Packing is one strided copy
+    per tensor and chunk into a preallocated send buffer; with B = 1 the receive buffer
+    [P, 1, S/P, hc, D] is already the [1, S, hc, D] layout PASA reads (no unpack) and the
+    attention writes its output straight into the return send buffer."""
+
+    def __init__(self, B: int, S: int, H: int, D: int, dtype, device, group=None,
+                 chunks: int = 1):
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.group = group
+        if H % self.P or S % self.P:
+            raise ValueError(f"H={H}, S={S} must split over {self.P} ranks")
+        self.B, self.S, self.H, self.D = B, S, H, D
+        self.Hl = H // self.P
+        if self.Hl % chunks:
+            raise ValueError(f"{self.Hl} local heads do not split into {chunks} chunks")
+        self.C, self.hc = chunks, self.Hl // chunks
+        Sl = S // self.P
+        shp = (self.P, B, Sl, self.hc, D)
+        mk = lambda: [torch.empty(shp, dtype=dtype, device=device) for _ in range(chunks)]  # noqa: E731
+        self.send = {n: mk() for n in "qkvo"} if self.P > 1 else None
+        self.recv = {n: mk() for n in "qkvo"} if self.P > 1 else None
+
+    def head_offset(self, c: int) -> int:
+        """Global head index of chunk c's first head on this rank."""
+        return self.rank * self.Hl + c * self.hc
+
+    def _heads(self, buf: torch.Tensor) -> torch.Tensor:
+        """[P, B, S/P, hc, D] (source rank major) -> [B, S, hc, D]."""
+        if self.B == 1:
+            return buf.view(1, self.S, self.hc, self.D)
+        return buf.permute(1, 0, 2, 3, 4).reshape(self.B, self.S, self.hc, self.D)
+
+    def __call__(self, q_s, k_s, v_s, out_s, compute: Callable) -> torch.Tensor:
+        """compute(c, q, k, v, out, head_offset) runs PASA on chunk c ([B, S, hc, D]
+        tensors; out is written).  Returns out_s ([B, S/P, H, D])."""
+        B, Sl, C, hc, Hl, P = self.B, self.S // self.P, self.C, self.hc, self.Hl, self.P
+        if P == 1:
+            for c in range(C):
+                sl = slice(c * hc, (c + 1) * hc)
+                compute(c, q_s[:, :, sl], k_s[:, :, sl], v_s[:, :, sl], out_s[:, :, sl],
+                        self.head_offset(c))
+            return out_s
+        works = []
+        for c in range(C):
+            w = []
+            for n, x in (("q", q_s), ("k", k_s), ("v", v_s)):
+                # send[p] = my sequence shard of rank p's chunk-c heads
+                src = x.view(B, Sl, P, Hl, self.D)[:, :, :, c * hc:(c + 1) * hc]
+                self.send[n][c].copy_(src.permute(2, 0, 1, 3, 4))
+                w.append(all_to_all(self.recv[n][c], self.send[n][c], self.group, async_op=True))
+            works.append(w)
+        back = []
+        for c in range(C):
+            for w in works[c]:
+                if w is not None:
+                    w.wait()
+            qh, kh, vh = (self._heads(self.recv[n][c]) for n in "qkv")
+            if B == 1:
+                oh = self.send["o"][c].view(1, self.S, hc, self.D)
+                compute(c, qh, kh, vh, oh, self.head_offset(c))
+            else:
+                oh = torch.empty((B, self.S, hc, self.D), dtype=out_s.dtype, device=out_s.device)
+                compute(c, qh, kh, vh, oh, self.head_offset(c))
+                self.send["o"][c].copy_(oh.view(B, P, Sl, hc, self.D).permute(1, 0, 2, 3, 4))
+            back.append(all_to_all(self.recv["o"][c], self.send["o"][c], self.group,
+                                   async_op=True))
+        for c in range(C):
+            if back[c] is not None:
+                back[c].wait()
+            # recv[p] = my sequence shard of rank p's chunk-c heads
+            dst = out_s.view(B, Sl, P, Hl, self.D)[:, :, :, c * hc:(c + 1) * hc]
+            dst.copy_(self.recv["o"][c].permute(1, 2, 0, 3, 4))
+        return out_s

@@ -110,3 +110,82 @@ def test_ulysses_gloo_world2_matches_single_process():
     errs = mp.Manager().dict()
     mp.spawn(_worker, args=(2, _free_port(), q, k, v, ref, errs), nprocs=2, join=True)
     assert errs[0] == 0.0 and errs[1] == 0.0
+
+
+# ---------------------------------------------------------------- round 2 --------
+def test_flat_partition_covers_items_once_and_balances():
+    """The flattened (head, q-block) split: every item exactly once, in
+    head-major order, each rank floor/ceil of N / P items, segments are valid handles."""
+    for H, NQ, P in [(12, 256, 8), (40, 591, 8), (3, 5, 2), (12, 256, 1), (5, 7, 3),
+                     (24, 929, 8), (1, 3, 4)]:
+        items = []
+        for r in range(P):
+            segs = pdist.flat_partition(H, NQ, P, r)
+            mine = []
+            for h, n, a, b in segs:
+                assert (a, b) == (0, 0) or (n == 1 and 0 <= a < b <= NQ)
+                a, b = (0, NQ) if (a, b) == (0, 0) else (a, b)
+                mine += [(hh, i) for hh in range(h, h + n) for i in range(a, b)]
+            assert len(mine) in (H * NQ // P, -(-H * NQ // P))
+            h0, nh = pdist.partition_heads(segs)
+            assert all(h0 <= hh < h0 + nh for hh, _ in mine)
+            items += mine
+        assert items == [(h, i) for h in range(H) for i in range(NQ)]
+    # Wan-1.3B over 8 ranks: 384 items each instead of 1 or 2 heads (256 or 512 items)
+    assert [sum((b or 256) - a if n == 1 else 256 * n for _, n, a, b in
+                pdist.flat_partition(12, 256, 8, r)) for r in range(8)] == [384] * 8
+
+
+def _chunked_worker(rank, world, port, q, k, v, ref, chunks, errs):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        B, S, H, D = q.shape
+        Sl = S // world
+        sl = slice(rank * Sl, (rank + 1) * Sl)
+        uly = pdist.Ulysses(B, S, H, D, q.dtype, "cpu", chunks=chunks)
+        seen = []
+
+        def compute(c, qh, kh, vh, oh, off):
+            seen.append(off)
+            oh.copy_(_oracle_pasa(qh.contiguous(), kh.contiguous(), vh.contiguous(), off, H)
+                     .reshape(oh.shape))
+
+        out = torch.empty(B, Sl, H, D, dtype=q.dtype)
+        uly(q[:, sl].contiguous(), k[:, sl].contiguous(), v[:, sl].contiguous(), out, compute)
+        assert seen == [rank * (H // world) + c * (H // world // chunks) for c in range(chunks)]
+        errs[rank] = float((out - ref[:, sl]).abs().max())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("B,chunks", [(1, 2), (2, 2), (1, 1)])
+def test_ulysses_chunked_gloo_world2(B, chunks):
+    """Chunked Ulysses (head groups, per-chunk all-to-alls, B = 1 zero-copy views and the
+    B > 1 unpack path) reproduces the single-process result exactly."""
+    g = torch.Generator().manual_seed(3)
+    S, H, D = 256, 4, 8
+    q, k, v = (torch.randn(B, S, H, D, generator=g, dtype=torch.float64) for _ in range(3))
+    ref = _oracle_pasa(q, k, v, 0, H).reshape(B, S, H, D)
+    errs = mp.Manager().dict()
+    mp.spawn(_chunked_worker, args=(2, _free_port(), q, k, v, ref, chunks, errs), nprocs=2,
+             join=True)
+    assert errs[0] == 0.0 and errs[1] == 0.0
+
+
+def _gather_worker(rank, world, port, errs):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        got = pdist.all_gather_sums(torch.tensor([10.0 * rank + 0.5], dtype=torch.float64))
+        errs[rank] = got.tolist()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_all_gather_sums_rank_order_gloo_world2():
+    errs = mp.Manager().dict()
+    mp.spawn(_gather_worker, args=(2, _free_port(), errs), nprocs=2, join=True)
+    assert errs[0] == errs[1] == [0.5, 10.5]

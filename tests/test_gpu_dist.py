@@ -1,0 +1,218 @@
+"""Multi-GPU paths of SURVEY.md §8e through the PRODUCT library (libpasa.so):
+
+* q-block ranges (pasa_route_cfg.qb_begin/qb_end), the building block of the flattened
+  (head, q-block) partition: rows in range equal the full run bit for bit, rows outside
+  are not written;
+* the sharded-latent budget (pasa_budget_local_sum / pasa_budget_from_sums) against the
+  unsharded call and the fp64 oracle;
+* two ranks (torch.multiprocessing, gloo, both on cuda:0 -- the gpurun box has one GPU):
+  the chunked Ulysses all-to-all with PASA per chunk, the flattened partition and the
+  sharded budget each reproduce the single-process result exactly.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pasa():
+    from paper_2604_12219_b200 import build
+    build.build()
+    import paper_2604_12219_b200 as P
+    return P
+
+
+def _budget(P, rho=0.15, step=25, T=50):
+    b = P.Budget()
+    x = torch.zeros(64, device="cuda")
+    b(x, x, x, T=T, step=step, rho_table=[rho] * T, l1_mean=1.0)
+    return b
+
+
+def _run(P, q, k, v, cfg, budget, seed=42, step=25, out=None):
+    B, S, H, D = q.shape
+    r = P.Route(B, S, H, D, cfg)
+    r(q, k, budget, seed, step)
+    out = P.attn(q, k, v, r, out)
+    torch.cuda.synchronize()
+    return r, out
+
+
+@pytest.mark.parametrize("dtype,Bq,rng", [
+    (torch.bfloat16, 128, (3, 17)), (torch.bfloat16, 128, (30, 33)),   # last one ragged
+    (torch.bfloat16, 256, (2, 9)), (torch.float32, 128, (0, 5)),        # q256 / SIMT kernels
+    (torch.bfloat16, 128, (0, 33)),                                     # the full range
+])
+def test_qblock_range_equals_full_run(pasa, dtype, Bq, rng):
+    P = pasa
+    B, S, H, D = 1, 4100, 2, 128
+    q, k, v = synth.video_qkv(B, (1, 1, S), H, D, seed=11, dtype=dtype, device="cuda")
+    budget = _budget(P)
+    full_r, full_o = _run(P, q, k, v, P.RouteCfg(Bq=Bq, G=32, beta=0.1), budget)
+    a, b = rng
+    NQ = full_r.NQ
+    b = min(b, NQ)
+    out = torch.full_like(q, float("nan"))
+    part_r, out = _run(P, q, k, v, P.RouteCfg(Bq=Bq, G=32, beta=0.1, qb_begin=a, qb_end=b),
+                       budget, out=out)
+    got, want = part_r.read(), full_r.read()
+    kk = got["k"]
+    assert kk == want["k"]
+    assert np.array_equal(got["idx"][:, a:b, :kk], want["idx"][:, a:b, :kk])
+    for key in ("count", "mask"):
+        assert np.array_equal(got[key][:, a:b], want[key][:, a:b]), key
+    t0, t1 = a * Bq, min(b * Bq, S)
+    assert torch.equal(out[:, t0:t1], full_o[:, t0:t1])
+    outside = torch.cat([out[:, :t0], out[:, t1:]], 1)
+    assert torch.isnan(outside.float()).all(), "rows outside the range were written"
+
+
+def test_qblock_range_rejects_bad_ranges(pasa):
+    P = pasa
+    with pytest.raises(P.PasaError):
+        P.Route(1, 4100, 1, 128, P.RouteCfg(qb_begin=5, qb_end=5))
+    with pytest.raises(P.PasaError):
+        P.Route(1, 4100, 1, 128, P.RouteCfg(qb_begin=0, qb_end=34))
+
+
+def test_sharded_budget_matches_unsharded_and_oracle(pasa):
+    P = pasa
+    tp = synth.ThreePhase(shape=(3 * 4096 + 12,), T=50, seed=7, device="cuda")
+    xs = [x.contiguous() for x in tp.latents(30)]
+    n = xs[0].numel()
+    kw = dict(T=50, step=30, rho=0.15, l1_mean=tp.expected_l1_mean(), h_t=1 / 50, h_tm1=1 / 50)
+    full = P.Budget()
+    full(*xs, **kw)
+    want = full.read()
+    orc = oracle.budget(*xs, **kw)
+    cuts = [0, 4096, 8192 + 8, n]                    # 16-byte aligned shard starts
+    b = P.Budget()
+    sums = torch.cat([b.local_sum(*(x[c0:c1] for x in xs), **kw)
+                      for c0, c1 in zip(cuts[:-1], cuts[1:])])
+    b.from_sums(sums, n, **kw)
+    got = b.read()
+    assert abs(got["l1"] - want["l1"]) <= 1e-12 * want["l1"]
+    assert abs(got["l1"] - orc["l1"]) <= 1e-12 * orc["l1"]
+    assert abs(got["rho_t"] - want["rho_t"]) <= 1e-12 * want["rho_t"]
+    assert (got["dense"], got["clipped"]) == (want["dense"], want["clipped"])
+    # the rank-order sum is exactly what from_sums divides
+    assert got["l1"] == float(sum(sums.cpu().tolist())) / n
+
+
+# ------------------------------------------------------------- two ranks ----------
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+CFG = dict(B=1, S=4096, H=4, D=128)
+
+
+def _inputs():
+    q, k, v = synth.video_qkv(CFG["B"], (1, 1, CFG["S"]), CFG["H"], CFG["D"], seed=21,
+                              dtype=torch.bfloat16, device="cuda")
+    tp = synth.ThreePhase(shape=(8192,), T=50, seed=7, device="cuda")
+    xs = [x.contiguous() for x in tp.latents(30)]
+    kw = dict(T=50, step=30, rho=0.15, l1_mean=tp.expected_l1_mean(), h_t=1 / 50, h_tm1=1 / 50)
+    return q, k, v, xs, kw
+
+
+def _rank_main(rank, world, port, mode, result):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2604_12219_b200 as P
+        from paper_2604_12219_b200 import dist as pdist
+        q, k, v, xs, kw = _inputs()
+        B, S, H, D = q.shape
+        seed, step = P.layer_seed(42, 0), 30
+        budget = P.Budget()
+        n = xs[0].numel()
+        sl = slice(rank * n // world, (rank + 1) * n // world)
+        pdist.sharded_budget(budget, *(x[sl] for x in xs), n_total=n, **kw)
+        if mode == "budget":
+            result[rank] = budget.read()
+            return
+        if mode == "ulysses":
+            Sl = S // world
+            ss = slice(rank * Sl, (rank + 1) * Sl)
+            uly = pdist.Ulysses(B, S, H, D, q.dtype, q.device, chunks=2)
+            routes = {}
+
+            def compute(c, qh, kh, vh, oh, off):
+                r = routes.get(c)
+                if r is None:
+                    cfg = P.RouteCfg(Bq=128, G=32, beta=0.1, H_total=H, head_offset=off)
+                    r = routes[c] = P.Route(B, S, qh.shape[2], D, cfg)
+                r(qh, kh, budget, seed, step)
+                P.attn(qh, kh, vh, r, oh)
+
+            out = torch.empty(B, Sl, H, D, dtype=q.dtype, device=q.device)
+            uly(q[:, ss].contiguous(), k[:, ss].contiguous(), v[:, ss].contiguous(), out, compute)
+            torch.cuda.synchronize()
+            result[rank] = (ss.start, ss.stop, out.cpu())
+        else:   # flattened (head, q-block) partition
+            NQ = (S + 127) // 128
+            segs = pdist.flat_partition(H, NQ, world, rank)
+            out = torch.full_like(q, float("nan"))
+            for h, nh, a, b in segs:
+                hs = slice(h, h + nh)
+                cfg = P.RouteCfg(Bq=128, G=32, beta=0.1, H_total=H, head_offset=h,
+                                 qb_begin=a, qb_end=b)
+                r = P.Route(B, S, nh, D, cfg)
+                r(q[:, :, hs], k[:, :, hs], budget, seed, step)
+                P.attn(q[:, :, hs], k[:, :, hs], v[:, :, hs], r, out[:, :, hs])
+            torch.cuda.synchronize()
+            result[rank] = (segs, out.cpu())
+    finally:
+        dist.destroy_process_group()
+
+
+def _single(P):
+    q, k, v, xs, kw = _inputs()
+    B, S, H, D = q.shape
+    budget = P.Budget()
+    n = xs[0].numel()
+    sums = torch.cat([budget.local_sum(*(x[c * n // 2:(c + 1) * n // 2] for x in xs), **kw)
+                      for c in range(2)])
+    budget.from_sums(sums, n, **kw)
+    r = P.Route(B, S, H, D, P.RouteCfg(Bq=128, G=32, beta=0.1))
+    r(q, k, budget, P.layer_seed(42, 0), 30)
+    out = P.attn(q, k, v, r)
+    torch.cuda.synchronize()
+    return budget.read(), out.cpu()
+
+
+@pytest.mark.parametrize("mode", ["budget", "ulysses", "flat"])
+def test_two_ranks_reproduce_single_process(pasa, mode):
+    rec, ref = _single(pasa)
+    res = mp.Manager().dict()
+    mp.spawn(_rank_main, args=(2, _port(), mode, res), nprocs=2, join=True)
+    if mode == "budget":
+        assert res[0] == res[1] == rec
+    elif mode == "ulysses":
+        for r in range(2):
+            a, b, o = res[r]
+            assert torch.equal(o, ref[:, a:b]), r
+    else:
+        got = torch.full_like(ref, float("nan"))
+        for r in range(2):
+            segs, o = res[r]
+            for h, nh, a, b in segs:
+                t0, t1 = (a * 128, min(b * 128, ref.shape[1])) if (a, b) != (0, 0) else (0, ref.shape[1])
+                got[:, t0:t1, h:h + nh] = o[:, t0:t1, h:h + nh]
+        assert torch.equal(got, ref)
