@@ -7,15 +7,17 @@
 // of the group's tokens, run on tcgen05 straight from TMA-loaded K / V tiles (both
 // operands MN-major: Ht[n][k] = sum_t V[t][n] K[t][k]); the second (the exact centring
 // correction, rank 1 per block) is accumulated in fp32 on CUDA cores.  Per-block H_j is
-// never materialised.  One CTA per (head, group) -- or per 32-block
-// chunk of a group larger than 32 blocks, reduced afterwards in a fixed order --,
-// 2-stage (d = 128) / 4-stage (d = 64) TMA ring with two CTAs per SM, HBM bound:
+// never materialised.  Work item = (head, group), or a 32-block chunk of
+// a group larger than 32 blocks (reduced afterwards in a fixed order); a persistent CTA
+// per SM walks its items with one TMA ring (4 x 32 KB at d = 128) running across them and
+// two TMEM accumulators, so item i's epilogue overlaps item i+1's loads.  HBM bound:
 // 2 S d * 2 bytes per head.
 // d = 64: the MMA keeps M = 128 with the A operand's second 64-row half pointed at a
 // zeroed 8 KB region of the stage (rows 64..127 of the accumulator are 0 and unused).
 #include <cuda.h>
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "pasa_internal.h"
@@ -27,10 +29,9 @@ namespace {
 using namespace ptx;
 
 constexpr int kBk = 64;
-constexpr int kMaxStages = 4;
 constexpr int kBox = kBk * 128;             // 8 KB: 64 tokens x 64 dims (128-byte rows)
-constexpr int kMaxG = 32;                   // blocks per group handled by one CTA's smem
-constexpr int kThreads = 256;               // warp 0 TMA, warp 1 MMA, warps 4-7 math
+constexpr int kMaxG = 32;                   // blocks per work item (group or 32-block chunk)
+constexpr int kThreads = 384;               // warp 0 TMA, warp 1 MMA, 4-7 Vsum, 8-11 epilogue
 constexpr int kChunkBlocks = 32;
 
 template <int D>
@@ -39,8 +40,8 @@ struct SGeo {
     static constexpr int TILE = kBk * D * 2;            // one K or V block tile
     // stage: K tile | V tile | (d = 64) zero box for the A operand's padded rows
     static constexpr int STAGE = 2 * TILE + (D == 64 ? kBox : 0);
-    // ring depth per CTA: two CTAs per SM (one's epilogue overlaps the other's loads)
-    static constexpr int STAGES = D == 64 ? 4 : 2;
+    // ring depth across work items (one CTA per SM): 4 x 32 KB at d = 128, 6 x 24 KB at 64
+    static constexpr int STAGES = D == 64 ? 6 : 4;
 };
 
 struct Args {
@@ -52,49 +53,76 @@ struct Args {
     __nv_bfloat16* ht;        // [BH][NG][D][D]
     float* part;              // G > kMaxG: fp32 partial sums [BH][NC][D][D] of 32-block chunks
     int64_t NC;               // chunks per head (ceil(N_K / 32)) when part != nullptr
+    int64_t items_per_head;   // NG, or NC for chunked groups
+    int64_t items;            // BH * items_per_head
 };
 
+constexpr int kNVS = 4;                     // TMEM slots of the per-block Vsum MMA
+constexpr int kVsCols = 16;                 // N of the Vsum MMA (all columns equal)
+
 struct Ctl {
-    uint64_t full[kMaxStages], empty[kMaxStages], acc_full;
+    uint64_t full[8], empty[8];          // TMA ring
+    uint64_t vs_full[kNVS], vs_empty[kNVS];   // per-block Vsum in TMEM (MMA <-> Vsum warps)
+    uint64_t acc_full[2], acc_empty[2];  // TMEM accumulators (MMA <-> epilogue)
+    uint64_t scr_full[2], scr_empty[2];  // Vsum / Kbar scratch (Vsum warps <-> epilogue)
     uint32_t tmem_base;
 };
 template <int D>
-struct Scratch {              // dynamic smem after the TMA stages
-    float vsum[kMaxG][D];     // fp32 Vsum_j of the group's blocks
-    float kb[kMaxG][D];       // fp32 Kbar_j
-    float part[4][D];         // per-warp partial column sums
+struct Scratch {              // dynamic smem after the TMA stages, double-buffered per item
+    float vsum[2][kMaxG][D];  // fp32 Vsum_j of the item's blocks
+    float kb[2][kMaxG][D];    // fp32 Kbar_j
+    alignas(1024) __nv_bfloat16 ones[kVsCols][kBk];   // B operand of the Vsum MMA (2 KB)
 };
 
+// Persistent: one CTA per SM walks work items (head, group) = blockIdx.x, +gridDim.x, ...
+// (head-major).  The TMA ring runs across items, the MMA warp accumulates item i in TMEM
+// accumulator i & 1, and a separate epilogue warpgroup centres / stores item i while the
+// ring and the Vsum warps already work on item i + 1.
 template <int D>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, 1)
     kv_stats_sm100_kernel(const __grid_constant__ CUtensorMap tmK,
                           const __grid_constant__ CUtensorMap tmV, const Args a) {
     using G_ = SGeo<D>;
-    constexpr uint32_t kCols = D;             // accumulator columns (N = D)
+    constexpr uint32_t kCols = D;             // accumulator columns (N = D) per buffer
+    constexpr uint32_t kVsBase = 2 * kCols;   // Vsum slots after the two accumulators
+    constexpr uint32_t kTmemAlloc = D == 128 ? 512 : 256;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                                ~uintptr_t(1023));
     __shared__ Ctl ctl;
     Scratch<D>& sc = *reinterpret_cast<Scratch<D>*>(smem + G_::STAGES * G_::STAGE);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int64_t g = blockIdx.x, bh = blockIdx.y;
-    const int64_t b = bh / a.H, h = bh % a.H;
-    // one group per CTA (G <= kMaxG), or one 32-block chunk of a large group
-    const int64_t j0 = a.part ? g * kChunkBlocks : g * a.G;
-    const int nb = (int)min(a.part ? (int64_t)kChunkBlocks : (int64_t)a.G, a.NK - j0);
+    auto item_geo = [&](int64_t it, int64_t& bh, int64_t& g, int64_t& j0, int& nb) {
+        bh = it / a.items_per_head;
+        g = it % a.items_per_head;
+        j0 = a.part ? g * kChunkBlocks : g * a.G;
+        nb = (int)min(a.part ? (int64_t)kChunkBlocks : (int64_t)a.G, a.NK - j0);
+    };
 
     if (tid == 0) {
         for (int s = 0; s < G_::STAGES; ++s) {
             mbar_init(&ctl.full[s], 1);
-            mbar_init(&ctl.empty[s], 2);     // MMA commit + the math warpgroup
+            mbar_init(&ctl.empty[s], 1);     // MMA commit (both MMAs read the stage)
         }
-        mbar_init(&ctl.acc_full, 1);
+        for (int s = 0; s < kNVS; ++s) {
+            mbar_init(&ctl.vs_full[s], 1);
+            mbar_init(&ctl.vs_empty[s], 128);
+        }
+        for (int b2 = 0; b2 < 2; ++b2) {
+            mbar_init(&ctl.acc_full[b2], 1);
+            mbar_init(&ctl.acc_empty[b2], 1);
+            mbar_init(&ctl.scr_full[b2], 2);   // Vsum warpgroup + the Kbar loaders
+            mbar_init(&ctl.scr_empty[b2], 1);
+        }
         fence_barrier_init();
     }
     if (warp == 1) {
-        tmem_alloc(&ctl.tmem_base, kCols);
+        tmem_alloc(&ctl.tmem_base, kTmemAlloc);
         tmem_relinquish();
     }
+    for (int e = tid; e < kVsCols * kBk / 2; e += kThreads)   // bf16 ones (0x3F80 pairs)
+        reinterpret_cast<uint32_t*>(&sc.ones[0][0])[e] = 0x3F803F80u;
+    fence_proxy_async();                     // generic-proxy ones visible to the MMA
     if constexpr (D == 64) {                 // the zero boxes (never written by TMA)
         for (int e = tid; e < G_::STAGES * kBox / 16; e += kThreads) {
             const int s = e / (kBox / 16), w = e % (kBox / 16);
@@ -103,146 +131,197 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         fence_proxy_async();                 // generic-proxy zeros visible to the MMA
     }
-    // fp32 Kbar of the group (and its bf16 copy for the attention kernel)
-    for (int e = tid; e < nb * D; e += kThreads) {
-        const int jj = e / D, d = e % D;
-        const double kv = a.kbar[(bh * a.NK + j0 + jj) * D + d];
-        sc.kb[jj][d] = (float)kv;
-        a.kbar_lp[(bh * a.NK + j0 + jj) * D + d] = __float2bfloat16_rn((float)kv);
-    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = ctl.tmem_base;
 
     if (warp == 0) {
+        // ======================= TMA producer (ring across items) =======================
         if (lane == 0) {
-            for (int jj = 0; jj < nb; ++jj) {
-                const int s = jj % G_::STAGES;
-                mbar_wait_sleep(&ctl.empty[s], ((jj / G_::STAGES) & 1) ^ 1);
-                uint8_t* st = smem + s * G_::STAGE;
-                mbar_arrive_expect_tx(&ctl.full[s], 2 * G_::TILE);
-                const int tok = (int)((j0 + jj) * kBk);
+            int n = 0;
+            for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x) {
+                int64_t bh, g, j0;
+                int nb;
+                item_geo(it, bh, g, j0, nb);
+                const int b = (int)(bh / a.H), h = (int)(bh % a.H);
+                for (int jj = 0; jj < nb; ++jj, ++n) {
+                    const int s = n % G_::STAGES;
+                    mbar_wait_sleep(&ctl.empty[s], ((n / G_::STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + s * G_::STAGE;
+                    mbar_arrive_expect_tx(&ctl.full[s], 2 * G_::TILE);
+                    const int tok = (int)((j0 + jj) * kBk);
 #pragma unroll
-                for (int bx = 0; bx < G_::NBOX; ++bx) {
-                    tma_load_4d(st + bx * kBox, &tmK, &ctl.full[s], 64 * bx, tok, (int)h, (int)b);
-                    tma_load_4d(st + G_::TILE + bx * kBox, &tmV, &ctl.full[s], 64 * bx, tok,
-                                (int)h, (int)b);
+                    for (int bx = 0; bx < G_::NBOX; ++bx) {
+                        tma_load_4d(st + bx * kBox, &tmK, &ctl.full[s], 64 * bx, tok, h, b);
+                        tma_load_4d(st + G_::TILE + bx * kBox, &tmV, &ctl.full[s], 64 * bx, tok, h,
+                                    b);
+                    }
                 }
             }
         }
         __syncwarp();
     } else if (warp == 1) {
+        // ======================= MMA issuer =======================
         // Ht[n][k] += sum_t V[t][n] K[t][k]:  A = V^T (M = n, MN-major), B = K (N = k, MN-major)
         // d = 64: A rows 64..127 come from the zero box one LBO (8 KB) after the V tile
         constexpr uint32_t kId = idesc_bf16_f32(128, D, 1, 1);
+        // Vsum_j[n] = sum_t V[t][n] * 1: A = V^T as above, B = ones (N = 16, K-major)
+        constexpr uint32_t kIdVs = idesc_bf16_f32(128, kVsCols, 1, 0);
         const uint64_t d0 = umma_desc_sw128(smem_u32(smem), kBox, 1024);
-        for (int jj = 0; jj < nb; ++jj) {
-            const int s = jj % G_::STAGES;
-            mbar_wait_sleep(&ctl.full[s], (jj / G_::STAGES) & 1);
+        const uint64_t d1 = umma_desc_sw128(smem_u32(&sc.ones[0][0]), 16, 1024);
+        int n = 0, li = 0;
+        for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x, ++li) {
+            int64_t bh, g, j0;
+            int nb;
+            item_geo(it, bh, g, j0, nb);
+            const int ab = li & 1;
+            mbar_wait_sleep(&ctl.acc_empty[ab], ((li >> 1) & 1) ^ 1);   // epilogue of li - 2
             tc_fence_after();
-            if (lane == 0) {
+            const uint32_t acc = tbase + ab * kCols;
+            for (int jj = 0; jj < nb; ++jj, ++n) {
+                const int s = n % G_::STAGES, vs = n % kNVS;
+                mbar_wait_sleep(&ctl.full[s], (n / G_::STAGES) & 1);
+                mbar_wait_sleep(&ctl.vs_empty[vs], ((n / kNVS) & 1) ^ 1);
+                tc_fence_after();
+                if (lane == 0) {
 #pragma unroll
-                for (int kk = 0; kk < kBk / 16; ++kk) {
-                    const uint32_t offk = ((uint32_t)s * G_::STAGE + kk * 2048) >> 4;
-                    const uint32_t offv = ((uint32_t)s * G_::STAGE + G_::TILE + kk * 2048) >> 4;
-                    mma_ss(tbase, d0 + offv, d0 + offk, kId, (jj > 0 || kk > 0) ? 1u : 0u);
+                    for (int kk = 0; kk < kBk / 16; ++kk) {
+                        const uint32_t offk = ((uint32_t)s * G_::STAGE + kk * 2048) >> 4;
+                        const uint32_t offv = ((uint32_t)s * G_::STAGE + G_::TILE + kk * 2048) >> 4;
+                        mma_ss(acc, d0 + offv, d0 + offk, kId, (jj > 0 || kk > 0) ? 1u : 0u);
+                        mma_ss(tbase + kVsBase + vs * kVsCols, d0 + offv, d1 + ((kk * 32) >> 4),
+                               kIdVs, kk > 0 ? 1u : 0u);
+                    }
+                    mma_commit(&ctl.empty[s]);
+                    mma_commit(&ctl.vs_full[vs]);
+                    if (jj == nb - 1) mma_commit(&ctl.acc_full[ab]);
                 }
-                mma_commit(&ctl.empty[s]);
-                if (jj == nb - 1) mma_commit(&ctl.acc_full);
+                __syncwarp();
             }
-            __syncwarp();
         }
-    } else if (warp >= 4) {
-        // Vsum_j: thread t sums 8 consecutive dims (one 16-byte chunk) over RPT rows
-        constexpr int CH = D / 8;                // 16-byte chunks per row
-        constexpr int RG = 128 / CH;             // row groups
-        constexpr int RPT = kBk / RG;            // rows per thread
-        const int mt = tid - 128;                // 0..127
-        const int chunk = mt % CH;
-        const int rg = mt / CH;
-        const int bx = chunk >> 3, c16 = chunk & 7;
-        for (int jj = 0; jj < nb; ++jj) {
-            const int s = jj % G_::STAGES;
-            mbar_wait_sleep(&ctl.full[s], (jj / G_::STAGES) & 1);
-            const uint8_t* vt = smem + s * G_::STAGE + G_::TILE + bx * kBox;
-            float acc[8];
+    } else if (warp == 2 || warp == 3) {
+        // ============ Kbar_j of each item: fp32 copy for the epilogue, bf16 copy out ============
+        // (independent loads batched 16 deep: the fp64 means come from L2 / HBM)
+        const int lt = tid - 64;                 // 0..63
+        int li = 0;
+        for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x, ++li) {
+            int64_t bh, g, j0;
+            int nb;
+            item_geo(it, bh, g, j0, nb);
+            const int sb = li & 1;
+            mbar_wait_sleep(&ctl.scr_empty[sb], ((li >> 1) & 1) ^ 1);   // epilogue of li - 2
+            const double* src = a.kbar + (bh * a.NK + j0) * D;
+            __nv_bfloat16* dst = a.kbar_lp + (bh * a.NK + j0) * D;
+            float* kbs = &sc.kb[sb][0][0];
+            const int ne = nb * D;
+            for (int e0 = lt; e0 < ne; e0 += 64 * 16) {
+                double v[16];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-#pragma unroll
-            for (int rr = 0; rr < RPT; ++rr) {
-                const int t = rg * RPT + rr;
-                const uint4 u = *reinterpret_cast<const uint4*>(vt + t * 128 + ((c16 ^ (t & 7)) << 4));
-                const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(v2[e]);
-                    acc[2 * e] += f.x;
-                    acc[2 * e + 1] += f.y;
+                for (int u = 0; u < 16; ++u) {
+                    const int e = e0 + 64 * u;
+                    v[u] = e < ne ? __ldg(src + e) : 0.0;
                 }
-            }
-            // reduce the row groups of this warp (lanes with equal chunk), then smem
 #pragma unroll
-            for (int o = CH; o < 32; o <<= 1)
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-            if (lane < CH) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) sc.part[warp - 4][chunk * 8 + e] = acc[e];
-            }
-            bar_sync(1, 128);
-            if (mt == 0) mbar_arrive(&ctl.empty[s]);   // this warpgroup is done with the stage
-            if (mt < D) {
-                const int d = mt;
-                const float vs = sc.part[0][d] + sc.part[1][d] + sc.part[2][d] + sc.part[3][d];
-                sc.vsum[jj][d] = vs;
-                a.vsum_lp[(bh * a.NK + j0 + jj) * D + d] = __float2bfloat16_rn(vs);
-            }
-            bar_sync(1, 128);
-        }
-        // epilogue: thread n (n < D) owns row n of Ht (TMEM lane n)
-        mbar_wait_sleep(&ctl.acc_full, 0);
-        tc_fence_after();
-        const int n = mt;
-        const uint32_t t_row = tbase + ((uint32_t)((warp & 3) * 32) << 16);
-        const float inv = 1.f / (float)nb;
-        if (warp - 4 < D / 32) {                      // warps holding lanes 0..D-1
-            __nv_bfloat16* out = a.ht + ((bh * a.NG + g) * D + n) * D;
-            float* pout = a.part ? a.part + ((bh * a.NC + g) * D + n) * D : nullptr;
-#pragma unroll 1
-            for (int c0 = 0; c0 < D; c0 += 32) {
-                uint32_t raw[32];
-                tmem_ld32(t_row + c0, raw);
-                tmem_wait_ld();
-                float acc[32];
-#pragma unroll
-                for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(raw[c]);
-                // exact centring: subtract sum_j Vsum_j[n] Kbar_j[k]
-                for (int jj = 0; jj < nb; ++jj) {
-                    const float vs = sc.vsum[jj][n];
-                    const float4* kb4 = reinterpret_cast<const float4*>(&sc.kb[jj][c0]);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float4 kv = kb4[c];
-                        acc[4 * c + 0] = fmaf(-vs, kv.x, acc[4 * c + 0]);
-                        acc[4 * c + 1] = fmaf(-vs, kv.y, acc[4 * c + 1]);
-                        acc[4 * c + 2] = fmaf(-vs, kv.z, acc[4 * c + 2]);
-                        acc[4 * c + 3] = fmaf(-vs, kv.w, acc[4 * c + 3]);
+                for (int u = 0; u < 16; ++u) {
+                    const int e = e0 + 64 * u;
+                    if (e < ne) {
+                        kbs[e] = (float)v[u];
+                        dst[e] = __float2bfloat16_rn((float)v[u]);
                     }
                 }
-                if (pout) {                       // partial sum of the chunk (fp32)
-#pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        reinterpret_cast<float4*>(pout + c0)[q] =
-                            make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
-                    continue;
+            }
+            bar_sync(3, 64);
+            if (lt == 0) mbar_arrive(&ctl.scr_full[sb]);
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ============ Vsum_j (and the item's fp32 / bf16 Kbar) per block ============
+        // thread mt = TMEM lane mt = head dim n: Vsum_j[n] from the Vsum MMA's slot
+        const int mt = tid - 128;                // 0..127
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        int n = 0, li = 0;
+        for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x, ++li) {
+            int64_t bh, g, j0;
+            int nb;
+            item_geo(it, bh, g, j0, nb);
+            const int sb = li & 1;
+            mbar_wait_sleep(&ctl.scr_empty[sb], ((li >> 1) & 1) ^ 1);   // epilogue of li - 2
+            for (int jj = 0; jj < nb; ++jj, ++n) {
+                const int vs = n % kNVS;
+                mbar_wait_sleep(&ctl.vs_full[vs], (n / kNVS) & 1);
+                tc_fence_after();
+                const float v = __uint_as_float(tmem_ld1(tbase + lane_off + kVsBase + vs * kVsCols));
+                tmem_wait_ld();
+                tc_fence_before();
+                mbar_arrive(&ctl.vs_empty[vs]);
+                if (mt < D) {
+                    sc.vsum[sb][jj][mt] = v;
+                    a.vsum_lp[(bh * a.NK + j0 + jj) * D + mt] = __float2bfloat16_rn(v);
                 }
-                uint4 pk[4];
-                uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+            }
+            bar_sync(1, 128);                    // every thread's vsum / kb entries written
+            if (mt == 0) mbar_arrive(&ctl.scr_full[sb]);   // vsum / kb of the item complete
+        }
+    } else if (warp >= 8) {
+        // ============ epilogue: thread n (n < D) owns row n of Ht (TMEM lane n) ============
+        const int n = tid - 256;                     // 0..127
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        int li = 0;
+        for (int64_t it = blockIdx.x; it < a.items; it += gridDim.x, ++li) {
+            int64_t bh, g, j0;
+            int nb;
+            item_geo(it, bh, g, j0, nb);
+            const int ab = li & 1;
+            mbar_wait_sleep(&ctl.acc_full[ab], (li >> 1) & 1);
+            mbar_wait_sleep(&ctl.scr_full[ab], (li >> 1) & 1);
+            tc_fence_after();
+            const uint32_t t_row = tbase + lane_off + ab * kCols;
+            const float inv = 1.f / (float)nb;
+            if (n < D) {
+                __nv_bfloat16* out = a.ht + ((bh * a.NG + g) * D + n) * D;
+                float* pout = a.part ? a.part + ((bh * a.NC + g) * D + n) * D : nullptr;
+#pragma unroll 1
+                for (int c0 = 0; c0 < D; c0 += 32) {
+                    uint32_t raw[32];
+                    tmem_ld32(t_row + c0, raw);
+                    tmem_wait_ld();
+                    float acc[32];
 #pragma unroll
-                for (int c = 0; c < 16; ++c) pw[c] = pack_bf16(acc[2 * c] * inv, acc[2 * c + 1] * inv);
+                    for (int c = 0; c < 32; ++c) acc[c] = __uint_as_float(raw[c]);
+                    // exact centring: subtract sum_j Vsum_j[n] Kbar_j[k]
+                    for (int jj = 0; jj < nb; ++jj) {
+                        const float vs = sc.vsum[ab][jj][n];
+                        const float4* kb4 = reinterpret_cast<const float4*>(&sc.kb[ab][jj][c0]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(out + c0)[q] = pk[q];
+                        for (int c = 0; c < 8; ++c) {
+                            const float4 kv = kb4[c];
+                            acc[4 * c + 0] = fmaf(-vs, kv.x, acc[4 * c + 0]);
+                            acc[4 * c + 1] = fmaf(-vs, kv.y, acc[4 * c + 1]);
+                            acc[4 * c + 2] = fmaf(-vs, kv.z, acc[4 * c + 2]);
+                            acc[4 * c + 3] = fmaf(-vs, kv.w, acc[4 * c + 3]);
+                        }
+                    }
+                    if (pout) {                       // partial sum of the chunk (fp32)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            reinterpret_cast<float4*>(pout + c0)[q] =
+                                make_float4(acc[4 * q], acc[4 * q + 1], acc[4 * q + 2], acc[4 * q + 3]);
+                        continue;
+                    }
+                    uint4 pk[4];
+                    uint32_t* pw = reinterpret_cast<uint32_t*>(pk);
+#pragma unroll
+                    for (int c = 0; c < 16; ++c)
+                        pw[c] = pack_bf16(acc[2 * c] * inv, acc[2 * c + 1] * inv);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) reinterpret_cast<uint4*>(out + c0)[q] = pk[q];
+                }
+            }
+            tc_fence_before();
+            bar_sync(2, 128);
+            if (n == 0) {
+                mbar_arrive(&ctl.acc_empty[ab]);
+                mbar_arrive(&ctl.scr_empty[ab]);
             }
         }
     }
@@ -250,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc(tbase, kCols);
+        tmem_dealloc(tbase, kTmemAlloc);
     }
 }
 
@@ -291,11 +370,20 @@ cudaError_t launch_d(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r
     const bool chunked = r->cfg.G > kMaxG;
     a.part = chunked ? r->part : nullptr;
     a.NC = (r->NK + kChunkBlocks - 1) / kChunkBlocks;
+    a.items_per_head = chunked ? a.NC : r->NG;
+    a.items = r->BH * a.items_per_head;
     const size_t smem = (size_t)SGeo<D>::STAGES * SGeo<D>::STAGE + sizeof(Scratch<D>) + 1024;
     auto kern = kv_stats_sm100_kernel<D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid((unsigned)(chunked ? a.NC : r->NG), (unsigned)r->BH);
+    static int n_sm = 0;
+    if (n_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+        if (n_sm <= 0) n_sm = 148;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(a.items, n_sm);
     kern<<<grid, kThreads, smem, st>>>(mK, mV, a);
     *launches += 1;
     if (chunked) {
