@@ -62,7 +62,9 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
     if (c->prior != PASA_PRIOR_NONE && !(c->eps > 0.0 && std::isfinite(c->eps)))
         return fail(PASA_EINVAL, "prior eps must be finite and > 0");
     const int64_t NK = (S + c->Bk - 1) / c->Bk;
-    if (NK > 2048) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 2048 (S too long)", (long long)NK);
+    // the tensor-core attention kernels' op list holds 4096 kept blocks (S <= 262,144 at
+    // Bk = 64); the route has no limit of its own
+    if (NK > 4096) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 4096 (S too long)", (long long)NK);
     const int64_t NQ = (S + c->Bq - 1) / c->Bq;
     if ((c->qb_begin != 0 || c->qb_end != 0) &&
         !(c->qb_begin >= 0 && c->qb_begin < c->qb_end && c->qb_end <= NQ))

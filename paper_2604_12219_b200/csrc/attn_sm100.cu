@@ -35,14 +35,19 @@ using namespace ptx;
 
 constexpr int kThreads = 256;
 constexpr int kBQ = 128, kBK = 64;
-constexpr int kMaxOps = 2048 + 32 + 64 + 64;
+// op list: kept blocks (<= N_K <= 4096) + centroid chunks (<= 64) + first-order ops
+// (<= N_K / 8 for G >= 8) + slack; 16-bit entries (type in the top 2 bits)
+constexpr int kMaxNK = 4096;
+constexpr int kMaxOps = kMaxNK + kMaxNK / 64 + kMaxNK / 8 + 64;
 constexpr int kTmemCols = 256;
 constexpr float kRescaleThresh = 8.f; // log2 units
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
-__device__ __forceinline__ int32_t op_make(int32_t type, int32_t v) { return (type << 24) | v; }
-__device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 24; }
-__device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0xFFFFFF; }
+__device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
+    return (uint16_t)((type << 14) | v);
+}
+__device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 14; }
+__device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0x3FFF; }
 
 // NB = S/P/Aq buffers in TMEM = K ring slots: 2 at d = 128 (TMEM: O 128 + 2 x 64
 // columns), 3 at d = 64 (O 64 + 3 x 64) -- QK of op n+NB-1 is issued before PV of op n.
@@ -99,8 +104,8 @@ struct Ctl {
     uint64_t p_full[3], pv_done[2];
     uint32_t tmem_base;
     int32_t nops;
-    uint32_t mask[64];
-    int32_t ops[kMaxOps];
+    uint32_t mask[kMaxNK / 32];
+    uint16_t ops[kMaxOps];
 };
 // EXP 1 (groups of 8 or 16 blocks): the 8-column P sums of the last C op, per row
 struct CtlSG : Ctl {
@@ -342,7 +347,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint8_t* qrow = smem + G_::OFF_Q;
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
-        int g_cur = -1, g_done = -1;          // 32-bit group bookkeeping (N_K <= 2048)
+        int g_cur = -1, g_done = -1;          // group of the running / last closed A sum
         const int G32 = (int)p.G, NK32 = (int)NK;
         int c_last = 0;   // G = 8 or 16: chunk of the last C op (ctl.sg holds its group sums)
         int sc0 = 0, sc1 = 0, sc2 = 0;   // S-type ops seen per S buffer (s_full parity)
@@ -671,8 +676,8 @@ cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const 
                  "multiples of 128, >= N_K)", r->cfg.G);
         return cudaErrorNotSupported;
     }
-    if (r->W > 64) {
-        snprintf(why, why_len, "N_K > 2048");
+    if (r->NK > kMaxNK) {
+        snprintf(why, why_len, "N_K > %d", kMaxNK);
         return cudaErrorNotSupported;
     }
     cudaError_t e = r->D == 128 ? launch_d<128>(q, k, v, r, out, st, why, why_len)

@@ -38,14 +38,19 @@ using namespace ptx;
 
 constexpr int kThreads = 384;
 constexpr int kBQ = 256, kBK = 64, kTile = 128;
-constexpr int kMaxOps = 2048 + 32 + 64 + 64;
+// op list: kept blocks (<= N_K <= 4096) + centroid chunks (<= 64) + first-order ops
+// (<= N_K / 8 for G >= 8) + slack; 16-bit entries (type in the top 2 bits)
+constexpr int kMaxNK = 4096;
+constexpr int kMaxOps = kMaxNK + kMaxNK / 64 + kMaxNK / 8 + 64;
 constexpr int kTmemCols = 512;
 constexpr float kRescaleThresh = 8.f;   // log2 units
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
-__device__ __forceinline__ int32_t op_make(int32_t type, int32_t v) { return (type << 24) | v; }
-__device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 24; }
-__device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0xFFFFFF; }
+__device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
+    return (uint16_t)((type << 14) | v);
+}
+__device__ __forceinline__ int32_t op_type(int32_t op) { return op >> 14; }
+__device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0x3FFF; }
 
 template <int D>
 struct Geo {
@@ -84,8 +89,8 @@ struct Ctl {
     uint64_t pv_done[2][2];             // [tile][n & 1]: the tile's O-MMA of the op done
     uint32_t tmem_base;
     int32_t nops;
-    uint32_t mask[64];
-    int32_t ops[kMaxOps];
+    uint32_t mask[kMaxNK / 32];
+    uint16_t ops[kMaxOps];
 };
 
 template <int D>
@@ -537,7 +542,7 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
 }  // namespace
 
 bool attn_sm100_q256_supported(const pasa_route_s* r) {
-    return r->cfg.Bq == kBQ && r->cfg.Bk == kBK && (r->D == 128 || r->D == 64) && r->W <= 64 &&
+    return r->cfg.Bq == kBQ && r->cfg.Bk == kBK && (r->D == 128 || r->D == 64) && r->NK <= kMaxNK &&
            (r->cfg.comp != PASA_COMP_GROUPED || r->cfg.G == 32 || r->cfg.G == 64 ||
             r->cfg.G % 128 == 0 || r->cfg.G >= r->NK);   // the attn_sm100.cu group set minus 8, 16
 }
@@ -546,7 +551,7 @@ cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, c
                                    pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                                    int* launches, char* why, size_t why_len) {
     if (!attn_sm100_q256_supported(r)) {
-        snprintf(why, why_len, "Bq = 256 kernel: needs Bk=64, d in {64, 128}, N_K <= 2048, "
+        snprintf(why, why_len, "Bq = 256 kernel: needs Bk=64, d in {64, 128}, N_K <= 4096, "
                  "G in {32, 64, multiples of 128, >= N_K} for grouped compensation");
         return cudaErrorNotSupported;
     }

@@ -67,7 +67,9 @@ def test_route_workspace_validation(L):
         assert L.pasa_route_workspace_bytes(ctypes.byref(bad), 1, 4096, 4, 128) == 0, why
         assert L.pasa_last_error()
     assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 4096, 4, 96) == 0
-    assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 64 * 2049, 4, 128) == 0
+    # N_K <= 4096 (S <= 262,144 at Bk = 64): the attention kernels' op-list capacity
+    assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 64 * 4096, 4, 128) > 0
+    assert L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 64 * 4097, 4, 128) == 0
 
 
 def test_prior_workspace_validation(L):

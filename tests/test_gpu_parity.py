@@ -504,3 +504,22 @@ def test_full_config_q256_sampled(pasa, parity_log):
                         log=parity_log, label="wan14b_720p Bq=256 full size, 4 heads x 16 q-blocks")
     assert bool(torch.isfinite(out).all())
     assert torch.equal(out, pasa.attn(q, k, v, route))
+
+
+def test_long_sequence_200k_route_and_attention(pasa, parity_log):
+    """S = 200,000 tokens (N_K = 3,125 > the 2,048 of round 1): the fused
+    route keeps its score rows in the workspace scratch (they no longer fit on chip) and the
+    tensor-core attention walks a 16-bit op list of up to 4,096 kept blocks.  Route against
+    the oracle on every q-block, attention on 16 q-blocks incl. the first and ragged last;
+    and a dense step (k = N_K = 3,125 kept blocks) on 4 q-blocks."""
+    B, S, H, D = 1, 200_000, 1, 128
+    q, k, v = synth.iid_qkv(B, S, H, D, seed=1010, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=128, G=32, beta=0.1)
+    route, got, ties = check_route(pasa, q, k, cfg, 0.15, seed=pasa.layer_seed(42, 0), step=25)
+    assert route.NK == 3125 and ties <= 2
+    check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs([0], route.NQ, 16), log=parity_log,
+               label="S = 200,000 (N_K = 3,125)")
+    route_d, got_d, _ = check_route(pasa, q, k, cfg, 1.0, seed=pasa.layer_seed(42, 0), step=25)
+    assert got_d["k"] == 3125
+    check_attn(pasa, q, k, v, route_d, got_d, cfg, pairs=_pairs([0], route_d.NQ, 4),
+               log=parity_log, label="S = 200,000 dense step (3,125 kept blocks)")
