@@ -72,6 +72,9 @@ def parse(argv=None):
     ap.add_argument("--ulysses-chunks", type=int, default=0,
                     help="head groups of the sequence-sharded Ulysses all-to-all (attention on "
                          "arrived heads overlaps the rest; 0 = auto, up to 4)")
+    ap.add_argument("--qk-precision", default="bf16", choices=["bf16", "fp8"],
+                    help="fp8: the opt-in FP8 QK^T variant (SURVEY.md §8f NEXT 4; its own "
+                         "tolerance; never the headline configuration)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1.  gloo is a debug mode: ranks may "
                          "share one GPU (device = local_rank %% device_count) and every "
@@ -364,7 +367,8 @@ def run_pasa(args):
 
     def rcfg_for(h, a=0, b=0):
         return P.RouteCfg(Bq=cfg["Bq"], Bk=cfg["Bk"], G=cfg["G"], comp="grouped", beta=0.1,
-                          H_total=H, head_offset=h, prior=args.prior, qb_begin=a, qb_end=b)
+                          H_total=H, head_offset=h, prior=args.prior, qb_begin=a, qb_end=b,
+                          qk_precision=args.qk_precision)
 
     rcfg = rcfg_for(off)
     if seq_sharded:
@@ -726,7 +730,8 @@ def run_pasa(args):
                                                   "meaningful)" if gloo else "")) if world > 1
             else None,
             "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
-            "step_t": t_step, "budget": args.budget, "prior": args.prior, "l1": rec["l1"], "alpha": rec["alpha"],
+            "step_t": t_step, "budget": args.budget, "prior": args.prior,
+            "qk_precision": args.qk_precision, "l1": rec["l1"], "alpha": rec["alpha"],
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",

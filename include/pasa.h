@@ -109,6 +109,16 @@ typedef struct {
                               * divide the GPU count: K/V statistics still cover whole heads,
                               * Philox keys on the global block index i, and rows outside the
                               * range of idx / count / mask / out are not written.            */
+    int32_t qk_fp8;          /* 1 = opt-in precision variant (reading R-30):
+                              * QK^T of kept blocks and the centroid logits run on the FP8 tensor
+                              * cores (E4M3 x E4M3 -> f32).  pasa_route also writes E4M3 copies of
+                              * Q (one scale per token row) and K (one per 64-token block), the
+                              * statistics pass an E4M3 Kbar (one scale per head); PV and the
+                              * first-order term stay bf16.  bf16 I/O, D = 128, Bq = 128, G >= 32
+                              * only (else EUNSUPPORTED).  Its own tolerance: 1e-1 max|O| (the
+                              * E4M3 rounding alone gives ~5e-2); never the
+                              * north-star configuration.  0 = bf16 everywhere (default).     */
+    int32_t _pad2;
 } pasa_route_cfg;
 
 typedef struct pasa_budget_s* pasa_budget_h;

@@ -61,7 +61,8 @@ class PasaRouteCfg(ctypes.Structure):
                 ("comp", ctypes.c_int32), ("beta", ctypes.c_double),
                 ("H_total", ctypes.c_int64), ("head_offset", ctypes.c_int64),
                 ("prior", ctypes.c_int32), ("_pad", ctypes.c_int32), ("eps", ctypes.c_double),
-                ("qb_begin", ctypes.c_int32), ("qb_end", ctypes.c_int32)]
+                ("qb_begin", ctypes.c_int32), ("qb_end", ctypes.c_int32),
+                ("qk_fp8", ctypes.c_int32), ("_pad2", ctypes.c_int32)]
 
 
 class PasaError(RuntimeError):

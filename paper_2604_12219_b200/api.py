@@ -148,11 +148,13 @@ class RouteCfg:
     eps: float = 1e-6
     qb_begin: int = 0            # query blocks [qb_begin, qb_end) only; (0, 0) = all
     qb_end: int = 0              # (flattened (head, q-block) partition)
+    qk_precision: str = "bf16"   # "fp8": opt-in FP8 QK^T variant (NEXT 4, R-30; own tolerance)
 
     def to_c(self, H: int) -> _C.PasaRouteCfg:
         return _C.PasaRouteCfg(self.Bq, self.Bk, self.G, _C.COMP[self.comp], self.beta,
                                self.H_total if self.H_total is not None else H, self.head_offset,
-                               _C.PRIOR[self.prior], 0, self.eps, self.qb_begin, self.qb_end)
+                               _C.PRIOR[self.prior], 0, self.eps, self.qb_begin, self.qb_end,
+                               {"bf16": 0, "fp8": 1}[self.qk_precision], 0)
 
 
 class Route:

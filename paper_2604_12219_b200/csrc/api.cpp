@@ -39,7 +39,7 @@ inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
 struct RouteLayout {
     int64_t NQ, NK, NG, W, BH;
-    size_t off_hdr, off_qbar, off_kbar, off_kfrag, off_scores, off_kbar_lp, off_vsum, off_ht, off_idx,
+    size_t off_hdr, off_qbar, off_kbar, off_kfrag, off_q8, off_k8, off_sq8, off_kb8, off_kamax, off_scores, off_kbar_lp, off_vsum, off_ht, off_idx,
         off_count, off_mask, off_het, off_prior, off_hj, off_hgs, off_hglob, off_part, total;
 };
 
@@ -65,6 +65,9 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
     // the tensor-core attention kernels' op list holds 4096 kept blocks (S <= 262,144 at
     // Bk = 64); the route has no limit of its own
     if (NK > 4096) return fail(PASA_EUNSUPPORTED, "N_K=%lld > 4096 (S too long)", (long long)NK);
+    if (c->qk_fp8 != 0 && c->qk_fp8 != 1) return fail(PASA_EINVAL, "qk_fp8=%d", c->qk_fp8);
+    if (c->qk_fp8 && (D != 128 || c->Bq != 128 || (c->comp == PASA_COMP_GROUPED && c->G < 32)))
+        return fail(PASA_EUNSUPPORTED, "qk_fp8 needs D = 128, Bq = 128 and G >= 32");
     const int64_t NQ = (S + c->Bq - 1) / c->Bq;
     if ((c->qb_begin != 0 || c->qb_end != 0) &&
         !(c->qb_begin >= 0 && c->qb_begin < c->qb_end && c->qb_end <= NQ))
@@ -85,6 +88,12 @@ RouteLayout layout(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, int
     L.off_qbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NQ * D);
     L.off_kbar = o;     o = align_up(o + sizeof(double) * L.BH * L.NK * D);
     L.off_kfrag = o;    o = align_up(o + sizeof(double) * L.BH * ((L.NK + 7) / 8) * 8 * D);
+    const bool f8 = c->qk_fp8 != 0;   // FP8 QK^T variant: E4M3 copies and scales
+    L.off_q8 = o;       o = align_up(o + (f8 ? (size_t)L.BH * S * D : 0));
+    L.off_k8 = o;       o = align_up(o + (f8 ? (size_t)L.BH * S * D : 0));
+    L.off_sq8 = o;      o = align_up(o + (f8 ? sizeof(float) * L.BH * S : 0));
+    L.off_kb8 = o;      o = align_up(o + (f8 ? (size_t)L.BH * L.NK * D : 0));
+    L.off_kamax = o;    o = align_up(o + (f8 ? sizeof(uint32_t) * 2 * L.BH : 0));
     // fp64 score rows: on chip (shared memory) unless a row tile does not fit there
     const bool gsc = pasa::route_rows_per_cta(L.NK, D) == 0;
     L.off_scores = o;   o = align_up(o + (gsc ? sizeof(double) * L.BH * L.NQ * pasa::route_score_stride(L.NK) : 0));
@@ -276,6 +285,13 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
     r->kbar = reinterpret_cast<double*>(w + L.off_kbar);
     r->kfrag = reinterpret_cast<double*>(w + L.off_kfrag);
+    const bool f8 = cfg->qk_fp8 != 0;
+    r->q8 = f8 ? reinterpret_cast<uint8_t*>(w + L.off_q8) : nullptr;
+    r->k8 = f8 ? reinterpret_cast<uint8_t*>(w + L.off_k8) : nullptr;
+    r->sq8 = f8 ? reinterpret_cast<float*>(w + L.off_sq8) : nullptr;
+    r->kb8 = f8 ? reinterpret_cast<uint8_t*>(w + L.off_kb8) : nullptr;
+    r->kamax = f8 ? reinterpret_cast<uint32_t*>(w + L.off_kamax) : nullptr;
+    r->kbamax = f8 ? r->kamax + L.BH : nullptr;
     r->scores = pasa::route_rows_per_cta(L.NK, D) == 0 ? reinterpret_cast<double*>(w + L.off_scores)
                                                         : nullptr;
     r->kbar_lp = w + L.off_kbar_lp;
@@ -382,6 +398,8 @@ pasa_status route_common(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     if ((st = check_tensor(q, "q")) != PASA_OK) return st;
     if ((st = check_tensor(k, "k")) != PASA_OK) return st;
     if (q->dtype != k->dtype) return fail(PASA_EDTYPE, "q and k dtypes differ");
+    if (route->cfg.qk_fp8 && q->dtype != PASA_BF16)
+        return fail(PASA_EUNSUPPORTED, "qk_fp8 needs bf16 q and k");
     if ((st = match_route(q, route, "q")) != PASA_OK) return st;
     if ((st = match_route(k, route, "k")) != PASA_OK) return st;
     if (v) {
@@ -436,6 +454,9 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route)");
     if (flags & ~(PASA_ATTN_FORCE_SIMT | PASA_ATTN_STATS_ONLY | PASA_ATTN_REUSE_STATS))
         return fail(PASA_EINVAL, "unknown pasa_attn_ex flags 0x%x", flags);
+    if (route->cfg.qk_fp8 && (q->dtype != PASA_BF16 || (flags & PASA_ATTN_FORCE_SIMT) ||
+                              !pasa::kv_stats_sm100_supported(route)))
+        return fail(PASA_EUNSUPPORTED, "qk_fp8 runs only the bf16 tensor-core path");
     int launches = 0;
     cudaStream_t s = (cudaStream_t)stream;
     if (!(flags & PASA_ATTN_REUSE_STATS)) {
@@ -469,6 +490,7 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     const bool fine_groups = c.comp == PASA_COMP_GROUPED && !pasa::sm100_supports_group(c.G, route->NK);
     const bool simt = q->dtype == PASA_F32 || (flags & PASA_ATTN_FORCE_SIMT) || c.Bq != 128 ||
                       fine_groups;
+
     if (simt) {
         e = pasa::launch_attn_simt(*q, *k, *v, route, *out, s, &launches);
     } else {

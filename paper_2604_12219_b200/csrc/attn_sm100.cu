@@ -78,6 +78,11 @@ struct Params {
     const uint32_t* mask;
     __nv_bfloat16* out;
     int64_t osB, osS, osH;
+    // FP8 QK^T variant (cfg.qk_fp8): per-row Q scales [BH][S]; per-head max |K| and
+    // max |Kbar| (float bits) [BH] each
+    const float* sq;
+    const uint32_t* kamax;
+    const uint32_t* kbamax;
     unsigned long long* trace;   // diagnostics: clock64 timeline of one CTA, or nullptr
     int32_t trace_x, trace_y;
     int32_t dbg;                 // diagnostics ablations (see pasa_debug_flags)
@@ -114,7 +119,10 @@ struct CtlSG : Ctl {
 
 // DIAG: diagnostics build (trace points, ablation flags, polling waits); the
 // production instantiation compiles all of it out
-template <int D, bool DIAG, int EXP>
+// F8: QK^T of kept blocks and the centroid logits on the FP8 tensor cores (E4M3 Q / K /
+// Kbar tiles from the route's and the statistics pass's FP8 copies, scales folded into
+// the per-op softmax scale), PV and the first-order op stay bf16 (d = 128 only)
+template <int D, bool DIAG, int EXP, bool F8 = false>
 __global__ void __launch_bounds__(kThreads, 2)
     attn_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                       const __grid_constant__ CUtensorMap tmK,
@@ -205,11 +213,16 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == 0) {
         // ======================= K-ring producer =======================
         if (lane == 0) {
-            mbar_arrive_expect_tx(&ctl.q_full, kBQ * D * 2);
+            if constexpr (F8) {
+                mbar_arrive_expect_tx(&ctl.q_full, kBQ * D);
+                tma_load_3d(smem + G_::OFF_Q, &tmQ, &ctl.q_full, 0, (int)(i * kBQ), (int)bh);
+            } else {
+                mbar_arrive_expect_tx(&ctl.q_full, kBQ * D * 2);
 #pragma unroll
-            for (int a = 0; a < G_::NBOX; ++a)
-                tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
-                            (int)(i * kBQ), (int)h, (int)b);
+                for (int a = 0; a < G_::NBOX; ++a)
+                    tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
+                                (int)(i * kBQ), (int)h, (int)b);
+            }
             for (int n = 0; n < nops; ++n) {
                 const int s = n % G_::NB;
                 mbar_wait_sleep(&ctl.k_empty[s], ((n / G_::NB) & 1) ^ 1);
@@ -221,6 +234,10 @@ __global__ void __launch_bounds__(kThreads, 2)
                 } else if (op_type(op) == OP_F) {
                     mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
                     tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
+                } else if constexpr (F8) {   // E4M3 K tile or Kbar chunk: 64 rows x 128 B
+                    mbar_arrive_expect_tx(&ctl.k_full[s], kBK * D);
+                    tma_load_3d(dst, op_type(op) == OP_E ? &tmK : &tmKb, &ctl.k_full[s], 0,
+                                v * kBK, (int)bh);
                 } else {
                     mbar_arrive_expect_tx(&ctl.k_full[s], G_::SLOT);
 #pragma unroll
@@ -290,11 +307,19 @@ __global__ void __launch_bounds__(kThreads, 2)
             // the whole warp runs the issue code with warp-uniform operands; elect.sync
             // picks the issuing lane (no per-instruction elect loop)
             const uint32_t d = tbase + G_::COLS + 64 * s;
+            if constexpr (F8) {   // E4M3: 32 elements (bytes) of the 128-byte rows per MMA
+                constexpr uint32_t kIdQK8 = idesc_e4m3_f32(128, kBK, 0, 0);
 #pragma unroll
-            for (int kk = 0; kk < D / 16; ++kk) {
-                const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
-                const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
-                mma_ss_elect(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
+                for (int kk = 0; kk < D / 32; ++kk)
+                    mma_ss_f8_elect(d, dq0 + ((kk * 32) >> 4),
+                                    dk0 + ((s * G_::SLOT + kk * 32) >> 4), kIdQK8, kk > 0);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t offq = ((kk >> 2) * G_::QBOX + (kk & 3) * 32) >> 4;
+                    const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
+                    mma_ss_elect(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
+                }
             }
             mma_commit_elect(&ctl.s_full[s]);
             mma_commit_elect(&ctl.k_empty[s]);
@@ -353,7 +378,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         int sc0 = 0, sc1 = 0, sc2 = 0;   // S-type ops seen per S buffer (s_full parity)
         const int64_t n_last = NK - 1;
         const int nlast_len = (int)(p.S - n_last * 64);
-        const float cs = p.scale_log2;   // logits in log2 units: x = S * s * log2(e)
+        float cs = p.scale_log2;         // logits in log2 units: x = S * s * log2(e)
+        // F8: this row's Q scale and the head's K / Kbar scales, folded into the softmax scale
+        float sq_row = 1.f, cs_e = cs, cs_c = cs;
+        if constexpr (F8) {
+            const int64_t t = i * kBQ + r;
+            sq_row = t < p.S ? p.sq[bh * p.S + t] : 1.f;
+            float ska = __uint_as_float(p.kamax[bh]) * (1.f / 448.f);
+            float skb = __uint_as_float(p.kbamax[bh]) * (1.f / 448.f);
+            if (!(ska > 0.f)) ska = 1.f;
+            if (!(skb > 0.f)) skb = 1.f;
+            cs_e = cs * sq_row * ska;
+            cs_c = cs * sq_row * skb;
+        }
         // pv_done[b] completes once per op on buffer b (ops b, b+2, ...): op m's completion
         // is phase m >> 1 of pv_done[m & 1].  The warps only ever wait for the LATEST op
         // issued on a buffer (the PV of op n cannot start before this warpgroup releases
@@ -374,6 +411,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             const int32_t op = ctl.ops[n];
             const int type = op_type(op), v = op_val(op);
             const uint32_t t_buf = tbase + lane_off + G_::COLS + 64 * bi;
+            if constexpr (F8) cs = type == OP_E ? cs_e : cs_c;   // E4M3 dequantisation
             if (DIAG && type != OP_F && (p.dbg & 1)) {
                 // diagnostics: skip the softmax arithmetic
                 mbar_wait_sleep(&ctl.s_full[bi], s_parity(bi));
@@ -554,14 +592,33 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {
                     uint32_t aq[32];
+                    if constexpr (F8) {
+                        // q_t = sq_row * Q8[t]: 16-byte chunk c of the row holds dims 16c..16c+15
+                        const float wq = w * sq_row;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const uint4 u = *reinterpret_cast<const uint4*>(
-                            qrow + a * G_::QBOX + r * 128 + ((c ^ (r & 7)) << 4));
-                        aq[c * 4 + 0] = hmul2_bf16(u.x, w2);
-                        aq[c * 4 + 1] = hmul2_bf16(u.y, w2);
-                        aq[c * 4 + 2] = hmul2_bf16(u.z, w2);
-                        aq[c * 4 + 3] = hmul2_bf16(u.w, w2);
+                        for (int c = 0; c < 4; ++c) {
+                            const int cc = 4 * a + c;
+                            const uint4 u = *reinterpret_cast<const uint4*>(
+                                qrow + r * 128 + ((cc ^ (r & 7)) << 4));
+                            const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) {
+                                const float2 f0 = e4m3x2_to_float2((uint16_t)(wd[e] & 0xffffu));
+                                const float2 f1 = e4m3x2_to_float2((uint16_t)(wd[e] >> 16));
+                                aq[c * 8 + 2 * e] = pack_bf16(f0.x * wq, f0.y * wq);
+                                aq[c * 8 + 2 * e + 1] = pack_bf16(f1.x * wq, f1.y * wq);
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            const uint4 u = *reinterpret_cast<const uint4*>(
+                                qrow + a * G_::QBOX + r * 128 + ((c ^ (r & 7)) << 4));
+                            aq[c * 4 + 0] = hmul2_bf16(u.x, w2);
+                            aq[c * 4 + 1] = hmul2_bf16(u.y, w2);
+                            aq[c * 4 + 2] = hmul2_bf16(u.z, w2);
+                            aq[c * 4 + 3] = hmul2_bf16(u.w, w2);
+                        }
                     }
                     tmem_st32(t_buf + 32 * a, aq);
                 }
@@ -614,13 +671,26 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
         uint32_t box[4] = {64, rows, 1, 1};
         return make_tensor_map(m, t.data, 4, dims, str, box, why, why_len);
     };
-    if (!act(&mQ, q, kBQ) || !act(&mK, k, kBK) || !act(&mV, v, kBK))
+    const bool f8 = r->cfg.qk_fp8 != 0;
+    if (!act(&mV, v, kBK)) return cudaErrorNotSupported;
+    if (f8) {   // E4M3 copies [BH][S][D] / [BH][N_K][D], 128-byte rows
+        auto u8map = [&](CUtensorMap* m, const void* base, uint64_t rows, uint32_t box_rows) {
+            uint64_t dims[3] = {(uint64_t)D, rows, (uint64_t)r->BH};
+            uint64_t str[2] = {(uint64_t)D, rows * D};
+            uint32_t box[3] = {(uint32_t)D, box_rows, 1};
+            return make_tensor_map(m, base, 3, dims, str, box, why, why_len, true);
+        };
+        if (!u8map(&mQ, r->q8, (uint64_t)r->S, kBQ) || !u8map(&mK, r->k8, (uint64_t)r->S, kBK) ||
+            !u8map(&mKb, r->kb8, (uint64_t)r->NK, 64))
+            return cudaErrorNotSupported;
+    } else if (!act(&mQ, q, kBQ) || !act(&mK, k, kBK)) {
         return cudaErrorNotSupported;
+    }
     {
         uint64_t dims[3] = {(uint64_t)D, (uint64_t)r->NK, (uint64_t)r->BH};
         uint64_t str[2] = {(uint64_t)D * 2, (uint64_t)r->NK * D * 2};
         uint32_t box[3] = {64, 64, 1};
-        if (!make_tensor_map(&mKb, r->kbar_lp, 3, dims, str, box, why, why_len) ||
+        if ((!f8 && !make_tensor_map(&mKb, r->kbar_lp, 3, dims, str, box, why, why_len)) ||
             !make_tensor_map(&mVs, r->vsum_lp, 3, dims, str, box, why, why_len))
             return cudaErrorNotSupported;
     }
@@ -639,6 +709,7 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     prm.idx = r->idx; prm.count = r->count; prm.mask = r->mask;
     prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
     prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
+    prm.sq = r->sq8; prm.kamax = r->kamax; prm.kbamax = r->kbamax;
     prm.trace = g_trace_buf;
     prm.trace_x = g_trace_x;
     prm.trace_y = g_trace_y;
@@ -654,6 +725,13 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     // instantiation carries none of that code
     auto kern = small_groups ? (diag ? attn_sm100_kernel<D, true, 1> : attn_sm100_kernel<D, false, 1>)
                              : (diag ? attn_sm100_kernel<D, true, 0> : attn_sm100_kernel<D, false, 0>);
+    if (f8) {
+        if (D != 128 || small_groups || diag) {
+            snprintf(why, why_len, "FP8 QK^T: d = 128, G >= 32, no diagnostics");
+            return cudaErrorNotSupported;
+        }
+        kern = attn_sm100_kernel<D, false, 0, true>;
+    }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     prm.qb0 = r->qb0;

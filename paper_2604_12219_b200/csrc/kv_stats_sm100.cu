@@ -49,6 +49,12 @@ struct Args {
     int32_t G;
     const double* kbar;       // [BH][NK][D] fp64 (route)
     __nv_bfloat16* kbar_lp;   // [BH][NK][D]
+    // FP8 QK^T variant: E4M3 K [BH][S][D] (scale kamax[bh] / 448) converted from the
+    // stage's K tile by the Vsum warps, E4M3 Kbar [BH][NK][D] (scale kbamax[bh] / 448)
+    uint8_t* k8;
+    uint8_t* kb8;
+    const uint32_t* kamax;
+    const uint32_t* kbamax;
     __nv_bfloat16* vsum_lp;   // [BH][NK][D]
     __nv_bfloat16* ht;        // [BH][NG][D][D]
     float* part;              // G > kMaxG: fp32 partial sums [BH][NC][D][D] of 32-block chunks
@@ -102,7 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (tid == 0) {
         for (int s = 0; s < G_::STAGES; ++s) {
             mbar_init(&ctl.full[s], 1);
-            mbar_init(&ctl.empty[s], 1);     // MMA commit (both MMAs read the stage)
+            // MMA commit (both MMAs read the stage) [+ the Vsum warps' E4M3 copy of K]
+            mbar_init(&ctl.empty[s], a.k8 ? 2 : 1);
         }
         for (int s = 0; s < kNVS; ++s) {
             mbar_init(&ctl.vs_full[s], 1);
@@ -215,6 +222,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             __nv_bfloat16* dst = a.kbar_lp + (bh * a.NK + j0) * D;
             float* kbs = &sc.kb[sb][0][0];
             const int ne = nb * D;
+            float kinv = 1.f;
+            if (a.kb8) {
+                const float am = __uint_as_float(a.kbamax[bh]);
+                kinv = am > 0.f ? 448.f / am : 1.f;
+            }
             for (int e0 = lt; e0 < ne; e0 += 64 * 16) {
                 double v[16];
 #pragma unroll
@@ -228,6 +240,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (e < ne) {
                         kbs[e] = (float)v[u];
                         dst[e] = __float2bfloat16_rn((float)v[u]);
+                    }
+                }
+                if (a.kb8) {   // E4M3 Kbar, two elements per conversion
+#pragma unroll
+                    for (int u = 0; u < 16; u += 2) {
+                        const int e = e0 + 64 * u;
+                        if (e < ne) {
+                            const uint16_t pr = cvt_e4m3x2((float)v[u] * kinv, 0.f);
+                            a.kb8[(bh * a.NK + j0) * D + e] = (uint8_t)(pr & 0xffu);
+                        }
+                        const int e1 = e0 + 64 * (u + 1);
+                        if (e1 < ne) {
+                            const uint16_t pr = cvt_e4m3x2((float)v[u + 1] * kinv, 0.f);
+                            a.kb8[(bh * a.NK + j0) * D + e1] = (uint8_t)(pr & 0xffu);
+                        }
                     }
                 }
             }
@@ -246,8 +273,43 @@ __global__ void __launch_bounds__(kThreads, 1)
             item_geo(it, bh, g, j0, nb);
             const int sb = li & 1;
             mbar_wait_sleep(&ctl.scr_empty[sb], ((li >> 1) & 1) ^ 1);   // epilogue of li - 2
+            float kinv = 1.f;
+            if (a.k8) {
+                const float am = __uint_as_float(a.kamax[bh]);
+                kinv = am > 0.f ? 448.f / am : 1.f;
+            }
             for (int jj = 0; jj < nb; ++jj, ++n) {
                 const int vs = n % kNVS;
+                if (a.k8) {   // E4M3 copy of the stage's K tile: thread = (row, 64-dim box)
+                    const int s = n % G_::STAGES;
+                    mbar_wait_sleep(&ctl.full[s], (n / G_::STAGES) & 1);
+                    const int t = mt >> 1, bx = mt & 1;
+                    const int64_t tok = (j0 + jj) * kBk + t;
+                    const uint8_t* kt = smem + s * G_::STAGE + bx * kBox + t * 128;
+                    uint32_t o[16];
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const uint4 u = *reinterpret_cast<const uint4*>(kt + ((c ^ (t & 7)) << 4));
+                        const uint32_t wd[4] = {u.x, u.y, u.z, u.w};
+                        uint16_t pr[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float2 f = __bfloat1622float2(
+                                *reinterpret_cast<const __nv_bfloat162*>(&wd[e]));
+                            pr[e] = cvt_e4m3x2(f.x * kinv, f.y * kinv);
+                        }
+                        o[2 * c] = (uint32_t)pr[0] | ((uint32_t)pr[1] << 16);
+                        o[2 * c + 1] = (uint32_t)pr[2] | ((uint32_t)pr[3] << 16);
+                    }
+                    if (tok < a.S) {
+                        uint4* dst = reinterpret_cast<uint4*>(a.k8 + (bh * a.S + tok) * D + bx * 64);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            dst[q] = make_uint4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                    }
+                    bar_sync(1, 128);
+                    if (mt == 0) mbar_arrive(&ctl.empty[s]);
+                }
                 mbar_wait_sleep(&ctl.vs_full[vs], (n / kNVS) & 1);
                 tc_fence_after();
                 const float v = __uint_as_float(tmem_ld1(tbase + lane_off + kVsBase + vs * kVsCols));
@@ -365,6 +427,10 @@ cudaError_t launch_d(const pasa_tensor& k, const pasa_tensor& v, pasa_route_s* r
     a.H = r->H; a.NK = r->NK; a.NG = r->NG; a.S = r->S; a.G = r->cfg.G;
     a.kbar = r->kbar;
     a.kbar_lp = reinterpret_cast<__nv_bfloat16*>(r->kbar_lp);
+    a.k8 = r->k8;
+    a.kb8 = r->kb8;
+    a.kamax = r->kamax;
+    a.kbamax = r->kbamax;
     a.vsum_lp = reinterpret_cast<__nv_bfloat16*>(r->vsum_lp);
     a.ht = reinterpret_cast<__nv_bfloat16*>(r->ht);
     const bool chunked = r->cfg.G > kMaxG;

@@ -51,6 +51,13 @@ struct pasa_route_s {
     int64_t idx_ld;                  // row stride of idx (entries)
     int32_t* count;                  // [BH][NQ]
     uint32_t* mask;                  // [BH][NQ][W]
+    // FP8 QK^T variant (cfg.qk_fp8) only, else null: E4M3 copies and their scales
+    uint8_t* q8;                     // [BH][S][D] E4M3 Q (pool_kernel), row t scaled by 1/sq8[t]
+    float* sq8;                      // [BH][S] per-row Q scales (row amax / 448)
+    uint8_t* k8;                     // [BH][S][D] E4M3 K (statistics pass), scale kamax / 448
+    uint8_t* kb8;                    // [BH][NK][D] E4M3 Kbar (statistics pass), scale kbamax / 448
+    uint32_t* kamax;                 // [BH] max |K| per head (float bits, pool_kernel), and
+    uint32_t* kbamax;                // [BH] max |Kbar| per head right after it
     double* het;                     // [BH][NK] ||H_j - C||_F (prior-enabled handles only)
     double* prior;                   // [BH][NK] log(het + eps)
     double* hj;                      // [BH][NK][D][D] fp64 H_j of every block (prior handles)
@@ -118,7 +125,7 @@ cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, c
 // diagnostics state set by pasa_debug_trace / pasa_debug_flags
 bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                      const uint64_t* strides_bytes, const uint32_t* box, char* why,
-                     size_t why_len);
+                     size_t why_len, bool u8 = false);
 extern unsigned long long* g_trace_buf;
 extern int g_trace_x, g_trace_y, g_dbg;
 

@@ -14,6 +14,7 @@
 #include "pasa_internal.h"
 #include "philox.cuh"
 #include "fastlog.cuh"
+#include "sm100_ptx.cuh"
 
 namespace pasa {
 namespace {
@@ -51,9 +52,24 @@ struct PoolArgs {
     int64_t blk0, ntask;   // blocks [blk0, blk0 + ntask) of every head are pooled
     double* out;    // [BH][nblk][D]
     double* frag;   // optional DMMA B-fragment copy [BH][ceil(nblk/8)][D/8][8][4][2]
+    // FP8 QK^T variant (cfg.qk_fp8, reading R-30), pool_kernel<T, true> only:
+    uint8_t* f8;          // Q: E4M3 copy [BH][S][D], row t scaled by 1 / f8scale[t]
+    float* f8scale;       // Q: [BH][S] per-row scales (row amax / 448)
+    uint32_t* amax;       // K: [BH] max |K| per head (float bits; the statistics pass
+                          //    quantises K with it)
+    uint32_t* bamax;      // K: [BH] max |Kbar| per head
 };
 
-template <typename T>
+__device__ __forceinline__ float group_max(float v, int ng, int lane) {
+    const unsigned m = (ng == 32 ? 0xffffffffu : ((1u << ng) - 1u) << (lane & ~(ng - 1)));
+    for (int o = 1; o < ng; o <<= 1) v = fmaxf(v, __shfl_xor_sync(m, v, o));
+    return v;
+}
+
+// F8 (the FP8 QK^T variant): also the E4M3 copy of Q with per-row scales (the ng = D / 8
+// threads of a block are adjacent lanes: one group max per token) and the per-head
+// max |K|, max |Kbar|; the ng-lane groups are whole (total, q_tasks multiples of ng)
+template <typename T, bool F8>
 // 4 CTAs (32 warps) per SM: at 3 (70 registers) the kernel lost 40% of its bandwidth
 __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, int64_t q_tasks,
                                                    int64_t total) {
@@ -74,6 +90,31 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
 #pragma unroll
     for (int i = 0; i < 8; ++i) acc[i] = 0.0;
     int64_t t = t0;
+    const int lane = threadIdx.x & 31;
+    const bool isq = a.f8 != nullptr;
+    float kam = 0.f;                       // F8, K tasks: max |K| of this thread's values
+    // F8: the E4M3 row (Q) / running max (K) of one token's 8 values
+    auto f8_row = [&](const double (&v)[8], int64_t tt) {
+        if constexpr (F8) {
+            float m = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) m = fmaxf(m, fabsf((float)v[i]));
+            if (isq) {
+                m = group_max(m, (int)ng, lane);
+                const float sc = m > 0.f ? m * (1.f / 448.f) : 1.f;
+                const float inv = 1.f / sc;
+                uint2 r;
+                r.x = (uint32_t)ptx::cvt_e4m3x2((float)v[0] * inv, (float)v[1] * inv) |
+                      ((uint32_t)ptx::cvt_e4m3x2((float)v[2] * inv, (float)v[3] * inv) << 16);
+                r.y = (uint32_t)ptx::cvt_e4m3x2((float)v[4] * inv, (float)v[5] * inv) |
+                      ((uint32_t)ptx::cvt_e4m3x2((float)v[6] * inv, (float)v[7] * inv) << 16);
+                *reinterpret_cast<uint2*>(a.f8 + (bh * a.S + tt) * a.D + dg * 8) = r;
+                if (dg == 0) a.f8scale[bh * a.S + tt] = sc;
+            } else {
+                kam = fmaxf(kam, m);
+            }
+        }
+    };
     // 4 rows in flight, summed strictly in token order
     for (; t + 4 <= t1; t += 4) {
         double v0[8], v1[8], v2[8], v3[8];
@@ -88,12 +129,14 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
             acc[i] = __dadd_rn(acc[i], v2[i]);
             acc[i] = __dadd_rn(acc[i], v3[i]);
         }
+        f8_row(v0, t); f8_row(v1, t + 1); f8_row(v2, t + 2); f8_row(v3, t + 3);
     }
     for (; t < t1; ++t) {
         double v0[8];
         load8<T>(base + t * a.sS, v0);
 #pragma unroll
         for (int i = 0; i < 8; ++i) acc[i] = __dadd_rn(acc[i], v0[i]);
+        f8_row(v0, t);
     }
     double n = (double)(t1 - t0);
     double m[8];
@@ -111,6 +154,19 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
             a.frag + ((bh * ((a.nblk + 7) / 8) + blk / 8) * (a.D / 8) + dg) * 64 + (blk % 8) * 8);
 #pragma unroll
         for (int fk = 0; fk < 4; ++fk) f[fk] = make_double2(m[fk], m[4 + fk]);
+    }
+    if constexpr (F8) {
+        if (!isq) {   // per-head max |K| and max |Kbar| (non-negative floats order as bits)
+            float bm = 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) bm = fmaxf(bm, fabsf((float)m[i]));
+            kam = group_max(kam, (int)ng, lane);
+            bm = group_max(bm, (int)ng, lane);
+            if (dg == 0) {
+                atomicMax(a.amax + bh, __float_as_uint(kam));
+                atomicMax(a.bamax + bh, __float_as_uint(bm));
+            }
+        }
     }
 }
 
@@ -514,18 +570,25 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches) {
     // Q only for this handle's query blocks [qb0, qb1); K for every block (all are scored)
+    const bool f8 = r->cfg.qk_fp8 != 0;
     PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qb0,
-                r->qb1 - r->qb0, r->qbar, nullptr};
+                r->qb1 - r->qb0, r->qbar, nullptr, f8 ? r->q8 : nullptr, r->sq8, nullptr, nullptr};
     PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, 0, r->NK, r->kbar,
-                r->kfrag};
+                r->kfrag, nullptr, nullptr, r->kamax, r->kbamax};
+    if (f8) {   // FP8 QK^T variant: the per-head maxima accumulate from 0
+        cudaError_t e = cudaMemsetAsync(r->kamax, 0, sizeof(uint32_t) * 2 * r->BH, st);
+        if (e != cudaSuccess) return e;
+    }
     int64_t ng = r->D / 8;
     int64_t q_tasks = r->BH * (r->qb1 - r->qb0) * ng;
     int64_t total = q_tasks + r->BH * r->NK * ng;
     const unsigned pgrid = (unsigned)((total + 255) / 256);
     if (q.dtype == PASA_F32)
-        pool_kernel<float><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
+        pool_kernel<float, false><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
+    else if (f8)
+        pool_kernel<__nv_bfloat16, true><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
     else
-        pool_kernel<__nv_bfloat16><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
+        pool_kernel<__nv_bfloat16, false><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
 
     const double* prior = nullptr;
     if (v) {

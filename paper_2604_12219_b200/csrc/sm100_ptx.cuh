@@ -3,6 +3,7 @@
 // TMEM alloc / ld / st / commit / fences, and UMMA descriptors.
 // Compile with -gencode arch=compute_100a,code=sm_100a (tcgen05 is "a"-only).
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda.h>
 #include <stdint.h>
 
@@ -159,6 +160,17 @@ __device__ __forceinline__ void mma_ss_elect(uint32_t d_tmem, uint64_t a_desc, u
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// FP8 operands (kind::f8f6f4, E4M3 x E4M3 -> f32; K = 32 per instruction)
+__device__ __forceinline__ void mma_ss_f8_elect(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 __device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                              uint32_t idesc, uint32_t accumulate) {
     asm volatile(
@@ -291,6 +303,27 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N, int a_mn_maj
            | ((uint32_t)b_mn_major << 16)  // B major
            | ((uint32_t)(N >> 3) << 17)    // N >> 3
            | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+
+// kind::f8f6f4 instruction descriptor: E4M3 A and B (format code 0), f32 accumulate
+__host__ __device__ constexpr uint32_t idesc_e4m3_f32(int M, int N, int a_mn_major, int b_mn_major) {
+    return (1u << 4)                       // D format f32
+           | ((uint32_t)a_mn_major << 15)  // A major
+           | ((uint32_t)b_mn_major << 16)  // B major
+           | ((uint32_t)(N >> 3) << 17)    // N >> 3
+           | ((uint32_t)(M >> 4) << 24);   // M >> 4
+}
+// two fp32 -> packed E4M3 pair (round to nearest even, saturate to +-448); lo in the low byte
+__device__ __forceinline__ uint16_t cvt_e4m3x2(float lo, float hi) {
+    uint16_t r;
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// packed E4M3 pair -> two fp32 (exact)
+__device__ __forceinline__ float2 e4m3x2_to_float2(uint16_t v) {
+    uint32_t h;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h) : "h"(v));
+    return __half22float2(*reinterpret_cast<__half2*>(&h));
 }
 
 __device__ __forceinline__ float ex2(float x) {

@@ -36,14 +36,15 @@ EncodeTiledFn encode_fn() {
 
 bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,
                      const uint64_t* strides_bytes, const uint32_t* box, char* why,
-                     size_t why_len) {
+                     size_t why_len, bool u8) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) {
         snprintf(why, why_len, "cuTensorMapEncodeTiled unavailable");
         return false;
     }
     cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    CUresult rc = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, (cuuint32_t)rank, const_cast<void*>(base),
+    CUresult rc = fn(m, u8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                     (cuuint32_t)rank, const_cast<void*>(base),
                      reinterpret_cast<const cuuint64_t*>(dims),
                      reinterpret_cast<const cuuint64_t*>(strides_bytes),
                      reinterpret_cast<const cuuint32_t*>(box), estr,
