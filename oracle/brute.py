@@ -40,11 +40,13 @@ def philox4x32_10(ctr: np.ndarray, key) -> np.ndarray:
 
 
 def gumbel_grid(seed: int, step: int, gh: int, NQ: int, NK: int) -> np.ndarray:
-    """g[i, j] for counters (j, i, gh, step), key (lo32 seed, hi32 seed)."""
+    """g[i, j] from word j mod 4 of counter (j // 4, i, gh, step), key (lo32 seed, hi32 seed)
+    (reading R-11: one Philox4x32-10 call serves four consecutive blocks)."""
     i, j = np.meshgrid(np.arange(NQ), np.arange(NK), indexing="ij")
-    ctr = np.stack([j, i, np.full_like(i, gh), np.full_like(i, step)], -1).astype(np.uint32)
-    x0 = philox4x32_10(ctr, (seed & 0xFFFFFFFF, seed >> 32))[..., 0]
-    u = (x0.astype(np.float64) + 0.5) * 2.0 ** -32
+    ctr = np.stack([j // 4, i, np.full_like(i, gh), np.full_like(i, step)], -1).astype(np.uint32)
+    words = philox4x32_10(ctr, (seed & 0xFFFFFFFF, seed >> 32))
+    xw = np.take_along_axis(words, (j % 4)[..., None], axis=-1)[..., 0]
+    u = (xw.astype(np.float64) + 0.5) * 2.0 ** -32
     return -np.log(-np.log(u))
 
 

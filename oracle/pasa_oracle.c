@@ -75,14 +75,16 @@ uint64_t orc_layer_seed(uint64_t seed, int32_t layer) {
     return z ^ (z >> 31);
 }
 
-/* R-11/R-12: ctr = (j, i, gh, step), key = (lo32(seed), hi32(seed)),
- * u = (x0 + 0.5) * 2^-32 in (0,1), g = -ln(-ln u). */
+/* R-11/R-12: one Philox4x32-10 call yields four 32-bit words; block j of query block
+ * i of global head gh at step `step` takes word w = j mod 4 of counter
+ * ctr = (floor(j/4), i, gh, step), key = (lo32(seed), hi32(seed));
+ * u = (x_w + 0.5) * 2^-32 in (0,1), g = -ln(-ln u). */
 double orc_gumbel(uint64_t seed, int32_t step, int64_t gh, int64_t i, int64_t j) {
-    uint32_t ctr[4] = {(uint32_t)j, (uint32_t)i, (uint32_t)gh, (uint32_t)step};
+    uint32_t ctr[4] = {(uint32_t)(j >> 2), (uint32_t)i, (uint32_t)gh, (uint32_t)step};
     uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
     uint32_t x[4];
     orc_philox4x32_10(ctr, key, x);
-    double u = ((double)x[0] + 0.5) * 2.3283064365386963e-10; /* 2^-32 */
+    double u = ((double)x[j & 3] + 0.5) * 2.3283064365386963e-10; /* 2^-32 */
     return -log(-log(u));
 }
 

@@ -240,14 +240,13 @@ struct FusedArgs {
 
 __device__ const LogEnt g_logtab[128] = PASA_LOGTAB_INIT;
 
-// Gumbel variate of score (i, j) of global head gh (R4, R-12): g = -log(-log u), with the
-// table-driven fp64 log of fastlog.cuh (within 1.5 ulp of the exact log; glibc's, which
-// the oracle uses, is within 0.52: r~ moves by ~1e-16 relative, inside the documented-tie
-// margin)
-__device__ __forceinline__ double gumbel(uint32_t j, uint32_t i, uint32_t gh, uint32_t step,
-                                         uint32_t k0, uint32_t k1) {
-    const uint32_t x0 = philox4x32_10_x0(j, i, gh, step, k0, k1);
-    const double u = __dmul_rn(__dadd_rn((double)x0, 0.5), 2.3283064365386963e-10);
+// Gumbel variate from one Philox word x (R4, R-12): g = -log(-log u), u = (x + 1/2) 2^-32,
+// with the table-driven fp64 log of fastlog.cuh (within 1.5 ulp of the exact log; glibc's,
+// which the oracle uses, is within 0.52: r~ moves by ~1e-16 relative, inside the
+// documented-tie margin).  Word j mod 4 of counter (floor(j/4), i, gh, step) serves block j
+// (R-11): one Philox call per four blocks.
+__device__ __forceinline__ double gumbel_of(uint32_t x) {
+    const double u = __dmul_rn(__dadd_rn((double)x, 0.5), 2.3283064365386963e-10);
     return -fastlog_tab(g_logtab, -fastlog_tab(g_logtab, u));
 }
 
@@ -301,7 +300,7 @@ __device__ __forceinline__ void select_row_mem(const uint64_t* key, int NK, int 
             for (int m = 0; m < HR; ++m) {
                 const uint32_t h16 = hr[m] >> 16;
                 gw += h16 > tw;
-                ew += h16 == tw && 32 * m + lane < NK;
+                ew += h16 == tw && hr[m] != 0u;   // absent blocks hold 0
             }
         } else {
             for (int j = lane; j < NK; j += 32) {
@@ -528,30 +527,53 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     // ---- phase C: keys in place, threshold, outputs -------------------------------------
     uint64_t* key = reinterpret_cast<uint64_t*>(row);
     const int64_t grow = bh * a.NQ + i0 + warp;
+    // lane handles the four consecutive blocks j = 4 (32 m4 + lane) + w, w = 0..3 (one Philox
+    // call each group of four)
+    auto keys4 = [&](int j4, uint64_t (&kx)[4]) {
+        uint4 x = make_uint4(0u, 0u, 0u, 0u);
+        if (biased) x = philox4x32_10((uint32_t)j4, i, gh, a.step, a.key0, a.key1);
+        const uint32_t xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            const int j = 4 * j4 + w;
+            kx[w] = 0ull;
+            if (j < NK) {
+                double xv = row[j];
+                if (biased)   // R5: rt = r + (beta sigma_i) g, two rounded operations
+                    xv = __dadd_rn(xv, __dmul_rn(bi, gumbel_of(xw[w])));
+                kx[w] = orderable(xv);
+            }
+        }
+    };
     if constexpr (HR > 0) {
         uint32_t hr[HR];
+        uint64_t kx[4];
 #pragma unroll
-        for (int m = 0; m < HR; ++m) {
-            const int j = 32 * m + lane;
-            hr[m] = 0u;
-            if (j < NK) {
-                double x = row[j];
-                if (biased)   // R4/R5: rt = r + (beta sigma_i) g, two rounded operations
-                    x = __dadd_rn(x, __dmul_rn(bi, gumbel((uint32_t)j, i, gh, a.step, a.key0, a.key1)));
-                const uint64_t kx = orderable(x);
-                key[j] = kx;
-                hr[m] = (uint32_t)(kx >> 32);
+        for (int m4 = 0; m4 < HR / 4; ++m4) {
+            const int j4 = 32 * m4 + lane;
+#pragma unroll
+            for (int w = 0; w < 4; ++w) hr[4 * m4 + w] = 0u;
+            if (4 * j4 < NK) {
+                keys4(j4, kx);
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                    if (4 * j4 + w < NK) {
+                        key[4 * j4 + w] = kx[w];
+                        hr[4 * m4 + w] = (uint32_t)(kx[w] >> 32);
+                    }
+                }
             }
         }
         __syncwarp();
         select_row_mem<HR>(key, NK, k, lane, cbuf + warp * 64, a.idx + grow * NK,
                            a.mask + grow * a.W, a.count + grow, hr);
     } else {
-        for (int j = lane; j < NK; j += 32) {
-            double x = row[j];
-            if (biased)
-                x = __dadd_rn(x, __dmul_rn(bi, gumbel((uint32_t)j, i, gh, a.step, a.key0, a.key1)));
-            key[j] = orderable(x);
+        for (int j4 = lane; 4 * j4 < NK; j4 += 32) {
+            uint64_t kx[4];
+            keys4(j4, kx);
+#pragma unroll
+            for (int w = 0; w < 4; ++w)
+                if (4 * j4 + w < NK) key[4 * j4 + w] = kx[w];
         }
         __syncwarp();
         const uint32_t none[1] = {0u};

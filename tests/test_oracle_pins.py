@@ -293,3 +293,15 @@ def test_block_means_constant_block_exact():
     x = np.full((100, 3), 0.375)
     m = oracle.block_means(x, 32)
     assert (m == 0.375).all()
+
+
+def test_gumbel_counter_layout_reading_r11():
+    """Reading R-11: block j of query block i takes word j mod 4 of the
+    Philox4x32-10 output for counter (floor(j/4), i, gh, step) -- checked against the
+    KAT-pinned generator for every word position and a counter word above 2^30."""
+    seed, step, gh = 0x1234_5678_9ABC_DEF0, 17, 5
+    key = (seed & 0xFFFFFFFF, seed >> 32)
+    for i, j in [(0, 0), (3, 1), (3, 2), (7, 3), (7, 4), (2, 1181), (9, (1 << 32) - 1)]:
+        x = oracle.philox((j >> 2, i, gh, step), key)[j & 3]
+        u = (float(x) + 0.5) * 2.0 ** -32
+        assert oracle.gumbel(seed, step, gh, i, j) == -math.log(-math.log(u))

@@ -17,4 +17,10 @@ run memcheck  memcheck_attn  "$ATTN or $ROUTE" tests/test_gpu_parity.py
 run racecheck racecheck_attn "$ATTN" tests/test_gpu_parity.py
 run synccheck synccheck_attn "$ATTN" tests/test_gpu_parity.py
 run racecheck racecheck_route "$ROUTE" tests/test_gpu_parity.py
-run memcheck  memcheck_stats "kv_stats" tests/test_gpu_stats.py
+run memcheck  memcheck_stats "kv_stats or stats" tests/test_gpu_stats.py
+run racecheck racecheck_stats "kv_stats or stats" tests/test_gpu_stats.py
+run synccheck synccheck_stats "kv_stats or stats" tests/test_gpu_stats.py
+# round 2: the fused route kernel, the persistent statistics kernel, q-block ranges, FP8 QK^T
+run memcheck  memcheck_r2 "qblock or sharded or fp8_qk_parity" tests/test_gpu_dist.py tests/test_gpu_fp8.py
+run racecheck racecheck_r2 "qblock_range_equals or fp8_qk_parity" tests/test_gpu_dist.py tests/test_gpu_fp8.py
+run synccheck synccheck_r2 "qblock_range_equals or fp8_qk_parity" tests/test_gpu_dist.py tests/test_gpu_fp8.py
