@@ -314,7 +314,7 @@ def run_pasa(args):
     except ValueError as exc:
         raise SystemExit(str(exc))
     # head-equivalents of attention work on this rank ((head, q-block) items / N_Q)
-    work_heads = sum(n * ((b - a) if (a, b) != (0, 0) else NQ) for _, n, a, b in segs) / NQ
+    work_heads = sum((b - a) if (a, b) != (0, 0) else n * NQ for _, n, a, b in segs) / NQ
     dev = torch.device("cuda", torch.cuda.current_device())
     cdev = torch.device("cpu") if gloo else dev      # where collective buffers live
 

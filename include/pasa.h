@@ -103,11 +103,13 @@ typedef struct {
     int32_t prior;           /* pasa_prior (PASA_PRIOR_NONE = the north star's route)          */
     int32_t _pad;
     double eps;              /* epsilon of the prior's log (1e-6); > 0 if prior on */
-    int32_t qb_begin;        /* this handle routes and attends query blocks [qb_begin, qb_end)  */
-    int32_t qb_end;          /* of every head only; (0, 0) = all N_Q.  The flattened (head,
-                              * q-block) partition of SURVEY.md §8e for head counts that do not
-                              * divide the GPU count: K/V statistics still cover whole heads,
-                              * Philox keys on the global block index i, and rows outside the
+    int32_t qb_begin;        /* this handle routes and attends only the work items               */
+    int32_t qb_end;          /* [qb_begin, qb_end) of its B*H*N_Q (head, query block) items,
+                              * item = (b*H + h)*N_Q + i (head-major); (0, 0) = all.  The
+                              * flattened (head, q-block) partition of SURVEY.md §8e for head
+                              * counts that do not divide the GPU count: one handle (one launch
+                              * per kernel) per rank; K/V statistics still cover whole heads,
+                              * Philox keys on the global head and block, and rows outside the
                               * range of idx / count / mask / out are not written.            */
     int32_t qk_fp8;          /* 1 = opt-in precision variant (reading R-30):
                               * QK^T of kept blocks and the centroid logits run on the FP8 tensor

@@ -14,13 +14,17 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIBDIR = os.path.join(PKG, "lib")
+# A/B builds (tools/): PASA_BUILD_DIR puts objects and the library elsewhere,
+# PASA_EXTRA_FLAGS adds nvcc flags (e.g. -DPASA_D64_POLY=4); the product build sets neither
+_ALT = os.environ.get("PASA_BUILD_DIR")
+LIBDIR = os.path.join(_ALT, "lib") if _ALT else os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libpasa.so")
-OBJDIR = os.path.join(PKG, "build")
+OBJDIR = os.path.join(_ALT, "build") if _ALT else os.path.join(PKG, "build")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                  "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+COMMON += os.environ.get("PASA_EXTRA_FLAGS", "").split()
 # per-file extra flags: the route unit must not contract fp64 mul+add into fma
 EXTRA = {"route.cu": ["--fmad=false"]}
 SOURCES = ["api.cpp", "tmap.cpp", "budget.cu", "route.cu", "het.cu", "kv_stats.cu", "attn_simt.cu",

@@ -70,9 +70,9 @@ pasa_status check_cfg(const pasa_route_cfg* c, int64_t B, int64_t S, int64_t H, 
         return fail(PASA_EUNSUPPORTED, "qk_fp8 needs D = 128, Bq = 128 and G >= 32");
     const int64_t NQ = (S + c->Bq - 1) / c->Bq;
     if ((c->qb_begin != 0 || c->qb_end != 0) &&
-        !(c->qb_begin >= 0 && c->qb_begin < c->qb_end && c->qb_end <= NQ))
-        return fail(PASA_EINVAL, "q-block range [%d, %d) outside [0, N_Q=%lld)", c->qb_begin,
-                    c->qb_end, (long long)NQ);
+        !(c->qb_begin >= 0 && c->qb_begin < c->qb_end && c->qb_end <= B * H * NQ))
+        return fail(PASA_EINVAL, "item range [%d, %d) outside [0, B*H*N_Q=%lld)", c->qb_begin,
+                    c->qb_end, (long long)(B * H * NQ));
     return PASA_OK;
 }
 
@@ -279,8 +279,8 @@ pasa_status pasa_route_init(void* dev_ws, size_t bytes, const pasa_route_cfg* cf
     r->B = B; r->S = S; r->H = H; r->D = D;
     r->NQ = L.NQ; r->NK = L.NK; r->NG = L.NG; r->W = L.W; r->BH = L.BH;
     const bool all = cfg->qb_begin == 0 && cfg->qb_end == 0;
-    r->qb0 = all ? 0 : cfg->qb_begin;
-    r->qb1 = all ? L.NQ : cfg->qb_end;
+    r->it0 = all ? 0 : cfg->qb_begin;
+    r->it1 = all ? L.BH * L.NQ : cfg->qb_end;
     r->hdr = reinterpret_cast<int32_t*>(w + L.off_hdr);
     r->qbar = reinterpret_cast<double*>(w + L.off_qbar);
     r->kbar = reinterpret_cast<double*>(w + L.off_kbar);

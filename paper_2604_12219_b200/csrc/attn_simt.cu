@@ -35,7 +35,7 @@ struct SimtArgs {
     void* out;
     int64_t qsB, qsS, qsH, ksB, ksS, ksH, vsB, vsS, vsH, osB, osS, osH;
     int64_t S, H, NQ, NK, NG, W;
-    int64_t qb0;          // first query block of the handle's range (grid.x covers the range)
+    int64_t it0;          // first (head, q-block) item of the handle's range (grid.x covers it)
     int32_t Bq, G, comp;
     float scale_log2;     // s * log2(e)
     float s;
@@ -53,7 +53,7 @@ __global__ void __launch_bounds__(256) attn_simt_kernel(SimtArgs a) {
     __shared__ float Ks[kTT][D];
     __shared__ float Vs[kTT][D];
 
-    const int64_t bh = blockIdx.y, i = a.qb0 + blockIdx.x;
+    const int64_t bh = (a.it0 + blockIdx.x) / a.NQ, i = (a.it0 + blockIdx.x) % a.NQ;
     const int64_t b = bh / a.H, h = bh % a.H;
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int r = tid >> 1, half = tid & 1;
@@ -190,8 +190,8 @@ cudaError_t launch_attn_simt(const pasa_tensor& q, const pasa_tensor& k, const p
     a.scale_log2 = (float)(1.0 / sqrt((double)r->D) * 1.4426950408889634);
     a.idx = r->idx; a.count = r->count; a.mask = r->mask;
     a.kbar_lp = r->kbar_lp; a.vsum_lp = r->vsum_lp; a.ht = r->ht;
-    a.qb0 = r->qb0;
-    dim3 grid((unsigned)(r->qb1 - r->qb0), (unsigned)r->BH);
+    a.it0 = r->it0;
+    const unsigned grid = (unsigned)(r->it1 - r->it0);   // head-major items
     const int threads = 2 * r->cfg.Bq;
     if (q.dtype == PASA_F32) {
         if (r->D == 128) attn_simt_kernel<float, 128><<<grid, threads, 0, st>>>(a);

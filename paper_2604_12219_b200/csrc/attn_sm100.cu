@@ -41,6 +41,11 @@ constexpr int kMaxNK = 4096;
 constexpr int kMaxOps = kMaxNK + kMaxNK / 64 + kMaxNK / 8 + 64;
 constexpr int kTmemCols = 256;
 constexpr float kRescaleThresh = 8.f; // log2 units
+// d = 64: one exponential pair in PASA_D64_POLY on the FMA pipe (degree-3 polynomial,
+// ex2_fma2) instead of MUFU (0 = none); A/B knob, see DESIGN.md §12
+#ifndef PASA_D64_POLY
+#define PASA_D64_POLY 0
+#endif
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
 __device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
@@ -69,7 +74,7 @@ struct Geo {
 
 struct Params {
     int64_t S, H, NQ, NK, NG, W;
-    int64_t qb0;        // first query block of the handle's range (grid.x covers the range)
+    int64_t it0;        // first (head, q-block) item of the handle's range (grid.x covers it)
     int32_t G, comp;
     float scale_log2;   // s * log2(e)
     float s;            // 1/sqrt(D)
@@ -138,9 +143,10 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const bool spin = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
-    const bool tracing = p.trace != nullptr && (int)blockIdx.x == p.trace_x &&
-                         (int)blockIdx.y == p.trace_y;
-    const int64_t i = p.qb0 + blockIdx.x, bh = blockIdx.y;
+    const bool tracing = p.trace != nullptr && (int)((p.it0 + blockIdx.x) % p.NQ) == p.trace_x &&
+                         (int)((p.it0 + blockIdx.x) / p.NQ) == p.trace_y;
+    const int64_t item = p.it0 + blockIdx.x;
+    const int64_t i = item % p.NQ, bh = item / p.NQ;
     const int64_t b = bh / p.H, h = bh % p.H;
     const int64_t row = bh * p.NQ + i;
     const int32_t cnt = p.count[row];
@@ -476,7 +482,20 @@ __global__ void __launch_bounds__(kThreads, 2)
                                                             __uint_as_float(sa[2 * c + 1])), cs2, nm2);
                         const float2 xb = ffma2(make_float2(__uint_as_float(sb[2 * c]),
                                                             __uint_as_float(sb[2 * c + 1])), cs2, nm2);
-                        const float p0 = ex2(xa.x), p1 = ex2(xa.y), p2 = ex2(xb.x), p3 = ex2(xb.y);
+                        float p0, p1, p2, p3;
+                        constexpr int kPoly = D == 64 ? PASA_D64_POLY : 0;
+                        if (kPoly > 0 && (2 * c) % kPoly == 0) {
+                            const float2 pa = ex2_fma2(xa);
+                            p0 = pa.x; p1 = pa.y;
+                        } else {
+                            p0 = ex2(xa.x); p1 = ex2(xa.y);
+                        }
+                        if (kPoly > 0 && (2 * c + 1) % kPoly == 0) {
+                            const float2 pb = ex2_fma2(xb);
+                            p2 = pb.x; p3 = pb.y;
+                        } else {
+                            p2 = ex2(xb.x); p3 = ex2(xb.y);
+                        }
                         a0 = fadd2(a0, make_float2(p0, p1));
                         a1 = fadd2(a1, make_float2(p2, p3));
                         pk[c] = pack_bf16(p0, p1);
@@ -734,8 +753,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     }
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    prm.qb0 = r->qb0;
-    dim3 grid((unsigned)(r->qb1 - r->qb0), (unsigned)r->BH);
+    prm.it0 = r->it0;
+    const unsigned grid = (unsigned)(r->it1 - r->it0);   // head-major items
     kern<<<grid, kThreads, smem, st>>>(mQ, mK, mV, mKb, mVs, mHt, prm);
     return cudaGetLastError();
 }

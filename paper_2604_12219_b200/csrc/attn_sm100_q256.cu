@@ -70,7 +70,7 @@ struct Geo {
 
 struct Params {
     int32_t S, H, NQ, NK, W, G, comp;
-    int32_t qb0;        // first query block of the handle's range (grid.x covers the range)
+    int32_t it0;        // first (head, q-block) item of the handle's range (grid.x covers it)
     float scale_log2;   // s * log2(e)
     float s;            // 1/sqrt(D)
     const int32_t* idx;
@@ -108,7 +108,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ Ctl ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int i = p.qb0 + (int)blockIdx.x, bh = blockIdx.y;
+    const int item = p.it0 + (int)blockIdx.x;
+    const int i = item % p.NQ, bh = item / p.NQ;
     const int b = bh / p.H, h = bh % p.H;
     const int64_t row = (int64_t)bh * p.NQ + i;
     const int32_t cnt = p.count[row];
@@ -533,8 +534,8 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     auto kern = attn_sm100_q256_kernel<D>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    prm.qb0 = (int32_t)r->qb0;
-    dim3 grid((unsigned)(r->qb1 - r->qb0), (unsigned)r->BH);
+    prm.it0 = (int32_t)r->it0;
+    const unsigned grid = (unsigned)(r->it1 - r->it0);   // head-major items
     kern<<<grid, kThreads, smem, st>>>(mQ, mK, mV, mKb, mVs, mHt, prm);
     return cudaGetLastError();
 }

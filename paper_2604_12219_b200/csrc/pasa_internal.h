@@ -36,7 +36,8 @@ struct pasa_budget_s {
 struct pasa_route_s {
     pasa_route_cfg cfg;
     int64_t B, S, H, D, NQ, NK, NG, W, BH;
-    int64_t qb0, qb1;                // query blocks this handle routes / attends: [qb0, qb1)
+    int64_t it0, it1;                // (head, q-block) items routed / attended: [it0, it1),
+                                     // item = bh * NQ + i
     int32_t* hdr;                    // device: [0] = k of the last pasa_route
     double* qbar;                    // [BH][NQ][D]
     double* kbar;                    // [BH][NK][D]

@@ -49,7 +49,7 @@ struct PoolArgs {
     int64_t S, H, D;
     int32_t bsz;    // block size in tokens
     int64_t nblk;   // blocks per head
-    int64_t blk0, ntask;   // blocks [blk0, blk0 + ntask) of every head are pooled
+    int64_t blk0, ntask;   // ntask > 0: all ntask blocks of every head; 0: items [blk0, ...)
     double* out;    // [BH][nblk][D]
     double* frag;   // optional DMMA B-fragment copy [BH][ceil(nblk/8)][D/8][8][4][2]
     // FP8 QK^T variant (cfg.qk_fp8, reading R-30), pool_kernel<T, true> only:
@@ -79,9 +79,11 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
     if (task >= q_tasks) task -= q_tasks;
     int64_t ng = a.D / 8;
     int64_t dg = task % ng;
+    // Q: items blk0 + rest of the flattened (head, block) list; K: every block of every head
     int64_t rest = task / ng;
-    int64_t blk = a.blk0 + rest % a.ntask;
-    int64_t bh = rest / a.ntask;
+    int64_t blk, bh;
+    if (a.ntask > 0) { blk = rest % a.ntask; bh = rest / a.ntask; }
+    else { blk = (a.blk0 + rest) % a.nblk; bh = (a.blk0 + rest) / a.nblk; }
     int64_t b = bh / a.H, h = bh % a.H;
     int64_t t0 = blk * a.bsz;
     int64_t t1 = min(t0 + (int64_t)a.bsz, a.S);
@@ -227,7 +229,7 @@ struct FusedArgs {
     const double* prior;       // [BH][NK] or nullptr
     const BudgetRec* rec;
     int64_t NQ, NK, W, H, H_total, head_offset;
-    int64_t qb0, qb1;          // query blocks routed: [qb0, qb1)
+    int64_t it0, it1;          // (head, q-block) items routed: [it0, it1), item = bh NQ + i
     int D, NKP;                // NKP: odd row stride of the score rows (doubles)
     double s, beta;
     uint32_t key0, key1, step;
@@ -393,8 +395,12 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     const int NK = (int)a.NK, NKP = a.NKP;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t bh = blockIdx.y;
-    const int64_t i0 = a.qb0 + (int64_t)blockIdx.x * R;
-    const int nrows = (int)min((int64_t)R, a.qb1 - i0);
+    // rows of this CTA inside the item range: [rlo, rhi) of i0 .. i0 + R - 1
+    const int64_t i0 = (int64_t)blockIdx.x * R;
+    const int64_t ilo = max(a.it0 - bh * a.NQ, (int64_t)0), ihi = min(a.it1 - bh * a.NQ, a.NQ);
+    const int rlo = (int)max(ilo - i0, (int64_t)0);
+    const int nrows = (int)max(min((int64_t)R, ihi - i0), (int64_t)0);   // rows < nrows exist
+    if (rlo >= nrows) return;                       // no item of this CTA is in range
     double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(sq + R * (D + 4));    // [NW][64]
     double* sc = SMEM_SC ? reinterpret_cast<double*>(cbuf + NW * 64)
@@ -404,7 +410,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     if (blockIdx.x == 0 && bh == 0 && tid == 0) a.hdr[0] = k;
     const int M = (NK + 31) >> 5;
     if (k >= NK) {   // dense step / full budget: every block exact, no scores needed
-        if (warp < nrows) {   // (one row per warp: R = 8)
+        if (warp >= rlo && warp < nrows) {   // (one row per warp: R = 8)
             const int64_t row = bh * a.NQ + i0 + warp;
             int32_t* orow = a.idx + row * NK;
             uint32_t* mrow = a.mask + row * a.W;
@@ -426,7 +432,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     const double* Q = a.qbar + (bh * a.NQ + i0) * D;
     for (int e = tid; e < R * D; e += NT) {
         const int r = e / D, c = e % D;
-        sq[r * (D + 4) + c] = r < nrows ? Q[(int64_t)r * D + c] : 0.0;
+        sq[r * (D + 4) + c] = r >= rlo && r < nrows ? Q[(int64_t)r * D + c] : 0.0;
     }
     __syncthreads();
     {
@@ -483,7 +489,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int j = (g * CG + c) * 8 + 2 * fk + h;
-                        if (j < NK && r < nrows) {
+                        if (j < NK && r >= rlo && r < nrows) {
                             double x = __dmul_rn(a.s, acc[t][c][h]);
                             if (a.prior) x = __dadd_rn(x, a.prior[bh * a.NK + j]);   // Eq. 8
                             sc[r * NKP + j] = x;
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
         }
     }
     __syncthreads();
-    if (warp >= nrows) return;
+    if (warp < rlo || warp >= nrows) return;
 
     // ---- phase B: sigma_i (R3) ---------------------------------------------------------
     // mu_i and the centred sum of squares as fixed-order warp reductions (lane-strided
@@ -591,10 +597,10 @@ constexpr size_t fused_fixed_smem(int R, int D) {
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches) {
-    // Q only for this handle's query blocks [qb0, qb1); K for every block (all are scored)
+    // Q only for this handle's (head, q-block) items [it0, it1); K for every block (all scored)
     const bool f8 = r->cfg.qk_fp8 != 0;
-    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->qb0,
-                r->qb1 - r->qb0, r->qbar, nullptr, f8 ? r->q8 : nullptr, r->sq8, nullptr, nullptr};
+    PoolArgs qa{q.data, q.sB, q.sS, q.sH, r->S, r->H, r->D, r->cfg.Bq, r->NQ, r->it0,
+                0, r->qbar, nullptr, f8 ? r->q8 : nullptr, r->sq8, nullptr, nullptr};
     PoolArgs ka{k.data, k.sB, k.sS, k.sH, r->S, r->H, r->D, r->cfg.Bk, r->NK, 0, r->NK, r->kbar,
                 r->kfrag, nullptr, nullptr, r->kamax, r->kbamax};
     if (f8) {   // FP8 QK^T variant: the per-head maxima accumulate from 0
@@ -602,7 +608,7 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
         if (e != cudaSuccess) return e;
     }
     int64_t ng = r->D / 8;
-    int64_t q_tasks = r->BH * (r->qb1 - r->qb0) * ng;
+    int64_t q_tasks = (r->it1 - r->it0) * ng;
     int64_t total = q_tasks + r->BH * r->NK * ng;
     const unsigned pgrid = (unsigned)((total + 255) / 256);
     if (q.dtype == PASA_F32)
@@ -622,7 +628,7 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     FusedArgs fa;
     fa.qbar = r->qbar; fa.kfrag = r->kfrag; fa.prior = prior; fa.rec = b->rec;
     fa.NQ = r->NQ; fa.NK = r->NK; fa.W = r->W; fa.H = r->H;
-    fa.qb0 = r->qb0; fa.qb1 = r->qb1;
+    fa.it0 = r->it0; fa.it1 = r->it1;
     fa.H_total = r->cfg.H_total; fa.head_offset = r->cfg.head_offset;
     fa.D = (int)r->D; fa.NKP = (int)route_score_stride(r->NK);
     fa.s = s; fa.beta = r->cfg.beta;
@@ -634,7 +640,7 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     constexpr int RR = kFRows;
     const size_t smem = fused_fixed_smem(RR, (int)r->D) +
                         (smem_sc ? sizeof(double) * (size_t)RR * fa.NKP : 0);
-    dim3 grid((unsigned)((r->qb1 - r->qb0 + RR - 1) / RR), (unsigned)r->BH);
+    dim3 grid((unsigned)((r->NQ + RR - 1) / RR), (unsigned)r->BH);   // CTAs out of range exit
     const bool hreg = r->NK <= 32 * kFHR;
 #define PASA_FUSED_PICK(DD)                                                                  \
     (!smem_sc ? route_fused_kernel<RR, DD, false, 0>                                         \

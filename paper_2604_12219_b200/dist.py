@@ -87,29 +87,18 @@ def flat_partition(H: int, NQ: int, world: int, rank: int) -> List[Tuple[int, in
     """Rank r owns the flattened work items [floor(r N / P), floor((r+1) N / P)) of the
     N = H * NQ (head, q-block) items, head-major (Wan-1.3B's 12 heads over
     8 ranks is capped at 75% efficiency by the head split; 3,072 items split to 384 each).
-    Returns segments (head_offset, n_heads, qb_begin, qb_end): one route handle each, with
-    (0, 0) = all N_Q q-blocks of n_heads whole heads, else one head's q-block range."""
+    Returns [(head_offset, n_heads, item_begin, item_end)]: one route handle over the
+    n_heads heads the range touches, with the item range relative to that handle
+    (RouteCfg(qb_begin=item_begin, qb_end=item_end); (0, 0) = all its items)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError(f"rank {rank} of world {world}")
     N = H * NQ
     a, b = N * rank // world, N * (rank + 1) // world
     if a >= b:
         return []
-    segs = []
-    ha, ia = divmod(a, NQ)
-    hb, ib = divmod(b - 1, NQ)
-    ib += 1
-    if ha == hb:
-        return [(ha, 1, 0, 0) if (ia, ib) == (0, NQ) else (ha, 1, ia, ib)]
-    if ia > 0:
-        segs.append((ha, 1, ia, NQ))
-        ha += 1
-    full_end = hb if ib < NQ else hb + 1
-    if full_end > ha:
-        segs.append((ha, full_end - ha, 0, 0))
-    if ib < NQ:
-        segs.append((hb, 1, 0, ib))
-    return segs
+    h0, h1 = a // NQ, (b - 1) // NQ + 1
+    lo, hi = a - h0 * NQ, b - h0 * NQ
+    return [(h0, h1 - h0, 0, 0) if (lo, hi) == (0, (h1 - h0) * NQ) else (h0, h1 - h0, lo, hi)]
 
 
 def partition_heads(segs) -> Tuple[int, int]:

@@ -115,25 +115,26 @@ def test_ulysses_gloo_world2_matches_single_process():
 # ---------------------------------------------------------------- round 2 --------
 def test_flat_partition_covers_items_once_and_balances():
     """The flattened (head, q-block) split: every item exactly once, in
-    head-major order, each rank floor/ceil of N / P items, segments are valid handles."""
+    head-major order, each rank floor/ceil of N / P items, one handle per rank whose item
+    range lies inside its heads."""
     for H, NQ, P in [(12, 256, 8), (40, 591, 8), (3, 5, 2), (12, 256, 1), (5, 7, 3),
                      (24, 929, 8), (1, 3, 4)]:
         items = []
         for r in range(P):
             segs = pdist.flat_partition(H, NQ, P, r)
+            assert len(segs) <= 1
             mine = []
             for h, n, a, b in segs:
-                assert (a, b) == (0, 0) or (n == 1 and 0 <= a < b <= NQ)
-                a, b = (0, NQ) if (a, b) == (0, 0) else (a, b)
-                mine += [(hh, i) for hh in range(h, h + n) for i in range(a, b)]
+                a, b = (0, n * NQ) if (a, b) == (0, 0) else (a, b)
+                assert 0 <= a < b <= n * NQ
+                assert a < NQ and b > (n - 1) * NQ          # touches every one of its heads
+                mine += [divmod(h * NQ + it, NQ) for it in range(a, b)]
             assert len(mine) in (H * NQ // P, -(-H * NQ // P))
-            h0, nh = pdist.partition_heads(segs)
-            assert all(h0 <= hh < h0 + nh for hh, _ in mine)
             items += mine
         assert items == [(h, i) for h in range(H) for i in range(NQ)]
-    # Wan-1.3B over 8 ranks: 384 items each instead of 1 or 2 heads (256 or 512 items)
-    assert [sum((b or 256) - a if n == 1 else 256 * n for _, n, a, b in
-                pdist.flat_partition(12, 256, 8, r)) for r in range(8)] == [384] * 8
+    # Wan-1.3B over 8 ranks: 384 items each (1.5 heads) instead of 1 or 2 heads
+    assert [pdist.flat_partition(12, 256, 8, r)[0] for r in range(3)] == [
+        (0, 2, 0, 384), (1, 2, 128, 512), (3, 2, 0, 384)]
 
 
 def _chunked_worker(rank, world, port, q, k, v, ref, chunks, errs):

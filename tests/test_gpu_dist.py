@@ -49,11 +49,13 @@ def _run(P, q, k, v, cfg, budget, seed=42, step=25, out=None):
 
 
 @pytest.mark.parametrize("dtype,Bq,rng", [
-    (torch.bfloat16, 128, (3, 17)), (torch.bfloat16, 128, (30, 33)),   # last one ragged
+    (torch.bfloat16, 128, (3, 17)), (torch.bfloat16, 128, (30, 33)),   # head 0, ragged last
+    (torch.bfloat16, 128, (30, 40)),                                    # across the heads
     (torch.bfloat16, 256, (2, 9)), (torch.float32, 128, (0, 5)),        # q256 / SIMT kernels
-    (torch.bfloat16, 128, (0, 33)),                                     # the full range
+    (torch.bfloat16, 128, (0, 66)),                                     # the full range
 ])
 def test_qblock_range_equals_full_run(pasa, dtype, Bq, rng):
+    """Item ranges [a, b) of the handle's (head, q-block) list, item = h * N_Q + i."""
     P = pasa
     B, S, H, D = 1, 4100, 2, 128
     q, k, v = synth.video_qkv(B, (1, 1, S), H, D, seed=11, dtype=dtype, device="cuda")
@@ -61,20 +63,23 @@ def test_qblock_range_equals_full_run(pasa, dtype, Bq, rng):
     full_r, full_o = _run(P, q, k, v, P.RouteCfg(Bq=Bq, G=32, beta=0.1), budget)
     a, b = rng
     NQ = full_r.NQ
-    b = min(b, NQ)
+    b = min(b, H * NQ)
     out = torch.full_like(q, float("nan"))
     part_r, out = _run(P, q, k, v, P.RouteCfg(Bq=Bq, G=32, beta=0.1, qb_begin=a, qb_end=b),
                        budget, out=out)
     got, want = part_r.read(), full_r.read()
     kk = got["k"]
     assert kk == want["k"]
-    assert np.array_equal(got["idx"][:, a:b, :kk], want["idx"][:, a:b, :kk])
-    for key in ("count", "mask"):
-        assert np.array_equal(got[key][:, a:b], want[key][:, a:b]), key
-    t0, t1 = a * Bq, min(b * Bq, S)
-    assert torch.equal(out[:, t0:t1], full_o[:, t0:t1])
-    outside = torch.cat([out[:, :t0], out[:, t1:]], 1)
-    assert torch.isnan(outside.float()).all(), "rows outside the range were written"
+    inside = torch.zeros(B, S, H, dtype=torch.bool)
+    for it in range(a, b):
+        h, i = divmod(it, NQ)
+        assert np.array_equal(got["idx"][h, i, :kk], want["idx"][h, i, :kk])
+        for key in ("count", "mask"):
+            assert np.array_equal(got[key][h, i], want[key][h, i]), key
+        t0, t1 = i * Bq, min((i + 1) * Bq, S)
+        assert torch.equal(out[:, t0:t1, h], full_o[:, t0:t1, h])
+        inside[:, t0:t1, h] = True
+    assert torch.isnan(out.float()[~inside.cuda()]).all(), "rows outside the range were written"
 
 
 def test_qblock_range_rejects_bad_ranges(pasa):
@@ -82,7 +87,7 @@ def test_qblock_range_rejects_bad_ranges(pasa):
     with pytest.raises(P.PasaError):
         P.Route(1, 4100, 1, 128, P.RouteCfg(qb_begin=5, qb_end=5))
     with pytest.raises(P.PasaError):
-        P.Route(1, 4100, 1, 128, P.RouteCfg(qb_begin=0, qb_end=34))
+        P.Route(1, 4100, 1, 128, P.RouteCfg(qb_begin=0, qb_end=34))   # 33 items
 
 
 def test_sharded_budget_matches_unsharded_and_oracle(pasa):
@@ -210,9 +215,13 @@ def test_two_ranks_reproduce_single_process(pasa, mode):
             assert torch.equal(o, ref[:, a:b]), r
     else:
         got = torch.full_like(ref, float("nan"))
+        NQ = (ref.shape[1] + 127) // 128
         for r in range(2):
             segs, o = res[r]
             for h, nh, a, b in segs:
-                t0, t1 = (a * 128, min(b * 128, ref.shape[1])) if (a, b) != (0, 0) else (0, ref.shape[1])
-                got[:, t0:t1, h:h + nh] = o[:, t0:t1, h:h + nh]
+                a, b = (0, nh * NQ) if (a, b) == (0, 0) else (a, b)
+                for it in range(a, b):
+                    hh, i = divmod(h * NQ + it, NQ)
+                    t0, t1 = i * 128, min((i + 1) * 128, ref.shape[1])
+                    got[:, t0:t1, hh] = o[:, t0:t1, hh]
         assert torch.equal(got, ref)
