@@ -381,7 +381,9 @@ def run_pasa(args):
         la = (rank * n_lat // world) // 4 * 4
         lb = n_lat if rank == world - 1 else ((rank + 1) * n_lat // world) // 4 * 4
         xs_sh = [x.reshape(-1)[la:lb] for x in (x_t, x_tm1, x_tm2)]
-        n_chunks_u = args.ulysses_chunks or max(c for c in (1, 2, 3, 4) if (H // world) % c == 0)
+        # chunks only pay with a transfer to overlap: one at N = 1
+        n_chunks_u = args.ulysses_chunks or (
+            1 if world == 1 else max(c for c in (1, 2, 3, 4) if (H // world) % c == 0))
         uly = pdist.Ulysses(B, S, H, D, q.dtype, dev, chunks=n_chunks_u)
         chunk_routes = {}
         chunk_ev = []   # per chunk: [before route, after route, after stats, after attn]
