@@ -530,6 +530,32 @@ def run_pasa(args):
         except Exception as exc:  # report, do not hide, a capture failure
             graph = {"error": f"{type(exc).__name__}: {exc}"[:300]}
 
+    # ---------------- the budget kernel inside a CUDA graph of repeated calls ---------
+    # (a launch-scale kernel, timed without launch gaps)
+    budget_graph = None
+    if not args.no_graph and not seq_sharded:
+        try:
+            reps = 50
+            gb = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gb):
+                for _ in range(reps):
+                    budget(x_t, x_tm1, x_tm2, **bkw)
+            gb.replay()
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record()
+            for _ in range(5):
+                gb.replay()
+            b1.record()
+            torch.cuda.synchronize()
+            us = b0.elapsed_time(b1) * 1e3 / (5 * reps)
+            nbytes = 3 * x_t.numel() * x_t.element_size()
+            budget_graph = {"us_per_call": us, "bytes": nbytes,
+                            "gbs": nbytes / (us * 1e-6) / 1e9,
+                            "note": f"{reps} pasa_budget calls captured in one CUDA graph"}
+        except Exception as exc:  # report, do not hide, a capture failure
+            budget_graph = {"error": f"{type(exc).__name__}: {exc}"[:200]}
+
     # ---------------- context: dense attention on the same shapes (library SDPA) -----
     dense = None
     if not args.no_dense and rank == 0:
@@ -756,6 +782,7 @@ def run_pasa(args):
         "gpu_launches": gpu_launches,
         "e2e": e2e,
         "graph": graph,
+        "budget_graph": budget_graph,
         "schedule": schedule,
         "dense_context": dense,
         "cpu_baseline": cpu,

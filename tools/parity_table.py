@@ -13,7 +13,8 @@ print("# GPU parity: achieved errors of every compared output\n")
 print("Written by `pytest tests -m gpu` (tests/conftest.py `parity_log`); reference = the fp64 "
       "oracle on the GPU route (`oracle`) or fp32 dense attention for the constant-key-block "
       "cases (`dense`).  Contract: max|dO|/max|O| <= 2e-2 (bf16 I/O), <= 1e-5 (fp32 I/O); "
-      "regression bound asserted by the tests: 8e-3 (bf16), 1e-5 (fp32).\n")
+      "regression bound asserted by the tests: 8e-3 (bf16), 1e-5 (fp32).  FP8 QK^T variant "
+      "(R-30): its own bound 1e-1 max / 6e-2 Frobenius.\n")
 print("| case | ref | max\\|dO\\|/max\\|O\\| | rel. Frobenius | bound | test |")
 print("|---|---|---|---|---|---|")
 for r in sorted(rows, key=lambda r: -r["max_rel"]):
