@@ -301,10 +301,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mma_ts_elect(o, a0 + kk * 8, bd, kIdF, 1u);
                     }
                 }
+                // the slot releases precede tile 1's pv_done: the last asynchronous arrival
+                // of the CTA is then one the softmax warps wait for before the epilogue (a
+                // commit still in flight at exit would land in the next CTA's barriers)
+                if (t == 1) {
+                    if (f_op) mma_commit_elect(&ctl.k_empty[s]);
+                    mma_commit_elect(&ctl.v_empty[s]);
+                }
                 mma_commit_elect(&ctl.pv_done[t][s]);
             }
-            if (f_op) mma_commit_elect(&ctl.k_empty[s]);
-            mma_commit_elect(&ctl.v_empty[s]);
             __syncwarp();
         }
     } else if (warp >= 4) {

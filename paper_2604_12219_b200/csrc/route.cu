@@ -400,6 +400,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     const int64_t ilo = max(a.it0 - bh * a.NQ, (int64_t)0), ihi = min(a.it1 - bh * a.NQ, a.NQ);
     const int rlo = (int)max(ilo - i0, (int64_t)0);
     const int nrows = (int)max(min((int64_t)R, ihi - i0), (int64_t)0);   // rows < nrows exist
+    if (blockIdx.x == 0 && bh == 0 && threadIdx.x == 0)   // k of this route, for pasa_route_read
+        a.hdr[0] = device_k(a.rec, (int)a.NK);            // (written even if CTA (0, 0) has no item)
     if (rlo >= nrows) return;                       // no item of this CTA is in range
     double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(sq + R * (D + 4));    // [NW][64]
@@ -407,7 +409,6 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
                          : a.gsc + (bh * a.NQ + i0) * (int64_t)NKP;     // [R][NKP]
 
     const int k = device_k(a.rec, NK);
-    if (blockIdx.x == 0 && bh == 0 && tid == 0) a.hdr[0] = k;
     const int M = (NK + 31) >> 5;
     if (k >= NK) {   // dense step / full budget: every block exact, no scores needed
         if (warp >= rlo && warp < nrows) {   // (one row per warp: R = 8)

@@ -42,6 +42,7 @@ def _budget(P, rho=0.15, step=25, T=50):
 def _run(P, q, k, v, cfg, budget, seed=42, step=25, out=None):
     B, S, H, D = q.shape
     r = P.Route(B, S, H, D, cfg)
+    r.ws.fill_(0xFF)          # poisoned workspace: nothing may rely on a stale value
     r(q, k, budget, seed, step)
     out = P.attn(q, k, v, r, out)
     torch.cuda.synchronize()

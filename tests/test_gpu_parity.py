@@ -47,6 +47,7 @@ def check_route(P, q, k, cfg, rho, seed=42, step=25, heads=None):
     """Build the GPU route and compare it with the oracle; returns (route, read)."""
     B, S, H, D = q.shape
     route = P.Route(B, S, H, D, cfg)
+    route.ws.fill_(0xFF)      # poisoned workspace (fp64 NaN, int -1): no stale value can pass
     budget = make_budget(P, rho, step)
     route(q, k, budget, seed, step)
     got = route.read()
