@@ -247,9 +247,11 @@ __device__ const LogEnt g_logtab[128] = PASA_LOGTAB_INIT;
 // which the oracle uses, is within 0.52: r~ moves by ~1e-16 relative, inside the
 // documented-tie margin).  Word j mod 4 of counter (floor(j/4), i, gh, step) serves block j
 // (R-11): one Philox call per four blocks.
-__device__ __forceinline__ double gumbel_of(uint32_t x) {
+// `tab`: the log table staged in shared memory by the calling CTA (in L1 it was evicted by
+// the streamed K-bar fragments: its loads were the fused kernel's top stall)
+__device__ __forceinline__ double gumbel_of(uint32_t x, const LogEnt* tab) {
     const double u = __dmul_rn(__dadd_rn((double)x, 0.5), 2.3283064365386963e-10);
-    return -fastlog_tab(g_logtab, -fastlog_tab(g_logtab, u));
+    return -fastlog_tab(tab, -fastlog_tab(tab, u));
 }
 
 // The k-th largest orderable key T of one row (the largest value with #{key >= T} >= k),
@@ -405,7 +407,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     if (rlo >= nrows) return;                       // no item of this CTA is in range
     double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
     uint64_t* cbuf = reinterpret_cast<uint64_t*>(sq + R * (D + 4));    // [NW][64]
-    double* sc = SMEM_SC ? reinterpret_cast<double*>(cbuf + NW * 64)
+    LogEnt* ltab = reinterpret_cast<LogEnt*>(cbuf + NW * 64);           // [128] log table
+    double* sc = SMEM_SC ? reinterpret_cast<double*>(ltab + 128)
                          : a.gsc + (bh * a.NQ + i0) * (int64_t)NKP;     // [R][NKP]
 
     const int k = device_k(a.rec, NK);
@@ -435,6 +438,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
         const int r = e / D, c = e % D;
         sq[r * (D + 4) + c] = r >= rlo && r < nrows ? Q[(int64_t)r * D + c] : 0.0;
     }
+    for (int e = tid; e < 128 * (int)sizeof(LogEnt) / 16; e += NT)
+        reinterpret_cast<uint4*>(ltab)[e] = reinterpret_cast<const uint4*>(g_logtab)[e];
     __syncthreads();
     {
         const int fr = lane >> 2, fk = lane & 3;
@@ -547,7 +552,7 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
             if (j < NK) {
                 double xv = row[j];
                 if (biased)   // R5: rt = r + (beta sigma_i) g, two rounded operations
-                    xv = __dadd_rn(xv, __dmul_rn(bi, gumbel_of(xw[w])));
+                    xv = __dadd_rn(xv, __dmul_rn(bi, gumbel_of(xw[w], ltab)));
                 kx[w] = orderable(xv);
             }
         }
@@ -590,7 +595,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
 }
 
 constexpr size_t fused_fixed_smem(int R, int D) {
-    return sizeof(double) * (size_t)R * (D + 4) + sizeof(uint64_t) * R * 64;
+    return sizeof(double) * (size_t)R * (D + 4) + sizeof(uint64_t) * R * 64 +
+           sizeof(LogEnt) * 128;
 }
 
 }  // namespace
