@@ -69,12 +69,10 @@ __device__ __forceinline__ float group_max(float v, int ng, int lane) {
 // F8 (the FP8 QK^T variant): also the E4M3 copy of Q with per-row scales (the ng = D / 8
 // threads of a block are adjacent lanes: one group max per token) and the per-head
 // max |K|, max |Kbar|; the ng-lane groups are whole (total, q_tasks multiples of ng)
+// one thread's pool task (task < q_tasks: Q, else K)
 template <typename T, bool F8>
-// 4 CTAs (32 warps) per SM: at 3 (70 registers) the kernel lost 40% of its bandwidth
-__global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, int64_t q_tasks,
-                                                   int64_t total) {
-    int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (task >= total) return;
+__device__ __forceinline__ void pool_task(const PoolArgs& qa, const PoolArgs& ka, int64_t q_tasks,
+                                          int64_t task) {
     const PoolArgs& a = task < q_tasks ? qa : ka;
     if (task >= q_tasks) task -= q_tasks;
     int64_t ng = a.D / 8;
@@ -170,6 +168,14 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
             }
         }
     }
+}
+
+template <typename T, bool F8>
+// 4 CTAs (32 warps) per SM: at 3 (70 registers) the kernel lost 40% of its bandwidth
+__global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, int64_t q_tasks,
+                                                   int64_t total) {
+    const int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (task < total) pool_task<T, F8>(qa, ka, q_tasks, task);
 }
 
 // ---------------------------------------------------------------------------
@@ -386,9 +392,10 @@ __device__ __forceinline__ void select_row_mem(const uint64_t* key, int NK, int 
 }
 
 // HR > 0 (N_K <= 32 HR): the high words of a row's keys stay in registers for the search
+// One CTA's route tile: 8 query-block rows `tile` of head bh.
 template <int R, int D, bool SMEM_SC, int HR>
-__global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a) {
-    extern __shared__ __align__(16) unsigned char f_smem[];
+__device__ __forceinline__ void route_tile(const FusedArgs& a, int64_t bh, int64_t tile,
+                                           unsigned char* f_smem) {
     constexpr int NT = 32 * R, NW = R;              // one warp per score row
     constexpr int RT = R / 8;                       // DMMA row tiles (all in every warp)
     constexpr int CG = kFCG4 / RT;                  // column tiles per work group
@@ -396,13 +403,12 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     static_assert(KB % 2 == 0, "ping-pong blocks must pair up inside a group");
     const int NK = (int)a.NK, NKP = a.NKP;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t bh = blockIdx.y;
     // rows of this CTA inside the item range: [rlo, rhi) of i0 .. i0 + R - 1
-    const int64_t i0 = (int64_t)blockIdx.x * R;
+    const int64_t i0 = tile * R;
     const int64_t ilo = max(a.it0 - bh * a.NQ, (int64_t)0), ihi = min(a.it1 - bh * a.NQ, a.NQ);
     const int rlo = (int)max(ilo - i0, (int64_t)0);
     const int nrows = (int)max(min((int64_t)R, ihi - i0), (int64_t)0);   // rows < nrows exist
-    if (blockIdx.x == 0 && bh == 0 && threadIdx.x == 0)   // k of this route, for pasa_route_read
+    if (tile == 0 && bh == 0 && threadIdx.x == 0)   // k of this route, for pasa_route_read
         a.hdr[0] = device_k(a.rec, (int)a.NK);            // (written even if CTA (0, 0) has no item)
     if (rlo >= nrows) return;                       // no item of this CTA is in range
     double* sq = reinterpret_cast<double*>(f_smem);                    // [R][D + 4]
@@ -456,8 +462,8 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
                 const bool ok = ct * 8 + fr < NK;
 #pragma unroll
                 for (int q = 0; q < kFKS / 2; ++q) {
-                    const double2 v = ok ? __ldg(KF + ((int64_t)ct * (D / 8) + kb * (kFKS / 2) + q) * 32)
-                                         : make_double2(0.0, 0.0);
+                    const double2* src = KF + ((int64_t)ct * (D / 8) + kb * (kFKS / 2) + q) * 32;
+                    const double2 v = ok ? __ldg(src) : make_double2(0.0, 0.0);
                     bb[2 * q][c] = v.x;
                     bb[2 * q + 1][c] = v.y;
                 }
@@ -594,6 +600,12 @@ __global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a
     }
 }
 
+template <int R, int D, bool SMEM_SC, int HR>
+__global__ void __launch_bounds__(32 * R, 16 / R) route_fused_kernel(FusedArgs a) {
+    extern __shared__ __align__(16) unsigned char f_smem[];
+    route_tile<R, D, SMEM_SC, HR>(a, blockIdx.y, blockIdx.x, f_smem);
+}
+
 constexpr size_t fused_fixed_smem(int R, int D) {
     return sizeof(double) * (size_t)R * (D + 4) + sizeof(uint64_t) * R * 64 +
            sizeof(LogEnt) * 128;
@@ -624,7 +636,6 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
         pool_kernel<__nv_bfloat16, true><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
     else
         pool_kernel<__nv_bfloat16, false><<<pgrid, 256, 0, st>>>(qa, ka, q_tasks, total);
-
     const double* prior = nullptr;
     if (v) {
         cudaError_t e = launch_het(k, *v, r, st, launches);
@@ -673,6 +684,8 @@ int route_rows_per_cta(int64_t NK, int64_t D) {
 }
 
 int64_t route_score_stride(int64_t NK) { return NK | 1; }
+
+
 
 
 
