@@ -75,8 +75,10 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // row tiles [w RTW, (w+1) RTW) x every column tile (32 8x8 tiles, 64 fp64 accumulators
 // per thread).  Fragments (PTX m8n8k4.f64): A[r][n] lane (r = lane/4, n = lane%4),
 // B[n][c] lane (n = lane%4, c = lane/4), C[r][c] lane (r = lane/4, c = 2(lane%4)+{0,1}).
-// The DMMA's internal rounding differs from a sequential fma chain by ~1e-16 relative:
-// the prior's tolerance against the oracle is 1e-10 (R-26).
+// Each DMMA step rounds like the sequential fma chain over its four k (tools/dmma_exact.cu),
+// but the token sum here runs unit-wise over centred rows in a different grouping from the
+// oracle's (and the Frobenius norm sums in another order), so H_j and het_j differ from the
+// oracle's by ~1e-16 relative: the prior's tolerance against the oracle is 1e-10 (R-26).
 template <typename T, int D>
 __global__ void __launch_bounds__(D * D / 64, 1) het_hj_kernel(HetArgs a) {
     constexpr int NT = D * D / 64;                   // threads: 256 at d = 128, 64 at d = 64

@@ -182,8 +182,11 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
 // shared helpers of the fused kernel
 // ---------------------------------------------------------------------------
 // fp64 tensor core: d (+)= a * b on an 8x8x4 tile.  Measured on this pool
-// (tools/dmma_exact.cu): bit-identical to the sequential fma chain over k = 0..3, so
-// a chain of these in ascending k is the oracle's ascending-d fma chain (R2).
+// (tools/dmma_exact.cu, 0 of 38 M outputs differ): bit-identical to the sequential fma
+// chain over k = 0..3, so a chain of these in ascending k reproduces the oracle's
+// ascending-d fma chain (R2).  PTX does not promise that rounding, so the parity contract
+// the tests check is the tie-tolerant one (a route may differ only where two
+// oracle scores tie within 1e-6 relative); the observed tie count is 0.
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
