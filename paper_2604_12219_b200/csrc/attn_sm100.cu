@@ -46,6 +46,13 @@ constexpr float kRescaleThresh = 8.f; // log2 units
 #ifndef PASA_D64_POLY
 #define PASA_D64_POLY 0
 #endif
+// d = 64: Q copied into TMEM once per CTA so QK^T is a TS MMA (only the K tile is read
+// from shared memory: the SS MMA at N = 64 is shared-memory bound), two S buffers instead
+// of three to make room (O 64 + S 2 x 64 + Q 32 columns)
+#ifndef PASA_D64_QTMEM
+#define PASA_D64_QTMEM 1
+#endif
+constexpr bool kD64QT = PASA_D64_QTMEM != 0;
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
 __device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
@@ -58,8 +65,10 @@ __device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0x3FFF; }
 // columns), 3 at d = 64 (O 64 + 3 x 64) -- QK of op n+NB-1 is issued before PV of op n.
 template <int D>
 struct Geo {
-    static constexpr int NB = D == 128 ? 2 : 3;
+    static constexpr bool QT = D == 64 && kD64QT;   // Q in TMEM (see kD64QT)
+    static constexpr int NB = D == 128 ? 2 : (QT ? 2 : 3);
     static constexpr uint32_t COLS = D == 128 ? 128 : 64;   // first S buffer column
+    static constexpr uint32_t QCOL = 192;           // QT: Q's 32 columns after the S buffers
     static constexpr int NBOX = D / 64;
     static constexpr int QBOX = kBQ * 128;          // bytes per 64-col box of Q
     static constexpr int KVBOX = kBK * 128;         // bytes per 64-col box of a K/V tile
@@ -104,7 +113,7 @@ enum { TR_KPROD = 0, TR_VPROD, TR_MMA_P, TR_MMA_V, TR_MMA_QK, TR_SA_W, TR_SA_OK,
     } while (0)
 
 struct Ctl {
-    uint64_t q_full;
+    uint64_t q_full, q_tmem;
     uint64_t k_full[3], k_empty[3], s_full[3];   // per K slot / S buffer (n % NB)
     // p_full per S buffer (n % NB): P ready + V landed.  With NB = 3 the softmax can finish
     // op n+2 before V(n) has even been requested (QK(n+2) is issued before PV(n)), so a
@@ -158,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2)
     for (int q = tid; q < cnt; q += blockDim.x) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
     if (tid == 0) {
         mbar_init(&ctl.q_full, 1);
+        mbar_init(&ctl.q_tmem, 128);          // QT: the softmax threads copied Q into TMEM
         for (int s = 0; s < G_::NB; ++s) {
             mbar_init(&ctl.k_full[s], 1);
             mbar_init(&ctl.k_empty[s], 1);
@@ -319,6 +329,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 for (int kk = 0; kk < D / 32; ++kk)
                     mma_ss_f8_elect(d, dq0 + ((kk * 32) >> 4),
                                     dk0 + ((s * G_::SLOT + kk * 32) >> 4), kIdQK8, kk > 0);
+            } else if constexpr (G_::QT) {   // A = Q from TMEM (8 columns per 16 elements)
+#pragma unroll
+                for (int kk = 0; kk < D / 16; ++kk) {
+                    const uint32_t offk = (s * G_::SLOT + (kk >> 2) * G_::KVBOX + (kk & 3) * 32) >> 4;
+                    mma_ts_elect(d, tbase + G_::QCOL + kk * 8, dk0 + offk, kIdQK, kk > 0);
+                }
             } else {
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
@@ -332,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (lane == 0) PASA_TR(TR_MMA_QK, n);
             __syncwarp();
         };
-        mbar_wait_sleep(&ctl.q_full, 0);
+        mbar_wait_sleep(G_::QT ? &ctl.q_tmem : &ctl.q_full, 0);
         tc_fence_after();
         for (int m = 0; m < G_::NB - 1 && m < nops; ++m)
             if (op_type(ctl.ops[m]) != OP_F) issue_qk(m);
@@ -376,6 +392,19 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t t_o = tbase + lane_off;
         const uint8_t* qrow = smem + G_::OFF_Q;
+        if constexpr (G_::QT) {   // Q row r -> TMEM lane r, columns QCOL..QCOL+31 (bf16 pairs)
+            mbar_wait_sleep(&ctl.q_full, 0);
+            uint32_t qa[32];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) {
+                const uint4 u = *reinterpret_cast<const uint4*>(qrow + r * 128 + ((cc ^ (r & 7)) << 4));
+                qa[cc * 4 + 0] = u.x; qa[cc * 4 + 1] = u.y; qa[cc * 4 + 2] = u.z; qa[cc * 4 + 3] = u.w;
+            }
+            tmem_st32(t_o + G_::QCOL, qa);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&ctl.q_tmem);
+        }
         float m = -INFINITY, l = 0.f;
         float A_cur = 0.f, A_done = 0.f;
         int g_cur = -1, g_done = -1;          // group of the running / last closed A sum
