@@ -53,6 +53,12 @@ constexpr float kRescaleThresh = 8.f; // log2 units
 #define PASA_D64_QTMEM 1
 #endif
 constexpr bool kD64QT = PASA_D64_QTMEM != 0;
+// d = 128 (A/B knob): Q in TMEM as well, which leaves room for ONE S buffer (O 128 + S 64 +
+// Q 64 columns): QK of op n+1 then follows PV of op n (a serial chain per CTA)
+#ifndef PASA_D128_QTMEM
+#define PASA_D128_QTMEM 0
+#endif
+constexpr bool kD128QT = PASA_D128_QTMEM != 0;
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
 __device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
@@ -65,10 +71,11 @@ __device__ __forceinline__ int32_t op_val(int32_t op) { return op & 0x3FFF; }
 // columns), 3 at d = 64 (O 64 + 3 x 64) -- QK of op n+NB-1 is issued before PV of op n.
 template <int D>
 struct Geo {
-    static constexpr bool QT = D == 64 && kD64QT;   // Q in TMEM (see kD64QT)
-    static constexpr int NB = D == 128 ? 2 : (QT ? 2 : 3);
+    static constexpr bool QT = D == 64 ? kD64QT : kD128QT;   // Q in TMEM
+    static constexpr int NB = D == 128 ? (QT ? 1 : 2) : (QT ? 2 : 3);   // S buffers
+    static constexpr int NKS = NB < 2 ? 2 : NB;     // K ring slots
     static constexpr uint32_t COLS = D == 128 ? 128 : 64;   // first S buffer column
-    static constexpr uint32_t QCOL = 192;           // QT: Q's 32 columns after the S buffers
+    static constexpr uint32_t QCOL = 192;           // QT: Q's D/2 columns after the S buffers
     static constexpr int NBOX = D / 64;
     static constexpr int QBOX = kBQ * 128;          // bytes per 64-col box of Q
     static constexpr int KVBOX = kBK * 128;         // bytes per 64-col box of a K/V tile
@@ -76,7 +83,7 @@ struct Geo {
     static constexpr int HTBOX = D * 128;           // bytes per 64-col box of Hbar^T
     static constexpr int OFF_Q = 0;
     static constexpr int OFF_K = kBQ * D * 2;
-    static constexpr int OFF_V = OFF_K + NB * SLOT;
+    static constexpr int OFF_V = OFF_K + NKS * SLOT;
     static constexpr int BYTES = OFF_V + 2 * SLOT;
     static_assert(HTBOX <= SLOT, "an Hbar^T box must fit one ring slot");
 };
@@ -121,6 +128,8 @@ struct Ctl {
     // let PV(n) read an unloaded V tile; one barrier per S buffer cannot be lapped, since
     // QK(n+NB) follows PV(n).  pv_done per V slot (n & 1): O-MMA done.
     uint64_t p_full[3], pv_done[2];
+    uint64_t v_full[2];   // NB = 1 only: the V tile of op n (slot n & 1) landed (own barrier:
+                          // the V producer runs two ops ahead of the single P barrier)
     uint32_t tmem_base;
     int32_t nops;
     uint32_t mask[kMaxNK / 32];
@@ -168,13 +177,17 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (tid == 0) {
         mbar_init(&ctl.q_full, 1);
         mbar_init(&ctl.q_tmem, 128);          // QT: the softmax threads copied Q into TMEM
-        for (int s = 0; s < G_::NB; ++s) {
+        for (int s = 0; s < G_::NKS; ++s) {
             mbar_init(&ctl.k_full[s], 1);
             mbar_init(&ctl.k_empty[s], 1);
-            mbar_init(&ctl.s_full[s], 1);
         }
+        for (int s = 0; s < G_::NB; ++s) mbar_init(&ctl.s_full[s], 1);
         for (int s = 0; s < G_::NB; ++s)
-            mbar_init(&ctl.p_full[s], 129);   // 128 softmax threads + the V producer (expect_tx)
+            mbar_init(&ctl.p_full[s], G_::NB == 1 ? 128 : 129);   // softmax threads + V producer
+        if (G_::NB == 1) {
+            mbar_init(&ctl.v_full[0], 1);
+            mbar_init(&ctl.v_full[1], 1);
+        }
         mbar_init(&ctl.pv_done[0], 1);
         mbar_init(&ctl.pv_done[1], 1);
         fence_barrier_init();
@@ -240,8 +253,8 @@ __global__ void __launch_bounds__(kThreads, 2)
                                 (int)(i * kBQ), (int)h, (int)b);
             }
             for (int n = 0; n < nops; ++n) {
-                const int s = n % G_::NB;
-                mbar_wait_sleep(&ctl.k_empty[s], ((n / G_::NB) & 1) ^ 1);
+                const int s = n % G_::NKS;
+                mbar_wait_sleep(&ctl.k_empty[s], ((n / G_::NKS) & 1) ^ 1);
                 uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
@@ -274,28 +287,29 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (lane == 0) {
             for (int n = 0; n < nops; ++n) {
                 const int s = n & 1, pb = n % G_::NB;
+                uint64_t* vbar = G_::NB == 1 ? &ctl.v_full[s] : &ctl.p_full[pb];
                 mbar_wait_sleep(&ctl.pv_done[s], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
                 uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
                 const int32_t op = ctl.ops[n];
                 const int v = op_val(op);
                 if (DIAG && (p.dbg & 2)) {
-                    mbar_arrive(&ctl.p_full[pb]);
+                    mbar_arrive(vbar);
                 } else if (op_type(op) == OP_F) {
                     if (G_::NBOX == 2) {
-                        mbar_arrive_expect_tx(&ctl.p_full[pb], G_::HTBOX);
-                        tma_load_3d(dst, &tmHt, &ctl.p_full[pb], 64, v * D, (int)bh);
+                        mbar_arrive_expect_tx(vbar, G_::HTBOX);
+                        tma_load_3d(dst, &tmHt, vbar, 64, v * D, (int)bh);
                     } else {
-                        mbar_arrive(&ctl.p_full[pb]);
+                        mbar_arrive(vbar);
                     }
                 } else {
-                    mbar_arrive_expect_tx(&ctl.p_full[pb], G_::SLOT);
+                    mbar_arrive_expect_tx(vbar, G_::SLOT);
 #pragma unroll
                     for (int a = 0; a < G_::NBOX; ++a) {
                         if (op_type(op) == OP_E)
-                            tma_load_4d(dst + a * G_::KVBOX, &tmV, &ctl.p_full[pb], 64 * a, v * kBK,
+                            tma_load_4d(dst + a * G_::KVBOX, &tmV, vbar, 64 * a, v * kBK,
                                         (int)h, (int)b);
                         else
-                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, &ctl.p_full[pb], 64 * a, v * 64,
+                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, vbar, 64 * a, v * 64,
                                         (int)bh);
                     }
                 }
@@ -315,14 +329,14 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint64_t dk0 = umma_desc_sw128(k_base, 16, 1024);
         const uint64_t dv0 = umma_desc_sw128(v_base, G_::KVBOX, 1024);
         auto issue_qk = [&](int n) {
-            const int s = n % G_::NB;
+            const int s = n % G_::NKS, sbuf = n % G_::NB;   // K ring slot, S buffer
             if (lane == 0) PASA_TR(TR_MMA_QKW, n);
-            mbar_wait_c(&ctl.k_full[s], (n / G_::NB) & 1, spin);
+            mbar_wait_c(&ctl.k_full[s], (n / G_::NKS) & 1, spin);
             if (lane == 0) PASA_TR(TR_SB_W, n);           // K(n) landed
             tc_fence_after();
             // the whole warp runs the issue code with warp-uniform operands; elect.sync
             // picks the issuing lane (no per-instruction elect loop)
-            const uint32_t d = tbase + G_::COLS + 64 * s;
+            const uint32_t d = tbase + G_::COLS + 64 * sbuf;
             if constexpr (F8) {   // E4M3: 32 elements (bytes) of the 128-byte rows per MMA
                 constexpr uint32_t kIdQK8 = idesc_e4m3_f32(128, kBK, 0, 0);
 #pragma unroll
@@ -343,7 +357,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     mma_ss_elect(d, dq0 + offq, dk0 + offk, kIdQK, kk > 0);
                 }
             }
-            mma_commit_elect(&ctl.s_full[s]);
+            mma_commit_elect(&ctl.s_full[sbuf]);
             mma_commit_elect(&ctl.k_empty[s]);
             if (lane == 0) PASA_TR(TR_MMA_QK, n);
             __syncwarp();
@@ -359,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             // V(n) lands on p_full[s] too (one wait for "P ready and V loaded")
             if (lane == 0) PASA_TR(TR_MMA_V, n);
             mbar_wait_c(&ctl.p_full[sb], (n / G_::NB) & 1, spin);
+            if (G_::NB == 1) mbar_wait_c(&ctl.v_full[s], (n >> 1) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_P, n);
             tc_fence_after();
             const int32_t op = ctl.ops[n];
@@ -372,16 +387,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                 mma_commit_elect(&ctl.pv_done[s]);
                 if (lane == 0) PASA_TR(TR_KPROD_W, n);
             } else {
-                mbar_wait_c(&ctl.k_full[sb], (n / G_::NB) & 1, spin);
+                const int sk = n % G_::NKS;   // the K slot holding H-bar^T box 0
+                mbar_wait_c(&ctl.k_full[sk], (n / G_::NKS) & 1, spin);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
-                    const uint32_t box = (kk >> 2) == 0 ? k_base + sb * G_::SLOT
+                    const uint32_t box = (kk >> 2) == 0 ? k_base + sk * G_::SLOT
                                                         : v_base + s * G_::SLOT;
                     const uint64_t bd = umma_desc_sw128(box + (kk & 3) * 32, 16, 1024);
                     mma_ts_elect(tbase, tbase + G_::COLS + 64 * sb + kk * 8, bd, kIdF, 1u);
                 }
-                mma_commit_elect(&ctl.k_empty[sb]);
+                mma_commit_elect(&ctl.k_empty[sk]);
                 mma_commit_elect(&ctl.pv_done[s]);
             }
             __syncwarp();
@@ -392,15 +408,20 @@ __global__ void __launch_bounds__(kThreads, 2)
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t t_o = tbase + lane_off;
         const uint8_t* qrow = smem + G_::OFF_Q;
-        if constexpr (G_::QT) {   // Q row r -> TMEM lane r, columns QCOL..QCOL+31 (bf16 pairs)
+        if constexpr (G_::QT) {   // Q row r -> TMEM lane r, columns QCOL.. (bf16 pairs)
             mbar_wait_sleep(&ctl.q_full, 0);
-            uint32_t qa[32];
 #pragma unroll
-            for (int cc = 0; cc < 8; ++cc) {
-                const uint4 u = *reinterpret_cast<const uint4*>(qrow + r * 128 + ((cc ^ (r & 7)) << 4));
-                qa[cc * 4 + 0] = u.x; qa[cc * 4 + 1] = u.y; qa[cc * 4 + 2] = u.z; qa[cc * 4 + 3] = u.w;
+            for (int a = 0; a < G_::NBOX; ++a) {
+                uint32_t qa[32];
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    const uint4 u = *reinterpret_cast<const uint4*>(qrow + a * G_::QBOX + r * 128 +
+                                                                    ((cc ^ (r & 7)) << 4));
+                    qa[cc * 4 + 0] = u.x; qa[cc * 4 + 1] = u.y; qa[cc * 4 + 2] = u.z;
+                    qa[cc * 4 + 3] = u.w;
+                }
+                tmem_st32(t_o + G_::QCOL + 32 * a, qa);
             }
-            tmem_st32(t_o + G_::QCOL, qa);
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&ctl.q_tmem);
@@ -635,7 +656,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 // may still be at op n-3's phase -- a wait for n-1 would then pass at once
                 // (the round-1 d = 64 hang / NaN under changed softmax timing).  Op n-2 is
                 // safe: its predecessor on the barrier, n-4, is complete.
-                consume_op(n - 2);
+                consume_op(G_::NB == 1 ? n - 1 : n - 2);   // NB = 1: the buffer held P(n - 1)
                 tc_fence_after();
 #pragma unroll
                 for (int a = 0; a < G_::NBOX; ++a) {
