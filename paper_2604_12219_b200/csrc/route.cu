@@ -678,12 +678,20 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
     return e;
 }
 
+// A/B knob: score rows in shared memory at one CTA per SM when two do not fit (measured
+// at HunyuanVideo, N_K = 1,857: 1.638 ms vs 1.607 ms for two CTAs per SM with the rows in
+// the L2-resident workspace scratch -- off)
+#ifndef PASA_ROUTE_SMEM1
+#define PASA_ROUTE_SMEM1 0
+#endif
+
 int route_rows_per_cta(int64_t NK, int64_t D) {
     // 8 rows (one DMMA row tile) per CTA, two CTAs per SM: 113 KB of shared memory each
     // (16 rows at one CTA per SM measured the same at Wan-14B: 1.142 vs 1.137 ms)
     const size_t nkp = (size_t)route_score_stride(NK);
-    return fused_fixed_smem(kFRows, (int)D) + sizeof(double) * kFRows * nkp <= 113 * 1024 ? kFRows
-                                                                                        : 0;
+    const size_t need = fused_fixed_smem(kFRows, (int)D) + sizeof(double) * kFRows * nkp;
+    const size_t cap = PASA_ROUTE_SMEM1 ? 227 * 1024 : 113 * 1024;
+    return need <= cap ? kFRows : 0;
 }
 
 int64_t route_score_stride(int64_t NK) { return NK | 1; }
