@@ -17,7 +17,8 @@ timeout 400 python bench.py --config cogvideox5b --schedule --no-cpu --no-e2e > 
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 python bench.py --config hunyuan_720p --gpus 2 --dist-backend gloo --no-cpu --steps 2 --no-dense --no-e2e > gpurun_out/bench_hy_gloo2.json 2> gpurun_out/bench_hy_gloo2.err
 timeout 900 python bench.py --config wan13b_480p --gpus 2 --partition flat --dist-backend gloo --no-cpu --steps 3 --no-dense --no-e2e > gpurun_out/bench_w13_flat_gloo2.json 2> gpurun_out/bench_w13_flat_gloo2.err
-for c in wan14b_720p wan13b_480p; do CFG=$c timeout 600 python tools/scaling_emulate.py > gpurun_out/scaling_$c.txt 2>&1; done
+timeout 900 python bench.py --gpus 2 --dist-backend gloo --no-cpu --steps 3 --no-dense --no-e2e > gpurun_out/bench_wan14b_gloo2.json 2> gpurun_out/bench_wan14b_gloo2.err
+for c in wan14b_720p wan13b_480p hunyuan_720p; do CFG=$c timeout 600 python tools/scaling_emulate.py > gpurun_out/scaling_$c.txt 2>&1; done
 CFG=wan13b_480p PART=heads timeout 600 python tools/scaling_emulate.py > gpurun_out/scaling_wan13b_480p_heads.txt 2>&1
 # launch list (serialised, cold cache: only the shares are comparable with bench.py)
 timeout 400 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \

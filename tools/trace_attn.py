@@ -49,6 +49,10 @@ def main():
 
     res = {e: col(e).tolist() for e in EV}
     json.dump(res, open(os.path.join(ROOT, "gpurun_out", "trace.json"), "w"))
+    raw = {e: np.where(tr[i] > 0, tr[i] - t0, -1).tolist() for i, e in enumerate(EV)}
+    json.dump(raw, open(os.path.join(ROOT, "gpurun_out", "trace_raw.json"), "w"))
+    if os.environ.get("RAW_ONLY"):
+        return
     sa_w, sa_ok, sa_arr = col("SA_W"), col("SA_OK"), col("SA_ARR")
     n = min(len(sa_ok), len(sa_arr))
     print("tile A ops:", len(sa_arr), "total cycles", int(sa_arr[-1]))
