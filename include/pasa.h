@@ -236,11 +236,18 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
  *   PASA_ATTN_STATS_ONLY   launch only the K/V statistics pass (Kbar, Vsum, Hbar^(g));
  *   PASA_ATTN_REUSE_STATS  skip the statistics pass: the caller guarantees that the
  *                          previous STATS_ONLY call on this route saw the same k, v.
+ *   PASA_ATTN_CTA_PAIR     Bq = 256 routes only: run the CTA-pair kernel (tcgen05
+ *                          cta_group::2, M = 256 over the two SMs of a TPC, each SM
+ *                          holding half of every K/V / statistics tile; SURVEY.md §8f
+ *                          NEXT 4) instead of the one-CTA two-tile kernel.  Same
+ *                          results up to fp32 summation order; d = 128 only, G as
+ *                          for Bq = 256; anything else returns EUNSUPPORTED.
  * STATS_ONLY followed by REUSE_STATS is exactly pasa_attn, split so that each
  * kernel can be timed on its own stream position. */
 #define PASA_ATTN_FORCE_SIMT 1u
 #define PASA_ATTN_STATS_ONLY 2u
 #define PASA_ATTN_REUSE_STATS 4u
+#define PASA_ATTN_CTA_PAIR 8u
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 

@@ -22,6 +22,7 @@ COMP = {"grouped": 0, "zeroth": 1, "none": 2}
 PASA_ATTN_FORCE_SIMT = 1
 PASA_ATTN_STATS_ONLY = 2
 PASA_ATTN_REUSE_STATS = 4
+PASA_ATTN_CTA_PAIR = 8
 PRIOR = {"none": 0, "global": 1, "group": 2}
 
 # every symbol include/pasa.h declares (tests check the library exports them all)

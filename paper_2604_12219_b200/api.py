@@ -250,15 +250,17 @@ class Route:
 
 
 def attn(q, k, v, route: Route, out=None, *, force_simt=False, stats_only=False,
-         reuse_stats=False, stream=None):
+         reuse_stats=False, cta_pair=False, stream=None):
     """pasa_attn: returns out ([B, S, H, D], q's dtype).  stats_only / reuse_stats
-    split the call into its statistics and attention kernels (PASA_ATTN_* flags)."""
+    split the call into its statistics and attention kernels; cta_pair runs a Bq = 256
+    route on the tcgen05 cta_group::2 kernel (PASA_ATTN_* flags)."""
     if out is None:
         out = torch.empty_like(q)
     qd, kd, vd, od = tensor_desc(q), tensor_desc(k), tensor_desc(v), tensor_desc(out)
     flags = ((_C.PASA_ATTN_FORCE_SIMT if force_simt else 0)
              | (_C.PASA_ATTN_STATS_ONLY if stats_only else 0)
-             | (_C.PASA_ATTN_REUSE_STATS if reuse_stats else 0))
+             | (_C.PASA_ATTN_REUSE_STATS if reuse_stats else 0)
+             | (_C.PASA_ATTN_CTA_PAIR if cta_pair else 0))
     _C.check(_C.lib().pasa_attn_ex(ctypes.byref(qd), ctypes.byref(kd), ctypes.byref(vd),
                                    route.handle, ctypes.byref(od), flags, _stream_ptr(stream)),
              "pasa_attn")

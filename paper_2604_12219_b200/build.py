@@ -28,7 +28,7 @@ COMMON += os.environ.get("PASA_EXTRA_FLAGS", "").split()
 # per-file extra flags: the route unit must not contract fp64 mul+add into fma
 EXTRA = {"route.cu": ["--fmad=false"]}
 SOURCES = ["api.cpp", "tmap.cpp", "budget.cu", "route.cu", "het.cu", "kv_stats.cu", "attn_simt.cu",
-           "attn_sm100.cu", "attn_sm100_q256.cu", "kv_stats_sm100.cu"]
+           "attn_sm100.cu", "attn_sm100_q256.cu", "attn_sm100_cta2.cu", "kv_stats_sm100.cu"]
 HEADERS = ["pasa_internal.h", "philox.cuh", "sm100_ptx.cuh", "fastlog.cuh", "logtab.h"]
 
 

@@ -452,7 +452,8 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
     if ((st = match_route(v, route, "v")) != PASA_OK) return st;
     if ((st = match_route(out, route, "out")) != PASA_OK) return st;
     if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route)");
-    if (flags & ~(PASA_ATTN_FORCE_SIMT | PASA_ATTN_STATS_ONLY | PASA_ATTN_REUSE_STATS))
+    if (flags & ~(PASA_ATTN_FORCE_SIMT | PASA_ATTN_STATS_ONLY | PASA_ATTN_REUSE_STATS |
+                  PASA_ATTN_CTA_PAIR))
         return fail(PASA_EINVAL, "unknown pasa_attn_ex flags 0x%x", flags);
     if (route->cfg.qk_fp8 && (q->dtype != PASA_BF16 || (flags & PASA_ATTN_FORCE_SIMT) ||
                               !pasa::kv_stats_sm100_supported(route)))
@@ -465,6 +466,13 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
         route->stats_dtype = q->dtype;
     } else if (route->stats_dtype != q->dtype) {
         return fail(PASA_EINVAL, "PASA_ATTN_REUSE_STATS without a matching STATS_ONLY call");
+    }
+    if ((flags & PASA_ATTN_CTA_PAIR) &&
+        (q->dtype != PASA_BF16 || (flags & PASA_ATTN_FORCE_SIMT) ||
+         !pasa::attn_sm100_cta2_supported(route))) {
+        g_launches = launches;
+        return fail(PASA_EUNSUPPORTED, "PASA_ATTN_CTA_PAIR: bf16, Bq = 256, d = 128, "
+                    "G in {32, 64, k*128, >= N_K}, no FORCE_SIMT");
     }
     if (flags & PASA_ATTN_STATS_ONLY) { g_launches = launches; return PASA_OK; }
     cudaError_t e = cudaSuccess;
@@ -481,8 +489,11 @@ pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_
                         "(d 64 / 128, G in {32, 64, k*128, >= N_K}, no FORCE_SIMT)");
         }
         char why[256] = {0};
-        cudaError_t e = pasa::launch_attn_sm100_q256(*q, *k, *v, route, *out, s, &launches, why,
-                                                     sizeof(why));
+        cudaError_t e = (flags & PASA_ATTN_CTA_PAIR)
+                            ? pasa::launch_attn_sm100_cta2(*q, *k, *v, route, *out, s, &launches, why,
+                                                           sizeof(why))
+                            : pasa::launch_attn_sm100_q256(*q, *k, *v, route, *out, s, &launches, why,
+                                                           sizeof(why));
         g_launches = launches;
         if (e == cudaErrorNotSupported) return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);
         return cuda_status(e, "attention launch");

@@ -122,6 +122,12 @@ bool attn_sm100_q256_supported(const pasa_route_s* r);
 cudaError_t launch_attn_sm100_q256(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                                    pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
                                    int* launches, char* why, size_t why_len);
+// Bq = 256 on a CTA pair (tcgen05 cta_group::2, M = 256; each SM holds half of every
+// operand tile); attn_sm100_cta2.cu, selected with PASA_ATTN_CTA_PAIR
+bool attn_sm100_cta2_supported(const pasa_route_s* r);
+cudaError_t launch_attn_sm100_cta2(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
+                                   pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
+                                   int* launches, char* why, size_t why_len);
 // tmap.cpp: TMA tensor-map encoding (bf16, 128-byte swizzle, zero OOB fill) and the
 // diagnostics state set by pasa_debug_trace / pasa_debug_flags
 bool make_tensor_map(CUtensorMap* m, const void* base, int rank, const uint64_t* dims,

@@ -89,8 +89,9 @@ def errors(o, ref):
             float(np.sqrt((d * d).sum() / (ref * ref).sum())))
 
 
-def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, log=None, label=""):
-    out = P.attn(q, k, v, route, force_simt=force_simt)
+def check_attn(P, q, k, v, route, got, cfg, force_simt=False, pairs=None, log=None, label="",
+               cta_pair=False):
+    out = P.attn(q, k, v, route, force_simt=force_simt, cta_pair=cta_pair)
     torch.cuda.synchronize()
     B, S, H, D = q.shape
     if pairs is None:
@@ -292,6 +293,45 @@ def test_attn_q256_rejects_unsupported(pasa):
     route(q, k, make_budget(pasa, 0.3), 1, 25)
     with pytest.raises(pasa.PasaError):
         pasa.attn(q, k, v, route)
+
+
+CTA2_CASES = [c for c in Q256_CASES if c[4] == 128]
+
+
+@pytest.mark.parametrize("case", CTA2_CASES, ids=[c[0] + "_cta2" for c in CTA2_CASES])
+def test_attn_parity_cta_pair(pasa, case, parity_log):
+    """Bq = 256 on the CTA-pair kernel (tcgen05 cta_group::2, M = 256, each SM holding half
+    of every operand tile) against the oracle's attention at Bq = 256; bitwise
+    reproducible, and equal to the one-CTA two-tile kernel up to fp32 summation order."""
+    name, B, S, H, D, Bq, G, comp, rho, dtype, gen = case
+    q, k, v = gen_qkv(gen, B, S, H, D, dtype, seed=13)
+    cfg = pasa.RouteCfg(Bq=Bq, G=G, comp=comp, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, rho)
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, log=parity_log, label=name + " cta_pair",
+                        cta_pair=True)
+    assert torch.equal(out, pasa.attn(q, k, v, route, cta_pair=True))
+    one = pasa.attn(q, k, v, route).float()
+    assert float((out.float() - one).abs().max()) <= 1e-2 * float(one.abs().max())
+
+
+@pytest.mark.parametrize("S", [1, 100, 256, 257, 511, 640])
+def test_attn_cta_pair_edges(pasa, S):
+    """CTA pair around the tile edges: the peer CTA's rows entirely past S (S <= 128),
+    exactly one q-block, one row past it, and k = 1."""
+    q, k, v = synth.iid_qkv(1, S, 2, 128, seed=S + 7, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=256, G=32, beta=0.1)
+    route, got, _ = check_route(pasa, q, k, cfg, 0.3 if S > 64 else 1.0)
+    check_attn(pasa, q, k, v, route, got, cfg, cta_pair=True)
+
+
+def test_attn_cta_pair_rejects_unsupported(pasa):
+    """d = 64 and Bq = 128 routes are outside the pair kernel's domain: EUNSUPPORTED."""
+    for D, Bq in ((64, 256), (128, 128)):
+        q, k, v = synth.iid_qkv(1, 1000, 1, D, seed=3, dtype=torch.bfloat16, device="cuda")
+        route = pasa.Route(1, 1000, 1, D, pasa.RouteCfg(Bq=Bq, G=32))
+        route(q, k, make_budget(pasa, 0.3), 1, 25)
+        with pytest.raises(pasa.PasaError):
+            pasa.attn(q, k, v, route, cta_pair=True)
 
 
 EDGE_CASES = [
@@ -505,6 +545,27 @@ def test_full_config_q256_sampled(pasa, parity_log):
                         log=parity_log, label="wan14b_720p Bq=256 full size, 4 heads x 16 q-blocks")
     assert bool(torch.isfinite(out).all())
     assert torch.equal(out, pasa.attn(q, k, v, route))
+
+
+def test_full_config_cta_pair_sampled(pasa, parity_log):
+    """Wan 2.1-14B 720p at full size with Bq = 256 on the CTA-pair kernel: attention on
+    4 heads x 16 q-blocks incl. the ragged last one against the oracle, whole output
+    finite and bitwise reproducible over three launches."""
+    c = synth.CONFIGS["wan14b_720p"]
+    B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    q, k, v = synth.iid_qkv(B, S, H, D, seed=1006, dtype=torch.bfloat16, device="cuda")
+    cfg = pasa.RouteCfg(Bq=256, G=c["G"], beta=0.1)
+    route, got, ties = check_route(pasa, q, k, cfg, c["rho"], seed=pasa.layer_seed(42, 0),
+                                   step=25, heads=[0, 17, 39])
+    out, _ = check_attn(pasa, q, k, v, route, got, cfg, pairs=_pairs(_attn_heads(H), route.NQ),
+                        log=parity_log, label="wan14b_720p Bq=256 cta_pair full size, 4 heads x 16 q-blocks",
+                        cta_pair=True)
+    for _ in range(2):
+        again = torch.full_like(q, float("nan"))
+        pasa.attn(q, k, v, route, again, cta_pair=True)
+        torch.cuda.synchronize()
+        assert bool(torch.isfinite(again).all())
+        assert torch.equal(out, again)
 
 
 def test_long_sequence_200k_route_and_attention(pasa, parity_log):
