@@ -59,6 +59,23 @@ constexpr bool kD64QT = PASA_D64_QTMEM != 0;
 #define PASA_D128_QTMEM 0
 #endif
 constexpr bool kD128QT = PASA_D128_QTMEM != 0;
+// critical-path barrier waits (A/B knob): 0 = try_wait with a suspend-time hint (default);
+// bit 0: the MMA warp's waits without the hint, bit 1: the softmax's S wait without the
+// hint, bit 2: those waits as test_wait polling loops
+// P release (A/B knob): 1 = one arrival per softmax warp after __syncwarp (p_full count
+// 4 + the V producer) instead of one per thread (128 + 1)
+#ifndef PASA_WARP_ARRIVE
+#define PASA_WARP_ARRIVE 0
+#endif
+#ifndef PASA_CRIT_WAIT
+#define PASA_CRIT_WAIT 0
+#endif
+__device__ __forceinline__ void crit_wait(uint64_t* bar, uint32_t parity, bool spin) {
+    if (PASA_CRIT_WAIT & 4) {
+        if (spin) { while (!ptx::mbar_test(bar, parity)) {} return; }
+    }
+    ptx::mbar_wait_c(bar, parity, spin);
+}
 
 enum : int32_t { OP_E = 0, OP_C = 1, OP_F = 2 };
 __device__ __forceinline__ uint16_t op_make(int32_t type, int32_t v) {
@@ -160,7 +177,9 @@ __global__ void __launch_bounds__(kThreads, 2)
     __shared__ std::conditional_t<EXP == 1, CtlSG, Ctl> ctl;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const bool spin = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
+    const bool spin_dbg = DIAG && (p.dbg & 4) != 0;   // diagnostics: poll critical-path barriers
+    const bool spin = spin_dbg || (PASA_CRIT_WAIT & 1) != 0;      // MMA warp
+    const bool spin_s = spin_dbg || (PASA_CRIT_WAIT & 2) != 0;    // softmax S wait
     const bool tracing = p.trace != nullptr && (int)((p.it0 + blockIdx.x) % p.NQ) == p.trace_x &&
                          (int)((p.it0 + blockIdx.x) / p.NQ) == p.trace_y;
     const int64_t item = p.it0 + blockIdx.x;
@@ -183,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         }
         for (int s = 0; s < G_::NB; ++s) mbar_init(&ctl.s_full[s], 1);
         for (int s = 0; s < G_::NB; ++s)
-            mbar_init(&ctl.p_full[s], G_::NB == 1 ? 128 : 129);   // softmax threads + V producer
+            mbar_init(&ctl.p_full[s], (PASA_WARP_ARRIVE ? 4 : 128) + (G_::NB == 1 ? 0 : 1));   // softmax + V producer
         if (G_::NB == 1) {
             mbar_init(&ctl.v_full[0], 1);
             mbar_init(&ctl.v_full[1], 1);
@@ -331,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 2)
         auto issue_qk = [&](int n) {
             const int s = n % G_::NKS, sbuf = n % G_::NB;   // K ring slot, S buffer
             if (lane == 0) PASA_TR(TR_MMA_QKW, n);
-            mbar_wait_c(&ctl.k_full[s], (n / G_::NKS) & 1, spin);
+            crit_wait(&ctl.k_full[s], (n / G_::NKS) & 1, spin);
             if (lane == 0) PASA_TR(TR_SB_W, n);           // K(n) landed
             tc_fence_after();
             // the whole warp runs the issue code with warp-uniform operands; elect.sync
@@ -372,7 +391,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (nq < nops && op_type(ctl.ops[nq]) != OP_F) issue_qk(nq);
             // V(n) lands on p_full[s] too (one wait for "P ready and V loaded")
             if (lane == 0) PASA_TR(TR_MMA_V, n);
-            mbar_wait_c(&ctl.p_full[sb], (n / G_::NB) & 1, spin);
+            crit_wait(&ctl.p_full[sb], (n / G_::NB) & 1, spin);
             if (G_::NB == 1) mbar_wait_c(&ctl.v_full[s], (n >> 1) & 1, spin);
             if (lane == 0) PASA_TR(TR_MMA_P, n);
             tc_fence_after();
@@ -388,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                 if (lane == 0) PASA_TR(TR_KPROD_W, n);
             } else {
                 const int sk = n % G_::NKS;   // the K slot holding H-bar^T box 0
-                mbar_wait_c(&ctl.k_full[sk], (n / G_::NKS) & 1, spin);
+                crit_wait(&ctl.k_full[sk], (n / G_::NKS) & 1, spin);
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < D / 16; ++kk) {
@@ -475,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             } else if (type != OP_F) {
                 const int par = s_parity(bi);
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_W, n);
-                mbar_wait_c(&ctl.s_full[bi], par, spin);
+                crit_wait(&ctl.s_full[bi], par, spin_s);
                 if (warp == 4 && lane == 0) PASA_TR(TR_SA_OK, n);
                 tc_fence_after();
                 uint32_t sa[32], sb[32];
@@ -694,7 +713,12 @@ __global__ void __launch_bounds__(kThreads, 2)
                 tmem_wait_st();
             }
             tc_fence_before();
-            mbar_arrive(&ctl.p_full[bi]);
+            if (PASA_WARP_ARRIVE) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&ctl.p_full[bi]);
+            } else {
+                mbar_arrive(&ctl.p_full[bi]);
+            }
             if (warp == 4 && lane == 0) PASA_TR(TR_SA_ARR, n);
         }
         // ---- epilogue: O / l -> bf16 -> global ----

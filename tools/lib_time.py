@@ -34,5 +34,7 @@ for rep in range(int(os.environ.get("REPS", "8"))):
     e1.record()
     torch.cuda.synchronize()
     xs.append(e0.elapsed_time(e1) / 10)
-print(f"{name} {os.path.basename(os.environ.get('PASA_LIB', 'in-tree'))}: attn min {min(xs):.4f} "
+_lib = os.environ.get("PASA_LIB", "in-tree")
+_tag = os.path.basename(os.path.dirname(os.path.dirname(_lib))) if "ab_tmp" in _lib else "default"
+print(f"{name} {_tag}: attn min {min(xs):.4f} "
       f"median {statistics.median(xs):.4f} ms, finite {bool(torch.isfinite(out).all())}", flush=True)

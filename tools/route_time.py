@@ -29,5 +29,5 @@ for beta in (0.1, 0.0):
         e1.record()
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / 10)
-    print(f"{name} {os.path.basename(os.environ.get('PASA_LIB', 'in-tree'))} beta {beta} "
+    print(f"{name} {os.path.basename(os.environ.get('PASA_LIB', 'in-tree'))} chunks {os.environ.get('PASA_ROUTE_CHUNKS', 'auto')} beta {beta} "
           f"route ms (min) {best:.3f}", flush=True)
