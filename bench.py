@@ -72,6 +72,12 @@ def parse(argv=None):
     ap.add_argument("--ulysses-chunks", type=int, default=0,
                     help="head groups of the sequence-sharded Ulysses all-to-all (attention on "
                          "arrived heads overlaps the rest; 0 = auto, up to 4)")
+    ap.add_argument("--bq", type=int, default=0, choices=[0, 128, 256],
+                    help="query block size of the route (0: the config's, 128); 256 = the "
+                         "Bq = 256 throughput variant (reading R-29, not a BASELINE config)")
+    ap.add_argument("--cta-pair", action="store_true",
+                    help="Bq = 256 attention on the tcgen05 cta_group::2 CTA pair "
+                         "(PASA_ATTN_CTA_PAIR) instead of the one-CTA two-tile kernel")
     ap.add_argument("--qk-precision", default="bf16", choices=["bf16", "fp8"],
                     help="fp8: the opt-in FP8 QK^T variant (SURVEY.md §8f NEXT 4; its own "
                          "tolerance; never the headline configuration)")
@@ -291,7 +297,12 @@ def run_pasa(args):
         dist.barrier()
     import paper_2604_12219_b200 as P
 
-    cfg = synth.CONFIGS[args.config]
+    cfg = dict(synth.CONFIGS[args.config])
+    if args.bq:
+        cfg["Bq"] = args.bq
+    if args.cta_pair and cfg["Bq"] != 256:
+        raise SystemExit("--cta-pair runs Bq = 256 routes (add --bq 256)")
+    attn_kw = {"cta_pair": True} if args.cta_pair else {}
     B, S, H, D = cfg["B"], cfg["S"], cfg["H"], cfg["D"]
     from paper_2604_12219_b200 import dist as pdist
     seq_sharded = (args.seq_sharded == "yes"
@@ -403,7 +414,7 @@ def run_pasa(args):
             launches[0] += P.last_launch_count()
             if evs:
                 evs[2].record(stream)
-            P.attn(qh, kh, vh, r, oh, reuse_stats=True)
+            P.attn(qh, kh, vh, r, oh, reuse_stats=True, **attn_kw)
             launches[0] += P.last_launch_count()
             if evs:
                 evs[3].record(stream)
@@ -455,7 +466,7 @@ def run_pasa(args):
         if ev is not None:
             ev[2].record(stream)
         for r, qu, ku, vu, ou in units:
-            P.attn(qu, ku, vu, r, ou, reuse_stats=True)
+            P.attn(qu, ku, vu, r, ou, reuse_stats=True, **attn_kw)
             launches[0] += P.last_launch_count()
         if ev is not None:
             ev[3].record(stream)
@@ -595,7 +606,7 @@ def run_pasa(args):
             budget(lat[2], lat[1], lat[0], T=T, step=t, rho=cfg["rho"], l1_mean=lbar,
                    h_t=1 / T, h_tm1=1 / T)
             route(q, k, budget, seed, t, v=v if use_v else None)
-            P.attn(q, k, v, route, out)
+            P.attn(q, k, v, route, out, **attn_kw)
             eb.record(stream)
             torch.cuda.synchronize()
             ms_t = all_max([ea.elapsed_time(eb)])[0]
@@ -648,13 +659,13 @@ def run_pasa(args):
                 budget(dx[0], dx[1], dx[2], **bkw)
                 for r, qu, ku, vu, ou in dunits:
                     r(qu, ku, budget, seed, t_step, v=vu if use_v else None)
-                    P.attn(qu, ku, vu, r, ou)
+                    P.attn(qu, ku, vu, r, ou, **attn_kw)
                 hout.copy_(dout, non_blocking=True)
         elif n_chunks > 1:
             # public API for host-resident tensors: head chunks on copy-in / compute /
             # copy-out streams (paper_2604_12219_b200.pipeline)
             from paper_2604_12219_b200.pipeline import HostPipeline
-            pipe = HostPipeline(B, S, Hl, D, rcfg, n_chunks=n_chunks, device=dev)
+            pipe = HostPipeline(B, S, Hl, D, rcfg, n_chunks=n_chunks, device=dev, attn_kw=attn_kw)
 
             def e2e_step():
                 pipe(hq, hk, hv, hout, hx, seed, t_step, v_for_prior=use_v, T=50,
@@ -669,7 +680,7 @@ def run_pasa(args):
                 budget(dx[0], dx[1], dx[2], T=50, step=t_step, rho=cfg["rho"], l1_mean=lbar,
                        h_t=1 / 50, h_tm1=1 / 50, rho_table=table)
                 route(dq, dk, budget, seed, t_step, v=dv if use_v else None)
-                P.attn(dq, dk, dv, route, out)
+                P.attn(dq, dk, dv, route, out, **attn_kw)
                 hout.copy_(out, non_blocking=True)
 
         e2e_step()
@@ -721,7 +732,8 @@ def run_pasa(args):
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
             tr = json.load(f)
-            if tr.get("config") == args.config and tr.get("heads") == work_heads:
+            if (tr.get("config") == args.config and tr.get("heads") == work_heads
+                    and cfg["Bq"] == 128):   # the capture is of the default Bq = 128 kernel
                 traffic = tr.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         pass
@@ -759,7 +771,7 @@ def run_pasa(args):
             else None,
             "Bq": cfg["Bq"], "Bk": cfg["Bk"], "G": cfg["G"], "rho": cfg["rho"],
             "step_t": t_step, "budget": args.budget, "prior": args.prior,
-            "qk_precision": args.qk_precision, "l1": rec["l1"], "alpha": rec["alpha"],
+            "qk_precision": args.qk_precision, "attn_kernel": "cta_pair" if args.cta_pair else ("q256_one_cta" if cfg["Bq"] == 256 else "default"), "l1": rec["l1"], "alpha": rec["alpha"],
             "rho_t": rec["rho_t"], "k": kk, "N_K": NK, "N_G": NG,
             "beta": 0.1, "inputs": "iid N(0,1) bf16, seeded per global head",
             "l2": "inputs larger than L2 (q,k,v 2.3 GB vs 126 MB), no flush",
@@ -773,7 +785,9 @@ def run_pasa(args):
                      "attn": float(ph[3]), "other": float(t_max - ph.sum())},
         "tflops_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12,
         "pct_of_peak_algorithmic": flops_head * B * H / (t_max * 1e-3) / 1e12 / peak,
-        "roofline": {"kernel": "attn_sm100_kernel", "bound": "tensor", "achieved": achieved,
+        "roofline": {"kernel": ("attn_sm100_cta2_kernel" if args.cta_pair else
+                                "attn_sm100_q256_kernel" if cfg["Bq"] == 256 else
+                                "attn_sm100_kernel"), "bound": "tensor", "achieved": achieved,
                      "peak": peak, "peak_kind": f"bf16 dense, sustained ({which})",
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                      "flops_per_launch": attn_flops},

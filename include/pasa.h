@@ -223,7 +223,8 @@ pasa_status pasa_route_v(const pasa_tensor* q, const pasa_tensor* k, const pasa_
  *   was built from; v and out have the same B,S,H,D (out may have its own
  *   strides).  bf16 I/O with Bq = 128 and G in {8, 16, 32, 64, multiples of 128,
  *   >= N_K} runs the tcgen05/TMEM/TMA kernel (fp32 accumulate; Kbar, Vsum, Hbar
- *   stored bf16, R-21); Bq = 256 (R-29) runs the two-tile tcgen05 kernel (bf16,
+ *   stored bf16, R-21); Bq = 256 (R-29) runs the two-tile tcgen05 kernel, or the
+ *   cta_group::2 CTA-pair kernel with PASA_ATTN_CTA_PAIR (bf16,
  *   G in {32, 64, multiples of 128, >= N_K}; anything else at Bq = 256 is
  *   EUNSUPPORTED); fp32 I/O, Bq = 64 or other group sizes run the fp32 CUDA-core
  *   kernel.

@@ -41,8 +41,10 @@ class HostPipeline:
     contiguous, bf16) split into ``n_chunks`` head chunks on three streams."""
 
     def __init__(self, B: int, S: int, H: int, D: int, cfg: Optional[RouteCfg] = None,
-                 n_chunks: int = 8, device=None, dtype=torch.bfloat16, taper: bool = True):
+                 n_chunks: int = 8, device=None, dtype=torch.bfloat16, taper: bool = True,
+                 attn_kw: Optional[dict] = None):
         self.shape = (B, S, H, D)
+        self.attn_kw = dict(attn_kw or {})   # extra pasa_attn flags (e.g. cta_pair=True)
         self.dtype = dtype
         self.device = torch.device(device if device is not None else "cuda")
         cfg = cfg or RouteCfg()
@@ -122,7 +124,7 @@ class HostPipeline:
         for (a, b), (q, k, v, o), route, e in zip(self.chunks, self.bufs, self.routes, ev_in):
             self.s_cmp.wait_event(e)
             route(q, k, self.budget, seed, step, v=v if v_for_prior else None, stream=self.s_cmp)
-            attn(q, k, v, route, o, stream=self.s_cmp)
+            attn(q, k, v, route, o, stream=self.s_cmp, **self.attn_kw)
             ec = torch.cuda.Event()
             ec.record(self.s_cmp)
             ev_cmp.append(ec)

@@ -505,7 +505,7 @@ def test_full_config_constant_key_blocks_equal_dense(pasa, name, parity_log):
         assert err <= REG[torch.bfloat16], err
 
 
-@pytest.mark.parametrize("variant", ["default", "q256"])
+@pytest.mark.parametrize("variant", ["default", "q256", "cta_pair"])
 @pytest.mark.parametrize("name", ["wan13b_480p", "cogvideox5b", "wan14b_720p", "hunyuan_720p"])
 def test_full_config_repeat_finite_bitwise(pasa, name, variant):
     """Every BASELINE config at full size in bench.py's launch configuration, three
@@ -514,14 +514,16 @@ def test_full_config_repeat_finite_bitwise(pasa, name, variant):
     V tile: a few rows of NaN in some runs, invisible to sampled parity.)"""
     c = synth.CONFIGS[name]
     B, S, H, D = c["B"], c["S"], c["H"], c["D"]
+    if variant == "cta_pair" and D != 128:
+        pytest.skip("the CTA-pair kernel is d = 128 only")
     q, k, v = synth.iid_qkv(B, S, H, D, seed=1004, dtype=torch.bfloat16, device="cuda")
-    cfg = pasa.RouteCfg(Bq=256 if variant == "q256" else c["Bq"], G=c["G"], beta=0.1)
+    cfg = pasa.RouteCfg(Bq=c["Bq"] if variant == "default" else 256, G=c["G"], beta=0.1)
     route = pasa.Route(B, S, H, D, cfg)
     route(q, k, make_budget(pasa, c["rho"]), pasa.layer_seed(42, 0), 25)
     first = None
     for _ in range(3):
         out = torch.full_like(q, float("nan"))
-        pasa.attn(q, k, v, route, out)
+        pasa.attn(q, k, v, route, out, cta_pair=variant == "cta_pair")
         torch.cuda.synchronize()
         assert bool(torch.isfinite(out).all())
         if first is None:
