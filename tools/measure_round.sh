@@ -1,5 +1,5 @@
 #!/usr/bin/env bash
-# One GPU measurement pass of round 2 (run on the B200 box from the repo root):
+# One GPU measurement pass of round 2 (third session: + the Bq = 256 CTA pair, torchrun N = 1) (run on the B200 box from the repo root):
 #   /usr/local/graft/bin/gpurun --timeout 3000 -- 'bash tools/measure_round.sh'
 # Writes everything under gpurun_out/; the summaries kept are copied into profiles/r02_*.
 set -u
@@ -13,6 +13,11 @@ for c in wan13b_480p cogvideox5b hunyuan_720p; do
   timeout 400 python bench.py --config "$c" --no-cpu > "gpurun_out/bench_$c.json" 2> "gpurun_out/bench_$c.err"
 done
 timeout 400 python bench.py --qk-precision fp8 --no-cpu > gpurun_out/bench_wan14b_fp8.json 2> gpurun_out/bench_wan14b_fp8.err
+timeout 400 python bench.py --bq 256 --cta-pair --no-cpu --no-dense > gpurun_out/bench_wan14b_q256_pair.json 2> gpurun_out/bench_wan14b_q256_pair.err
+timeout 400 python bench.py --bq 256 --no-cpu --no-dense > gpurun_out/bench_wan14b_q256.json 2> gpurun_out/bench_wan14b_q256.err
+# the NCCL plumbing at N = 1 (init, barriers, MAX all-reduce), as the driver launches N > 1
+timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
+  --master-port 29511 bench.py --gpus 1 --no-cpu --no-dense > gpurun_out/bench_wan14b_torchrun1.json 2> gpurun_out/bench_wan14b_torchrun1.err
 timeout 400 python bench.py --config cogvideox5b --schedule --no-cpu --no-e2e > gpurun_out/bench_cogvideox5b_schedule.json 2> gpurun_out/bench_cogvideox5b_schedule.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 900 python bench.py --config hunyuan_720p --gpus 2 --dist-backend gloo --no-cpu --steps 2 --no-dense --no-e2e > gpurun_out/bench_hy_gloo2.json 2> gpurun_out/bench_hy_gloo2.err
