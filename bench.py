@@ -300,8 +300,6 @@ def run_pasa(args):
     cfg = dict(synth.CONFIGS[args.config])
     if args.bq:
         cfg["Bq"] = args.bq
-    if args.cta_pair and cfg["Bq"] != 256:
-        raise SystemExit("--cta-pair runs Bq = 256 routes (add --bq 256)")
     attn_kw = {"cta_pair": True} if args.cta_pair else {}
     B, S, H, D = cfg["B"], cfg["S"], cfg["H"], cfg["D"]
     from paper_2604_12219_b200 import dist as pdist
@@ -810,6 +808,8 @@ def run_pasa(args):
 def main(argv=None):
     argv = sys.argv[1:] if argv is None else argv
     args = parse(argv)
+    if args.cta_pair and args.bq != 256:
+        raise SystemExit("bench.py: --cta-pair runs Bq = 256 routes (add --bq 256)")
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # one process per GPU: re-launch under torchrun (rank 0 prints the JSON line)
         return subprocess.call(torchrun_cmd(argv, args.gpus, free_port()))

@@ -70,3 +70,14 @@ def test_reference_arm_world2_rank1_exits_without_work(monkeypatch):
     monkeypatch.setenv("WORLD_SIZE", "2")
     monkeypatch.setenv("RANK", "1")
     assert b.main(["--gpus", "2", "--impl", "reference"]) == 0
+
+
+def test_cta_pair_needs_bq256_and_parses():
+    """--cta-pair (the tcgen05 cta_group::2 kernel) is a Bq = 256 variant: without
+    --bq 256 bench.py refuses before touching a GPU; with it the flags parse."""
+    b = _bench()
+    import pytest
+    with pytest.raises(SystemExit):
+        b.main(["--cta-pair"])
+    a = b.parse(["--bq", "256", "--cta-pair"])
+    assert a.bq == 256 and a.cta_pair
