@@ -4,7 +4,9 @@ while NVML samples board power, SM clock and throttle reasons (every 20 ms).  Re
 per variant: ms per launch, median SM MHz, median W, throttle reasons, and
 energy per launch (J) = median W x ms.  If every variant sits at the board power
 limit, time per launch is energy per launch / power: the kernel is power-bound.
-    CFG=wan14b_720p SECS=4 python tools/power_probe.py"""
+    CFG=wan14b_720p SECS=4 [DENSE_HEADS=8] python tools/power_probe.py
+(DENSE_HEADS: also torch's dense SDPA on that many heads, the library kernel on the same
+box and cap; pJ/FLOP uses the algorithmic FLOPs of each.)"""
 import os
 import statistics
 import sys
@@ -36,6 +38,25 @@ for bq in (128, 256):
         variants["default (Bq 128, 2 CTAs/SM)"] = (r, out, {})
     else:
         variants["q256 (Bq 256, 1 CTA/SM, 2 tiles)"] = (r, out, {})
+        if D == 128:
+            variants["pair (Bq 256, cta_group::2)"] = (r, torch.empty_like(out), {"cta_pair": True})
+# algorithmic FLOPs per launch (the same for Bq = 128 and 256)
+NK, NG = variants["default (Bq 128, 2 CTAs/SM)"][0].NK, variants["default (Bq 128, 2 CTAs/SM)"][0].NG
+kk = variants["default (Bq 128, 2 CTAs/SM)"][0].read()["k"]
+flops = {vn: (4.0 * S * kk * 64 * D + 4.0 * S * NK * D + 2.0 * S * D * D * NG) * B * H
+         for vn in variants}
+DENSE_H = int(os.environ.get("DENSE_HEADS", "0"))   # > 0: also dense SDPA on that many heads
+if DENSE_H:
+    qd, kd, vd = (t[:, :, :DENSE_H].transpose(1, 2).contiguous() for t in (q, k, v))
+    variants[f"dense SDPA ({DENSE_H} heads, torch / cuDNN)"] = (None, None, {"dense": (qd, kd, vd)})
+    flops[f"dense SDPA ({DENSE_H} heads, torch / cuDNN)"] = 4.0 * S * S * D * B * DENSE_H
+
+
+def launch(r, out, kw):
+    if "dense" in kw:
+        torch.nn.functional.scaled_dot_product_attention(*kw["dense"])
+    else:
+        P.attn(q, k, v, r, out, reuse_stats=True, **kw)
 
 pynvml.nvmlInit()
 dev = pynvml.nvmlDeviceGetHandleByIndex(torch.cuda.current_device())
@@ -57,7 +78,7 @@ print(f"{name}: enforced power limit {limit_w:.0f} W", flush=True)
 for rep in range(2):
     for vname, (r, out, kw) in variants.items():
         for _ in range(3):
-            P.attn(q, k, v, r, out, reuse_stats=True, **kw)
+            launch(r, out, kw)
         torch.cuda.synchronize()
         t0 = time.time()
         n = 0
@@ -65,7 +86,7 @@ for rep in range(2):
         e0.record()
         while time.time() - t0 < SECS:
             for _ in range(10):
-                P.attn(q, k, v, r, out, reuse_stats=True, **kw)
+                launch(r, out, kw)
             n += 10
             torch.cuda.synchronize()
         e1.record()
@@ -83,5 +104,6 @@ for rep in range(2):
                                     (0x80, "hw_power_brake")) if reasons & bit]
         print(f"rep {rep} {vname}: {ms:.3f} ms/launch, SM {mhz:.0f} MHz, {w:.0f} W, "
               f"{w * ms / 1000:.2f} J/launch, {ms * mhz / 1000:.0f} kcycles/launch, "
-              f"reasons {names}", flush=True)
+              f"{flops[vname] / (ms * 1e-3) / 1e12:,.0f} TFLOP/s, "
+              f"{w * ms * 1e-3 / flops[vname] * 1e12:.3f} pJ/FLOP, reasons {names}", flush=True)
 stop.set()
