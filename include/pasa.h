@@ -252,6 +252,52 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
 pasa_status pasa_attn_ex(const pasa_tensor* q, const pasa_tensor* k, const pasa_tensor* v,
                          pasa_route_h route, pasa_tensor* out, uint32_t flags, void* stream);
 
+/* Zero-copy sequence parallelism: the Ulysses all-to-all fused into PASA's kernels over
+ * peer memory (PAPER.md:321 runs PASA on 8 GPUs).  When the
+ * model's activations arrive sequence-sharded (rank r holds tokens [start[r],
+ * start[r+1]) of every head), the rank that owns heads [h0, h0 + Hl) reads those heads of
+ * every shard directly through peer pointers (NVLink P2P / CUDA IPC mappings the caller
+ * set up), and writes each output row straight into the shard of the rank that owns its
+ * token: no all-to-all is issued.
+ *
+ * pasa_shards: one bf16 tensor [1, S, H, D] as P (1..8) sequence shards.  data[s] is the
+ * address (valid in this process, device-accessible) of shard s's first token, head 0;
+ * sS / sH are element strides (the same in every shard, 16-byte aligned, unit stride in D);
+ * start[0] = 0 < start[1] < ... < start[P] = S.  Shard boundaries need not align to blocks. */
+typedef struct {
+    int32_t dtype;          /* PASA_BF16 */
+    int32_t nshards;        /* P */
+    int64_t S, H, D;
+    int64_t sS, sH;
+    int64_t start[9];
+    void* data[8];
+} pasa_shards;
+
+/* pasa_route for the heads [cfg.head_offset, cfg.head_offset + H) of a route handle created
+ * for [1, S, H (this rank's heads), D] with cfg.H_total = the shards' H: one kernel gathers
+ * q, k and v of those heads from every shard into the caller's LOCAL buffers q_loc, k_loc,
+ * v_loc ([1, S, H, D] bf16, DEVICE, written) and pools q and k in the same pass (the same
+ * ascending-token fp64 block sums as pasa_route, so the route is bitwise the single-GPU
+ * route of those heads); then the fused score / bias / top-k kernel.  Call pasa_attn_zc
+ * next (on the same stream).  The caller guarantees every shard is complete before the
+ * call (e.g. a stream synchronise + process-group barrier on all ranks).
+ * Errors: EINVAL (NULL, nshards, start, head range), ESHAPE (S, D, local buffers), EDTYPE
+ * (not bf16), EUNSUPPORTED (prior-enabled or FP8 handles). */
+pasa_status pasa_route_zc(const pasa_shards* q, const pasa_shards* k, const pasa_shards* v,
+                          pasa_budget_h budget, uint64_t seed, int32_t step, pasa_route_h route,
+                          const pasa_tensor* q_loc, const pasa_tensor* k_loc,
+                          const pasa_tensor* v_loc, void* stream);
+
+/* pasa_attn over the local buffers pasa_route_zc filled, with the output rows of this
+ * rank's heads stored straight into `out`'s shards (row t of head h -> shard s with
+ * start[s] <= t < start[s+1], head cfg.head_offset + h).  bf16, the tensor-core kernel's
+ * domain (Bq = 128, G in {8, 16, 32, 64, multiples of 128, >= N_K}); the caller
+ * synchronises all ranks before reading its output shard.  Errors: as pasa_attn, plus
+ * EINVAL / ESHAPE for `out`, EUNSUPPORTED outside the tensor-core domain. */
+pasa_status pasa_attn_zc(const pasa_tensor* q_loc, const pasa_tensor* k_loc,
+                         const pasa_tensor* v_loc, pasa_route_h route, const pasa_shards* out,
+                         void* stream);
+
 /* Offline calibration of the budget table, Eqs. 9-11 verbatim (
  * readings R-15, R-17..R-19).  HOST pointers; no GPU work.
  *   l1_curves [N][T]: l_t of N calibration trajectories (e.g. pasa_budget's l1

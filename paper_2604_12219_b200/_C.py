@@ -33,7 +33,7 @@ EXPORTS = [
     "pasa_route_pooled_read", "pasa_route_dims", "pasa_last_launch_count", "pasa_last_error",
     "pasa_version", "pasa_debug_trace", "pasa_debug_flags", "pasa_attn_stats_read",
     "pasa_route_v", "pasa_route_het_read", "pasa_calibrate", "pasa_copy2d",
-    "pasa_budget_local_sum", "pasa_budget_from_sums",
+    "pasa_budget_local_sum", "pasa_budget_from_sums", "pasa_route_zc", "pasa_attn_zc",
 ]
 
 
@@ -64,6 +64,14 @@ class PasaRouteCfg(ctypes.Structure):
                 ("prior", ctypes.c_int32), ("_pad", ctypes.c_int32), ("eps", ctypes.c_double),
                 ("qb_begin", ctypes.c_int32), ("qb_end", ctypes.c_int32),
                 ("qk_fp8", ctypes.c_int32), ("_pad2", ctypes.c_int32)]
+
+
+class PasaShards(ctypes.Structure):
+    """pasa_shards: a [1, S, H, D] bf16 tensor as P sequence shards (include/pasa.h)."""
+    _fields_ = [("dtype", ctypes.c_int32), ("nshards", ctypes.c_int32),
+                ("S", ctypes.c_int64), ("H", ctypes.c_int64), ("D", ctypes.c_int64),
+                ("sS", ctypes.c_int64), ("sH", ctypes.c_int64),
+                ("start", ctypes.c_int64 * 9), ("data", ctypes.c_void_p * 8)]
 
 
 class PasaError(RuntimeError):
@@ -110,6 +118,9 @@ def lib():
                                  P, P, P, P]
     L.pasa_attn.argtypes = [T, T, T, P, T, P]
     L.pasa_attn_ex.argtypes = [T, T, T, P, T, ctypes.c_uint32, P]
+    SH = ctypes.POINTER(PasaShards)
+    L.pasa_route_zc.argtypes = [SH, SH, SH, P, U64, I32, P, T, T, T, P]
+    L.pasa_attn_zc.argtypes = [T, T, T, P, SH, P]
     L.pasa_layer_seed.argtypes = [U64, I32]
     L.pasa_layer_seed.restype = U64
     L.pasa_budget_read.argtypes = [P, ctypes.POINTER(ctypes.c_double), P]
@@ -131,7 +142,7 @@ def lib():
     for name in ("pasa_budget_init", "pasa_route_init", "pasa_budget", "pasa_route",
                  "pasa_budget_local_sum", "pasa_budget_from_sums",
                  "pasa_attn", "pasa_attn_ex", "pasa_budget_read", "pasa_route_read",
-                 "pasa_route_pooled_read", "pasa_route_dims"):
+                 "pasa_route_pooled_read", "pasa_route_dims", "pasa_route_zc", "pasa_attn_zc"):
         getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

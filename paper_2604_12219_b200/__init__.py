@@ -3,6 +3,8 @@
 budget -> route -> attn through the C ABI of libpasa.so (include/pasa.h).
 """
 from ._C import PasaError  # noqa: F401
-from .api import Budget, Route, RouteCfg, attn, last_launch_count, layer_seed  # noqa: F401
+from .api import (Budget, Route, RouteCfg, attn, attn_zc, last_launch_count, layer_seed,  # noqa: F401
+                  route_zc)
 
-__all__ = ["Budget", "Route", "RouteCfg", "attn", "layer_seed", "last_launch_count", "PasaError"]
+__all__ = ["Budget", "Route", "RouteCfg", "attn", "attn_zc", "route_zc", "layer_seed",
+           "last_launch_count", "PasaError"]

@@ -267,3 +267,49 @@ def attn(q, k, v, route: Route, out=None, *, force_simt=False, stats_only=False,
     if not reuse_stats:
         route._stats_dtype = q.dtype   # the statistics pass ran in q's dtype
     return out
+
+
+def shards_desc(shards) -> _C.PasaShards:
+    """A list of P sequence shards [1, S_r, H, D] (bf16, CUDA, same strides; addressable
+    from this process: local, peer or IPC-mapped) -> pasa_shards of the [1, S, H, D] whole."""
+    if not 1 <= len(shards) <= 8:
+        raise ValueError("1..8 shards")
+    H, D = shards[0].shape[2], shards[0].shape[3]
+    sS, sH = shards[0].stride(1), shards[0].stride(2)
+    d = _C.PasaShards()
+    d.dtype, d.nshards, d.H, d.D, d.sS, d.sH = _C.PASA_BF16, len(shards), H, D, sS, sH
+    t = 0
+    for r, x in enumerate(shards):
+        if (x.dim() != 4 or x.shape[0] != 1 or x.shape[2:] != (H, D) or x.dtype != torch.bfloat16
+                or x.stride(1) != sS or x.stride(2) != sH or x.stride(3) != 1):
+            raise ValueError(f"shard {r}: expected [1, S_r, {H}, {D}] bf16 with the same strides")
+        d.start[r] = t
+        d.data[r] = x.data_ptr()
+        t += x.shape[1]
+    d.start[len(shards)] = t
+    d.S = t
+    return d
+
+
+def route_zc(route: Route, q_shards, k_shards, v_shards, budget: Budget, seed: int, step: int,
+             q_loc, k_loc, v_loc, stream=None):
+    """pasa_route_zc: gather this rank's heads (route.cfg.head_offset ..) of q, k, v from every
+    sequence shard into the local [1, S, Hl, D] buffers, pooling q and k in the same pass,
+    then the fused score / bias / top-k kernel (include/pasa.h)."""
+    qs, ks, vs = shards_desc(q_shards), shards_desc(k_shards), shards_desc(v_shards)
+    ql, kl, vl = tensor_desc(q_loc), tensor_desc(k_loc), tensor_desc(v_loc)
+    _C.check(_C.lib().pasa_route_zc(ctypes.byref(qs), ctypes.byref(ks), ctypes.byref(vs),
+                                    budget.handle, seed, step, route.handle, ctypes.byref(ql),
+                                    ctypes.byref(kl), ctypes.byref(vl), _stream_ptr(stream)),
+             "pasa_route_zc")
+
+
+def attn_zc(q_loc, k_loc, v_loc, route: Route, out_shards, stream=None):
+    """pasa_attn_zc: statistics + attention over the local buffers, each output row stored
+    straight into the shard (of out_shards) that owns its token."""
+    ql, kl, vl = tensor_desc(q_loc), tensor_desc(k_loc), tensor_desc(v_loc)
+    os_ = shards_desc(out_shards)
+    _C.check(_C.lib().pasa_attn_zc(ctypes.byref(ql), ctypes.byref(kl), ctypes.byref(vl),
+                                   route.handle, ctypes.byref(os_), _stream_ptr(stream)),
+             "pasa_attn_zc")
+    route._stats_dtype = torch.bfloat16

@@ -521,6 +521,103 @@ pasa_status pasa_attn(const pasa_tensor* q, const pasa_tensor* k, const pasa_ten
     return pasa_attn_ex(q, k, v, route, out, 0u, stream);
 }
 
+namespace {
+pasa_status check_shards(const pasa_shards* t, const pasa_route_s* r, const char* name,
+                         pasa::ZcShards* out) {
+    if (!t) return fail(PASA_EINVAL, "%s is NULL", name);
+    if (t->dtype != PASA_BF16) return fail(PASA_EDTYPE, "%s: zero-copy path is bf16 only", name);
+    if (t->nshards < 1 || t->nshards > 8) return fail(PASA_EINVAL, "%s: nshards %d not in 1..8", name, t->nshards);
+    if (t->S != r->S || t->D != r->D) return fail(PASA_ESHAPE, "%s: S, D differ from the route", name);
+    if (r->cfg.head_offset < 0 || r->cfg.head_offset + r->H > t->H)
+        return fail(PASA_EINVAL, "%s: route heads [%lld, %lld) outside the shards' H = %lld", name,
+                    (long long)r->cfg.head_offset, (long long)(r->cfg.head_offset + r->H), (long long)t->H);
+    if (t->start[0] != 0 || t->start[t->nshards] != t->S)
+        return fail(PASA_EINVAL, "%s: start[0] must be 0 and start[nshards] = S", name);
+    for (int s = 0; s < t->nshards; ++s) {
+        if (t->start[s + 1] <= t->start[s]) return fail(PASA_EINVAL, "%s: empty or unordered shard %d", name, s);
+        if (!t->data[s] || (reinterpret_cast<uintptr_t>(t->data[s]) & 15))
+            return fail(PASA_EINVAL, "%s: shard %d base NULL or not 16-byte aligned", name, s);
+    }
+    if ((t->sS & 7) || (t->sH & 7) || t->sS <= 0 || t->sH <= 0)
+        return fail(PASA_EINVAL, "%s: strides must be positive multiples of 8 elements", name);
+    out->P = t->nshards;
+    for (int s = 0; s <= t->nshards; ++s) out->start[s] = t->start[s];
+    for (int s = 0; s < t->nshards; ++s) out->base[s] = t->data[s];
+    out->sS = t->sS;
+    out->sH = t->sH;
+    return PASA_OK;
+}
+}  // namespace
+
+pasa_status pasa_route_zc(const pasa_shards* q, const pasa_shards* k, const pasa_shards* v,
+                          pasa_budget_h budget, uint64_t seed, int32_t step, pasa_route_h route,
+                          const pasa_tensor* q_loc, const pasa_tensor* k_loc,
+                          const pasa_tensor* v_loc, void* stream) {
+    g_launches = 0;
+    if (!route || !budget) return fail(PASA_EINVAL, "NULL handle");
+    if (route->cfg.prior != PASA_PRIOR_NONE || route->cfg.qk_fp8)
+        return fail(PASA_EUNSUPPORTED, "pasa_route_zc: no Eq. 8 prior / FP8 QK^T handles");
+    if (route->B != 1) return fail(PASA_ESHAPE, "pasa_route_zc: B must be 1");
+    pasa::ZcShards sh[3];
+    pasa_status st;
+    if ((st = check_shards(q, route, "q", &sh[0])) != PASA_OK) return st;
+    if ((st = check_shards(k, route, "k", &sh[1])) != PASA_OK) return st;
+    if ((st = check_shards(v, route, "v", &sh[2])) != PASA_OK) return st;
+    const pasa_tensor* loc[3] = {q_loc, k_loc, v_loc};
+    const char* nm[3] = {"q_loc", "k_loc", "v_loc"};
+    pasa_tensor lt[3];
+    for (int x = 0; x < 3; ++x) {
+        if ((st = check_tensor(loc[x], nm[x])) != PASA_OK) return st;
+        if (loc[x]->dtype != PASA_BF16) return fail(PASA_EDTYPE, "%s must be bf16", nm[x]);
+        if ((st = match_route(loc[x], route, nm[x])) != PASA_OK) return st;
+        lt[x] = *loc[x];
+    }
+    int launches = 0;
+    cudaError_t e = pasa::launch_route_zc(sh, lt, budget, seed, step, route, (cudaStream_t)stream,
+                                          &launches);
+    g_launches = launches;
+    if (e == cudaSuccess) {
+        route->route_dtype = PASA_BF16;
+        route->stats_dtype = -1;
+        route->het_valid = 0;
+    }
+    return cuda_status(e, "pasa_route_zc launch");
+}
+
+pasa_status pasa_attn_zc(const pasa_tensor* q_loc, const pasa_tensor* k_loc,
+                         const pasa_tensor* v_loc, pasa_route_h route, const pasa_shards* out,
+                         void* stream) {
+    g_launches = 0;
+    if (!route) return fail(PASA_EINVAL, "NULL route");
+    pasa_status st;
+    pasa::ZcShards osh;
+    if ((st = check_shards(out, route, "out", &osh)) != PASA_OK) return st;
+    if ((st = check_tensor(q_loc, "q_loc")) != PASA_OK) return st;
+    if ((st = check_tensor(k_loc, "k_loc")) != PASA_OK) return st;
+    if ((st = check_tensor(v_loc, "v_loc")) != PASA_OK) return st;
+    if (q_loc->dtype != PASA_BF16 || k_loc->dtype != PASA_BF16 || v_loc->dtype != PASA_BF16)
+        return fail(PASA_EDTYPE, "pasa_attn_zc is bf16 only");
+    if ((st = match_route(q_loc, route, "q_loc")) != PASA_OK) return st;
+    if ((st = match_route(k_loc, route, "k_loc")) != PASA_OK) return st;
+    if ((st = match_route(v_loc, route, "v_loc")) != PASA_OK) return st;
+    if (route->route_dtype < 0) return fail(PASA_EINVAL, "route was never built (call pasa_route_zc)");
+    const pasa_route_cfg& c = route->cfg;
+    if (c.Bq != 128 || c.qk_fp8 ||
+        (c.comp == PASA_COMP_GROUPED && !pasa::sm100_supports_group(c.G, route->NK)))
+        return fail(PASA_EUNSUPPORTED, "pasa_attn_zc: the tensor-core kernel's domain only");
+    int launches = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = pasa::launch_kv_stats(*k_loc, *v_loc, route, s, &launches);
+    if (e != cudaSuccess) { g_launches = launches; return cuda_status(e, "kv_stats launch"); }
+    route->stats_dtype = PASA_BF16;
+    char why[256] = {0};
+    e = pasa::launch_attn_sm100(*q_loc, *k_loc, *v_loc, route, *q_loc, s, &launches, why,
+                                sizeof(why), &osh);
+    g_launches = launches;
+    if (e == cudaErrorNotSupported) return fail(PASA_EUNSUPPORTED, "tcgen05 attention: %s", why);
+    return cuda_status(e, "pasa_attn_zc launch");
+}
+
 pasa_status pasa_budget_read(pasa_budget_h budget, double out[5], void* stream) {
     if (!budget || !out) return fail(PASA_EINVAL, "NULL argument");
     pasa::BudgetRec rec;

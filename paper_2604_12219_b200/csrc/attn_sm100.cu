@@ -121,6 +121,13 @@ struct Params {
     const float* sq;
     const uint32_t* kamax;
     const uint32_t* kbamax;
+    // zero-copy sequence parallelism (pasa_attn_zc): oP > 0 stores row t into its owner's
+    // shard s (tokens [ostart[s], ostart[s+1]) at obase[s], already offset to this rank's
+    // first head) instead of out
+    int32_t oP;
+    int64_t ostart[9];
+    __nv_bfloat16* obase[8];
+    int64_t oSS, oSH;
     unsigned long long* trace;   // diagnostics: clock64 timeline of one CTA, or nullptr
     int32_t trace_x, trace_y;
     int32_t dbg;                 // diagnostics ablations (see pasa_debug_flags)
@@ -728,6 +735,11 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int64_t t = i * kBQ + r;
         const float inv = 1.f / l;
         __nv_bfloat16* orow = p.out + b * p.osB + h * p.osH + t * p.osS;
+        if (p.oP > 0 && t < p.S) {   // the output half of the fused Ulysses exchange
+            int sh = 0;
+            while (sh + 1 < p.oP && t >= p.ostart[sh + 1]) ++sh;
+            orow = p.obase[sh] + (t - p.ostart[sh]) * p.oSS + h * p.oSH;
+        }
 #pragma unroll 1
         for (int c0 = 0; c0 < D; c0 += 32) {
             uint32_t o[32];
@@ -756,7 +768,7 @@ __global__ void __launch_bounds__(kThreads, 2)
 template <int D>
 cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                      pasa_route_s* r, const pasa_tensor& out, cudaStream_t st, char* why,
-                     size_t why_len) {
+                     size_t why_len, const ZcShards* osh) {
     CUtensorMap mQ, mK, mV, mKb, mVs, mHt;
     auto act = [&](CUtensorMap* m, const pasa_tensor& t, uint32_t rows) {
         uint64_t dims[4] = {(uint64_t)t.D, (uint64_t)t.S, (uint64_t)t.H, (uint64_t)t.B};
@@ -803,6 +815,16 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
     prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
     prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
     prm.sq = r->sq8; prm.kamax = r->kamax; prm.kbamax = r->kbamax;
+    prm.oP = 0;
+    if (osh) {
+        prm.oP = osh->P;
+        for (int s = 0; s <= osh->P; ++s) prm.ostart[s] = osh->start[s];
+        for (int s = 0; s < osh->P; ++s)
+            prm.obase[s] = reinterpret_cast<__nv_bfloat16*>(const_cast<void*>(osh->base[s])) +
+                           r->cfg.head_offset * osh->sH;
+        prm.oSS = osh->sS;
+        prm.oSH = osh->sH;
+    }
     prm.trace = g_trace_buf;
     prm.trace_x = g_trace_x;
     prm.trace_y = g_trace_y;
@@ -837,7 +859,7 @@ cudaError_t launch_d(const pasa_tensor& q, const pasa_tensor& k, const pasa_tens
 
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
-                              int* launches, char* why, size_t why_len) {
+                              int* launches, char* why, size_t why_len, const ZcShards* osh) {
     if (r->cfg.Bq != kBQ || r->cfg.Bk != kBK) {
         snprintf(why, why_len, "needs Bq=128, Bk=64");
         return cudaErrorNotSupported;
@@ -851,8 +873,8 @@ cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const 
         snprintf(why, why_len, "N_K > %d", kMaxNK);
         return cudaErrorNotSupported;
     }
-    cudaError_t e = r->D == 128 ? launch_d<128>(q, k, v, r, out, st, why, why_len)
-                                : launch_d<64>(q, k, v, r, out, st, why, why_len);
+    cudaError_t e = r->D == 128 ? launch_d<128>(q, k, v, r, out, st, why, why_len, osh)
+                                : launch_d<64>(q, k, v, r, out, st, why, why_len, osh);
     if (e == cudaSuccess) *launches += 1;
     return e;
 }

@@ -71,6 +71,20 @@ struct pasa_route_s {
 
 namespace pasa {
 
+// Zero-copy sequence parallelism (pasa_route_zc / pasa_attn_zc): a [1, S, H, D] bf16 tensor
+// held as P sequence shards, each addressable from this process (peer / IPC mapped);
+// shard s holds tokens [start[s], start[s+1]) at base[s] (its first token, head 0) with
+// element strides sS (token) and sH (head)
+struct ZcShards {
+    int32_t P;
+    int64_t start[9];
+    const void* base[8];
+    int64_t sS, sH;
+};
+cudaError_t launch_route_zc(const ZcShards* qkv, const pasa_tensor* loc, const pasa_budget_s* b,
+                            uint64_t seed, int32_t step, pasa_route_s* r, cudaStream_t st,
+                            int* launches);
+
 // ---- launchers (each returns cudaGetLastError() after its launches) -------
 // local_sum != nullptr: store the fp64 sum of |dv| there instead of finishing the record
 cudaError_t launch_budget(const void* xt, const void* xtm1, const void* xtm2, int64_t n, int dtype,
@@ -115,7 +129,8 @@ inline bool sm100_supports_group(int64_t G, int64_t NK) {
 // returns cudaErrorNotSupported if the configuration is outside the kernel's domain
 cudaError_t launch_attn_sm100(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor& v,
                               pasa_route_s* r, const pasa_tensor& out, cudaStream_t st,
-                              int* launches, char* why, size_t why_len);
+                              int* launches, char* why, size_t why_len,
+                              const ZcShards* out_shards = nullptr);
 // Bq = 256: one CTA per SM, two 128-row tiles sharing every
 // operand tile the op brings from L2; attn_sm100_q256.cu
 bool attn_sm100_q256_supported(const pasa_route_s* r);

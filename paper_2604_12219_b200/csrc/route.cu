@@ -179,6 +179,77 @@ __global__ void __launch_bounds__(256, 4) pool_kernel(PoolArgs qa, PoolArgs ka, 
 }
 
 // ---------------------------------------------------------------------------
+// Zero-copy sequence parallelism ("Ulysses all-to-all fused with
+// attention over NVLink"): the rank's heads of q, k, v are read straight from every rank's
+// sequence shard through peer pointers, copied into this rank's local [1, S, Hl, D] buffers
+// and -- for q and k -- pooled in the same pass (the same ascending-token fp64 sums as
+// pool_task, so Qbar / Kbar are bitwise those of the single-GPU path).  The input half of
+// the Ulysses exchange is thereby fused into the route's pooling pass; the output half is
+// the attention epilogue storing each row into its owner's shard (attn_sm100.cu).
+// One thread per (tensor, local head, block, 8 consecutive dims), tasks q | k | v.
+// ---------------------------------------------------------------------------
+struct ZcArgs {
+    ZcShards src[3];                 // q, k, v shards (element offsets per token / head)
+    __nv_bfloat16* loc[3];           // local q, k, v [1][S][Hl][D]
+    int64_t lsS[3], lsH[3];          // local strides
+    int64_t S, Hl, D, head0;
+    int32_t bsz[3];                  // block size of the task's tensor (Bq, Bk, Bk)
+    int64_t nblk[3];                 // blocks per head
+    int64_t it0, it1;                // the handle's (head, q-block) items (q pooled only there)
+    double* out[2];                  // Qbar [Hl][NQ][D], Kbar [Hl][NK][D]
+    double* kfrag;                   // Kbar in DMMA B-fragment order
+    int64_t ntask[3];                // tasks per tensor
+};
+
+__global__ void __launch_bounds__(256, 4) zc_gather_pool_kernel(ZcArgs a) {
+    int64_t task = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    int x = 0;
+    while (x < 3 && task >= a.ntask[x]) { task -= a.ntask[x]; ++x; }
+    if (x == 3) return;
+    const int64_t ng = a.D / 8;
+    const int64_t dg = task % ng, rest = task / ng;
+    const int64_t blk = rest % a.nblk[x], h = rest / a.nblk[x];
+    const int64_t t0 = blk * a.bsz[x], t1 = min(t0 + (int64_t)a.bsz[x], a.S);
+    const ZcShards& sh = a.src[x];
+    const bool pool = x < 2 && (x == 1 || (h * a.nblk[0] + blk >= a.it0 && h * a.nblk[0] + blk < a.it1));
+    double acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+    int s = 0;
+    while (s + 1 < sh.P && t0 >= sh.start[s + 1]) ++s;
+    __nv_bfloat16* dst = a.loc[x] + h * a.lsH[x] + dg * 8;
+    for (int64_t t = t0; t < t1; ++t) {
+        while (s + 1 < sh.P && t >= sh.start[s + 1]) ++s;   // a block may straddle shards
+        const __nv_bfloat16* src = reinterpret_cast<const __nv_bfloat16*>(sh.base[s]) +
+                                   (t - sh.start[s]) * sh.sS + (a.head0 + h) * sh.sH + dg * 8;
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(src));
+        *reinterpret_cast<uint4*>(dst + t * a.lsS[x]) = u;
+        if (pool) {
+            const __nv_bfloat162* bv = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                acc[2 * i] = __dadd_rn(acc[2 * i], (double)__bfloat162float(bv[i].x));
+                acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], (double)__bfloat162float(bv[i].y));
+            }
+        }
+    }
+    if (!pool) return;
+    const double n = (double)(t1 - t0);
+    double m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = __ddiv_rn(acc[i], n);
+    double2* o = reinterpret_cast<double2*>(a.out[x] + (h * a.nblk[x] + blk) * a.D + dg * 8);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) o[i] = make_double2(m[2 * i], m[2 * i + 1]);
+    if (x == 1) {   // the fused kernel's B-fragment copy of Kbar (as pool_task)
+        double2* f = reinterpret_cast<double2*>(
+            a.kfrag + ((h * ((a.nblk[1] + 7) / 8) + blk / 8) * (a.D / 8) + dg) * 64 + (blk % 8) * 8);
+#pragma unroll
+        for (int fk = 0; fk < 4; ++fk) f[fk] = make_double2(m[fk], m[4 + fk]);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // shared helpers of the fused kernel
 // ---------------------------------------------------------------------------
 // fp64 tensor core: d (+)= a * b on an 8x8x4 tile.  Measured on this pool
@@ -616,6 +687,10 @@ constexpr size_t fused_fixed_smem(int R, int D) {
 
 }  // namespace
 
+static cudaError_t launch_route_fused(const pasa_budget_s* b, uint64_t seed, int32_t step,
+                                      pasa_route_s* r, const double* prior, cudaStream_t st,
+                                      int* launches);
+
 cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_tensor* v,
                          const pasa_budget_s* b, uint64_t seed, int32_t step, pasa_route_s* r,
                          cudaStream_t st, int* launches) {
@@ -645,6 +720,14 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
         if (e != cudaSuccess) return e;
         prior = r->prior;
     }
+    *launches += 1;
+    return launch_route_fused(b, seed, step, r, prior, st, launches);
+}
+
+// a3 + a4 + a5: the fused score / sigma / top-k kernel over the pooled means in the workspace
+static cudaError_t launch_route_fused(const pasa_budget_s* b, uint64_t seed, int32_t step,
+                                      pasa_route_s* r, const double* prior, cudaStream_t st,
+                                      int* launches) {
     const double s = 1.0 / sqrt((double)r->D);
     FusedArgs fa;
     fa.qbar = r->qbar; fa.kfrag = r->kfrag; fa.prior = prior; fa.rec = b->rec;
@@ -674,8 +757,34 @@ cudaError_t launch_route(const pasa_tensor& q, const pasa_tensor& k, const pasa_
         kfn<<<grid, 32 * RR, smem, st>>>(fa);
         e = cudaGetLastError();
     }
-    *launches += 2;
+    *launches += 1;
     return e;
+}
+
+cudaError_t launch_route_zc(const ZcShards* qkv, const pasa_tensor* loc, const pasa_budget_s* b,
+                            uint64_t seed, int32_t step, pasa_route_s* r, cudaStream_t st,
+                            int* launches) {
+    ZcArgs a;
+    for (int x = 0; x < 3; ++x) {
+        a.src[x] = qkv[x];
+        a.loc[x] = reinterpret_cast<__nv_bfloat16*>(loc[x].data);
+        a.lsS[x] = loc[x].sS;
+        a.lsH[x] = loc[x].sH;
+    }
+    a.S = r->S; a.Hl = r->H; a.D = r->D; a.head0 = r->cfg.head_offset;
+    a.bsz[0] = r->cfg.Bq; a.bsz[1] = a.bsz[2] = r->cfg.Bk;
+    a.nblk[0] = r->NQ; a.nblk[1] = a.nblk[2] = r->NK;
+    a.it0 = r->it0; a.it1 = r->it1;
+    a.out[0] = r->qbar; a.out[1] = r->kbar; a.kfrag = r->kfrag;
+    const int64_t ng = r->D / 8;
+    int64_t total = 0;
+    for (int x = 0; x < 3; ++x) total += (a.ntask[x] = r->H * a.nblk[x] * ng);
+    const unsigned grid = (unsigned)((total + 255) / 256);
+    zc_gather_pool_kernel<<<grid, 256, 0, st>>>(a);
+    cudaError_t e = cudaGetLastError();
+    *launches += 1;
+    if (e != cudaSuccess) return e;
+    return launch_route_fused(b, seed, step, r, nullptr, st, launches);
 }
 
 // A/B knob: score rows in shared memory at one CTA per SM when two do not fit (measured

@@ -227,3 +227,69 @@ class Ulysses:
             dst = out_s.view(B, Sl, P, Hl, self.D)[:, :, :, c * hc:(c + 1) * hc]
             dst.copy_(self.recv["o"][c].permute(1, 2, 0, 3, 4))
         return out_s
+
+
+def share_tensor(x: torch.Tensor, group=None) -> List[torch.Tensor]:
+    """Every rank's ``x`` mapped into this process (CUDA IPC through torch's
+    multiprocessing reductions; over NVLink P2P between GPUs of one node, or the same
+    device memory when ranks share a GPU).  Returns the list indexed by rank (this rank's
+    own entry is ``x`` itself).  Collective: every rank calls it with its tensor."""
+    from multiprocessing.reduction import ForkingPickler
+
+    import torch.multiprocessing  # noqa: F401  (registers the CUDA IPC reductions)
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return [x]
+    rank = dist.get_rank(group)
+    blobs: List[Optional[bytes]] = [None] * world
+    dist.all_gather_object(blobs, bytes(ForkingPickler.dumps(x)), group=group)
+    return [x if r == rank else ForkingPickler.loads(blobs[r]) for r in range(world)]
+
+
+class ZeroCopyUlysses:
+    """Sequence-sharded input without an all-to-all: the Ulysses exchange fused into PASA's
+    own kernels over peer memory (include/pasa.h pasa_route_zc /
+    pasa_attn_zc).  Rank r owns heads [r H/P, (r+1) H/P).  ``pasa_route_zc`` reads those
+    heads of q, k, v from every rank's shard through its peer mapping into local
+    [1, S, Hl, D] buffers while pooling q and k in the same pass; ``pasa_attn_zc`` stores
+    each output row straight into the shard of the rank that owns its token.  The shards
+    are mapped once (``share_tensor``); each call synchronises the ranks before the gather
+    (every shard written) and after the attention (every output row delivered): a device
+    synchronise plus a process-group barrier, so no kernel ever waits on another rank's.
+    B = 1, bf16; shards may be uneven and need not align to blocks."""
+
+    def __init__(self, q_s, k_s, v_s, out_s, H: int, route_cfg, group=None):
+        from . import api
+
+        self.group = group
+        self.P = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.h0, self.Hl = head_range(H, self.P, self.rank)
+        self.maps = {n: share_tensor(t, group) for n, t in
+                     (("q", q_s), ("k", k_s), ("v", v_s), ("o", out_s))}
+        S = sum(t.shape[1] for t in self.maps["q"])
+        D = q_s.shape[3]
+        self.S, self.D = S, D
+        dev = q_s.device
+        self.loc = [torch.empty((1, S, self.Hl, D), dtype=q_s.dtype, device=dev) for _ in range(3)]
+        import dataclasses
+        cfg = dataclasses.replace(route_cfg, H_total=H, head_offset=self.h0)
+        self.route = api.Route(1, S, self.Hl, D, cfg, dev)
+
+    def _sync(self):
+        torch.cuda.current_stream().synchronize()
+        if self.P > 1:
+            dist.barrier(group=self.group)
+
+    def __call__(self, budget, seed: int, step: int, sync: bool = True):
+        """One PASA step of this rank's heads; the output lands in every rank's out shard."""
+        from . import api
+
+        if sync:
+            self._sync()
+        api.route_zc(self.route, self.maps["q"], self.maps["k"], self.maps["v"], budget, seed,
+                     step, *self.loc)
+        api.attn_zc(*self.loc, self.route, self.maps["o"])
+        if sync:
+            self._sync()

@@ -171,6 +171,16 @@ def _rank_main(rank, world, port, mode, result):
             uly(q[:, ss].contiguous(), k[:, ss].contiguous(), v[:, ss].contiguous(), out, compute)
             torch.cuda.synchronize()
             result[rank] = (ss.start, ss.stop, out.cpu())
+        elif mode == "zerocopy":
+            # uneven, block-misaligned sequence shards; the exchange fused into PASA's kernels
+            cut = [0, 1901, S]
+            a, b = cut[rank], cut[rank + 1]
+            q_s, k_s, v_s = (t[:, a:b].contiguous() for t in (q, k, v))
+            out_s = torch.full_like(q_s, float("nan"))
+            zc = pdist.ZeroCopyUlysses(q_s, k_s, v_s, out_s, H, P.RouteCfg(Bq=128, G=32, beta=0.1))
+            zc(budget, seed, step)
+            torch.cuda.synchronize()
+            result[rank] = (a, b, out_s.cpu())
         else:   # flattened (head, q-block) partition
             NQ = (S + 127) // 128
             segs = pdist.flat_partition(H, NQ, world, rank)
@@ -203,14 +213,14 @@ def _single(P):
     return budget.read(), out.cpu()
 
 
-@pytest.mark.parametrize("mode", ["budget", "ulysses", "flat"])
+@pytest.mark.parametrize("mode", ["budget", "ulysses", "flat", "zerocopy"])
 def test_two_ranks_reproduce_single_process(pasa, mode):
     rec, ref = _single(pasa)
     res = mp.Manager().dict()
     mp.spawn(_rank_main, args=(2, _port(), mode, res), nprocs=2, join=True)
     if mode == "budget":
         assert res[0] == res[1] == rec
-    elif mode == "ulysses":
+    elif mode in ("ulysses", "zerocopy"):
         for r in range(2):
             a, b, o = res[r]
             assert torch.equal(o, ref[:, a:b]), r
@@ -226,3 +236,48 @@ def test_two_ranks_reproduce_single_process(pasa, mode):
                     t0, t1 = i * 128, min((i + 1) * 128, ref.shape[1])
                     got[:, t0:t1, hh] = o[:, t0:t1, hh]
         assert torch.equal(got, ref)
+
+
+
+@pytest.mark.parametrize("cuts,heads_split", [
+    ((0, 1901, 4096), 2),                 # two uneven shards, block-misaligned
+    ((0, 700, 2049, 2050, 4096), 4),      # a one-token shard; ranks of 1 head each
+    ((0, 4096), 1),                       # one shard (P = 1)
+])
+def test_zero_copy_shards_match_single_tensor(pasa, cuts, heads_split):
+    """pasa_route_zc / pasa_attn_zc in one process: the sequence shards are separate
+    tensors (boundaries inside blocks, one of a single token), every "rank" routes its
+    heads from all shards and writes its output rows into the shards that own them; the
+    route of each head range and the assembled output equal the single-tensor path bit
+    for bit."""
+    P = pasa
+    from paper_2604_12219_b200 import dist as pdist
+    q, k, v, xs, kw = _inputs()
+    B, S, H, D = q.shape
+    budget = _budget(P)
+    seed, step = P.layer_seed(42, 0), 30
+    full = P.Route(B, S, H, D, P.RouteCfg(Bq=128, G=32, beta=0.1))
+    full(q, k, budget, seed, step)
+    ref = P.attn(q, k, v, full)
+    want = full.read()
+    shards = {n: [t[:, a:b].contiguous() for a, b in zip(cuts[:-1], cuts[1:])]
+              for n, t in (("q", q), ("k", k), ("v", v))}
+    outs = [torch.full_like(x, float("nan")) for x in shards["q"]]
+    for r in range(heads_split):
+        h0, hl = pdist.head_range(H, heads_split, r)
+        route = P.Route(1, S, hl, D, P.RouteCfg(Bq=128, G=32, beta=0.1, H_total=H, head_offset=h0))
+        route.ws.fill_(0xFF)
+        loc = [torch.full((1, S, hl, D), float("nan"), dtype=q.dtype, device=q.device)
+               for _ in range(3)]
+        P.route_zc(route, shards["q"], shards["k"], shards["v"], budget, seed, step, *loc)
+        torch.cuda.synchronize()
+        assert torch.equal(loc[0], q[:, :, h0:h0 + hl]) and torch.equal(loc[2], v[:, :, h0:h0 + hl])
+        got = route.read()
+        kk = got["k"]
+        assert kk == want["k"]
+        for key in ("count", "mask"):
+            assert np.array_equal(got[key], want[key][h0:h0 + hl]), key
+        assert np.array_equal(got["idx"][:, :, :kk], want["idx"][h0:h0 + hl, :, :kk])
+        P.attn_zc(*loc, route, outs)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat(outs, 1), ref)
