@@ -69,6 +69,11 @@ def parse(argv=None):
                     help="work split over ranks: contiguous heads, or the flattened (head, "
                          "q-block) list (SURVEY.md §8e; auto: flat when the heads do not divide "
                          "the rank count, e.g. Wan-1.3B's 12 heads over 8 GPUs)")
+    ap.add_argument("--ulysses", default="nccl", choices=["nccl", "zc"],
+                    help="sequence-sharded input: head-chunked NCCL all-to-all overlapped with "
+                         "PASA per chunk (nccl), or zero-copy: PASA's kernels read every rank's "
+                         "shard through peer memory and store output rows into their owners' "
+                         "shards (zc; pasa_route_zc / pasa_attn_zc)")
     ap.add_argument("--ulysses-chunks", type=int, default=0,
                     help="head groups of the sequence-sharded Ulysses all-to-all (attention on "
                          "arrived heads overlaps the rest; 0 = auto, up to 4)")
@@ -380,6 +385,7 @@ def run_pasa(args):
                           qk_precision=args.qk_precision)
 
     rcfg = rcfg_for(off)
+    zc = None   # zero-copy sequence parallelism (--ulysses zc)
     if seq_sharded:
         # sequence-sharded input [B, S/P, H, D] and latents: the step is the sharded budget
         # (one fp64 partial per rank, all_gather) and the chunked Ulysses all-to-all with
@@ -393,6 +399,12 @@ def run_pasa(args):
         # chunks only pay with a transfer to overlap: one at N = 1
         n_chunks_u = args.ulysses_chunks or (
             1 if world == 1 else max(c for c in (1, 2, 3, 4) if (H // world) % c == 0))
+        if args.ulysses == "zc":
+            if use_v or args.qk_precision != "bf16" or args.cta_pair or cfg["Bq"] != 128:
+                raise SystemExit("--ulysses zc: Bq = 128 bf16 path without prior / FP8 / pair")
+            n_chunks_u = 1
+            # the shards are mapped into every rank (CUDA IPC) once, outside the timed region
+            zc = pdist.ZeroCopyUlysses(q_s, k_s, v_s, out_s, H, rcfg_for(0))
         uly = pdist.Ulysses(B, S, H, D, q.dtype, dev, chunks=n_chunks_u)
         chunk_routes = {}
         chunk_ev = []   # per chunk: [before route, after route, after stats, after attn]
@@ -416,13 +428,18 @@ def run_pasa(args):
             launches[0] += P.last_launch_count()
             if evs:
                 evs[3].record(stream)
-        # the first call builds the chunk handles (outside any timed region)
-        chunk_ev.append(None)
-        uly(q_s, k_s, v_s, out_s, compute)
-        route = chunk_routes[0]
-        # this rank's head-sharded tensors (dense-attention context): chunk 0 as received
-        q, k, v = ((q_s, k_s, v_s) if world == 1 else
-                   tuple(uly._heads(uly.recv[n][0]) for n in "qkv"))
+        if zc is not None:
+            zc(budget, seed, t_step)
+            route = zc.route
+            q, k, v = zc.loc    # this rank's heads, gathered (dense-attention context)
+        else:
+            # the first call builds the chunk handles (outside any timed region)
+            chunk_ev.append(None)
+            uly(q_s, k_s, v_s, out_s, compute)
+            route = chunk_routes[0]
+            # this rank's head-sharded tensors (dense-attention context): chunk 0 as received
+            q, k, v = ((q_s, k_s, v_s) if world == 1 else
+                       tuple(uly._heads(uly.recv[n][0]) for n in "qkv"))
     else:
         units = []
         for h, n, a, b in segs:
@@ -442,6 +459,23 @@ def run_pasa(args):
         do_budget()
         if ev is not None:
             ev[0].record(stream)
+        if seq_sharded and zc is not None:
+            # zero copy: every shard complete on every rank, gather + pool + route, then
+            # statistics + attention storing rows into their owners' shards, all ranks done
+            if world > 1:
+                zc.sync()
+            zc.gather_route(budget, seed, t_step)
+            launches[0] += P.last_launch_count()
+            if ev is not None:
+                ev[1].record(stream)
+                ev[2].record(stream)   # the statistics run inside pasa_attn_zc (counted there)
+            zc.attend()
+            launches[0] += P.last_launch_count()
+            if ev is not None:
+                ev[3].record(stream)
+            if world > 1:
+                zc.sync()
+            return
         if seq_sharded:
             if ev is not None:
                 chunk_ev.append([[torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -501,7 +535,7 @@ def run_pasa(args):
     for it in range(K):
         prev = e_start if it == 0 else evs[it - 1][3]
         ph[0] += prev.elapsed_time(evs[it][0])
-        if seq_sharded:   # route / stats / attention summed over the Ulysses chunks
+        if seq_sharded and zc is None:   # route / stats / attention summed over the chunks
             for ce in chunk_ev[-K + it]:
                 for j in range(1, 4):
                     ph[j] += ce[j - 1].elapsed_time(ce[j])
@@ -517,7 +551,7 @@ def run_pasa(args):
 
     # ---------------- the same step captured once in a CUDA graph, replayed K times -----
     graph = None
-    if not args.no_graph and not (seq_sharded and world > 1):   # no collective inside a capture
+    if not args.no_graph and not (seq_sharded and world > 1):   # no collective / sync inside a capture
         try:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
@@ -626,7 +660,20 @@ def run_pasa(args):
         # head chunks: about one per 0.12 ms of device step (enough work per chunk to fill
         # the GPU and hide the per-chunk launches; Wan-14B 20, CogVideoX / Wan-1.3B 12)
         n_chunks = args.e2e_chunks or max(4, min(20, round(t_max / 0.12)))
-        if seq_sharded and world > 1:
+        if seq_sharded and zc is not None:
+            # host shard -> this rank's (IPC-shared) device shard -> sharded budget -> zero-copy
+            # PASA (rows land in their owners' shards) -> host shard
+            dx = [torch.empty_like(x) for x in xs_sh]
+            hx = [x.cpu().pin_memory() for x in xs_sh]
+            h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv, *hx))
+
+            def e2e_step():
+                for d, hsrc in zip((q_s, k_s, v_s, *dx), (hq, hk, hv, *hx)):
+                    d.copy_(hsrc, non_blocking=True)
+                pdist.sharded_budget(budget, *dx, n_total=x_t.numel(), **bkw)
+                zc(budget, seed, t_step, sync=world > 1)
+                hout.copy_(out_s, non_blocking=True)
+        elif seq_sharded and world > 1:
             # host shards -> device -> sharded budget -> chunked Ulysses + PASA -> host shard
             dsq, dsk, dsv = (torch.empty_like(t) for t in src)
             dx = [torch.empty_like(x) for x in xs_sh]
@@ -763,7 +810,8 @@ def run_pasa(args):
             "workload": args.config, "B": B, "S": S, "H": H, "D": D,
             "heads_per_rank": work_heads, "nranks": world, "heads_per_rank_all": heads_all,
             "partition": partition, "segments": segs if partition == "flat" else None,
-            "ulysses_chunks": uly.C if seq_sharded else None,
+            "ulysses_chunks": (("zero-copy" if zc is not None else uly.C) if seq_sharded
+                               else None),
             "dist_backend": (args.dist_backend + (" (debug: ranks share GPUs, timings not "
                                                   "meaningful)" if gloo else "")) if world > 1
             else None,

@@ -277,19 +277,28 @@ class ZeroCopyUlysses:
         cfg = dataclasses.replace(route_cfg, H_total=H, head_offset=self.h0)
         self.route = api.Route(1, S, self.Hl, D, cfg, dev)
 
-    def _sync(self):
+    def sync(self):
+        """Every rank's work so far complete (device synchronise + barrier)."""
         torch.cuda.current_stream().synchronize()
         if self.P > 1:
             dist.barrier(group=self.group)
 
-    def __call__(self, budget, seed: int, step: int, sync: bool = True):
-        """One PASA step of this rank's heads; the output lands in every rank's out shard."""
+    def gather_route(self, budget, seed: int, step: int):
+        """pasa_route_zc: this rank's heads gathered from every shard, pooled, routed."""
         from . import api
-
-        if sync:
-            self._sync()
         api.route_zc(self.route, self.maps["q"], self.maps["k"], self.maps["v"], budget, seed,
                      step, *self.loc)
+
+    def attend(self):
+        """pasa_attn_zc: statistics + attention, rows stored into their owners' out shards."""
+        from . import api
         api.attn_zc(*self.loc, self.route, self.maps["o"])
+
+    def __call__(self, budget, seed: int, step: int, sync: bool = True):
+        """One PASA step of this rank's heads; the output lands in every rank's out shard."""
         if sync:
-            self._sync()
+            self.sync()
+        self.gather_route(budget, seed, step)
+        self.attend()
+        if sync:
+            self.sync()
