@@ -144,3 +144,54 @@ def test_route_attn_host_validation(L):
                        ctypes.byref(good), None) == _C.PASA_EINVAL
     L.pasa_route_fini(h)
     L.pasa_budget_fini(hb)
+
+
+def test_zero_copy_host_validation(L):
+    """pasa_route_zc / pasa_attn_zc reject bad shard tables on the host, launching nothing:
+    NULL handles, a shard table whose starts do not cover [0, S), a head range outside the
+    shards' H, fp32 shards, misaligned bases, and attention before a zero-copy route."""
+    c = cfg(H_total=4)
+    c.head_offset = 2
+    h = ctypes.c_void_p()
+    fake = ctypes.c_void_p(0x10000)
+    n = L.pasa_route_workspace_bytes(ctypes.byref(c), 1, 1000, 2, 64)
+    assert L.pasa_route_init(fake, n, ctypes.byref(c), 1, 1000, 2, 64, ctypes.byref(h)) == 0
+    hb = ctypes.c_void_p()
+    assert L.pasa_budget_init(fake, L.pasa_budget_workspace_bytes(), ctypes.byref(hb)) == 0
+    loc = _C.PasaTensor(0x40000, 0, 0, 1, 1000, 2, 64, 1000 * 128, 128, 64)
+
+    def shards(H=4, starts=(0, 400, 1000), dtype=0, base=0x80000):
+        d = _C.PasaShards()
+        d.dtype, d.nshards, d.S, d.H, d.D, d.sS, d.sH = dtype, len(starts) - 1, 1000, H, 64, H * 64, 64
+        for i, s in enumerate(starts):
+            d.start[i] = s
+        for i in range(len(starts) - 1):
+            d.data[i] = base + i * 0x100000
+        return d
+
+    good = shards()
+    args = lambda q, hh=h, bb=hb: (ctypes.byref(q), ctypes.byref(good), ctypes.byref(good), bb, 1,  # noqa: E731
+                                   3, hh, ctypes.byref(loc), ctypes.byref(loc), ctypes.byref(loc), None)
+    assert L.pasa_route_zc(*args(good, hh=None)) == _C.PASA_EINVAL
+    assert L.pasa_route_zc(*args(shards(starts=(0, 400, 999)))) == _C.PASA_EINVAL     # S not covered
+    assert L.pasa_route_zc(*args(shards(starts=(0, 400, 400, 1000)))) == _C.PASA_EINVAL  # empty shard
+    assert L.pasa_route_zc(*args(shards(H=3))) == _C.PASA_EINVAL                       # heads 2..3 of 3
+    assert L.pasa_route_zc(*args(shards(dtype=1))) == _C.PASA_EDTYPE
+    assert L.pasa_route_zc(*args(shards(base=0x80004))) == _C.PASA_EINVAL              # misaligned
+    assert L.pasa_attn_zc(ctypes.byref(loc), ctypes.byref(loc), ctypes.byref(loc), h,
+                          ctypes.byref(good), None) == _C.PASA_EINVAL   # no route built yet
+    L.pasa_route_fini(h)
+    L.pasa_budget_fini(hb)
+
+
+def test_shards_desc_layout():
+    """The Python shard table: starts accumulate the shard lengths, strides are checked."""
+    import torch
+    from paper_2604_12219_b200 import api
+    xs = [torch.zeros(1, n, 3, 64, dtype=torch.bfloat16) for n in (5, 1, 10)]
+    # tensor_desc needs CUDA; shards_desc only reads shapes, strides and data pointers
+    d = api.shards_desc(xs)
+    assert d.nshards == 3 and d.S == 16 and list(d.start[:4]) == [0, 5, 6, 16]
+    assert d.sS == 3 * 64 and d.sH == 64
+    with pytest.raises(ValueError):
+        api.shards_desc([xs[0], torch.zeros(1, 4, 2, 64, dtype=torch.bfloat16)])
