@@ -611,6 +611,8 @@ pasa_status pasa_attn_zc(const pasa_tensor* q_loc, const pasa_tensor* k_loc,
     if (e != cudaSuccess) { g_launches = launches; return cuda_status(e, "kv_stats launch"); }
     route->stats_dtype = PASA_BF16;
     char why[256] = {0};
+    // the `out` argument is only a shape carrier here: with output shards every row the
+    // kernel stores goes to its owner's shard (rows past S are never stored)
     e = pasa::launch_attn_sm100(*q_loc, *k_loc, *v_loc, route, *q_loc, s, &launches, why,
                                 sizeof(why), &osh);
     g_launches = launches;
