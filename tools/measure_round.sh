@@ -15,6 +15,8 @@ done
 timeout 400 python bench.py --qk-precision fp8 --no-cpu > gpurun_out/bench_wan14b_fp8.json 2> gpurun_out/bench_wan14b_fp8.err
 timeout 400 python bench.py --bq 256 --cta-pair --no-cpu --no-dense > gpurun_out/bench_wan14b_q256_pair.json 2> gpurun_out/bench_wan14b_q256_pair.err
 timeout 400 python bench.py --bq 256 --no-cpu --no-dense > gpurun_out/bench_wan14b_q256.json 2> gpurun_out/bench_wan14b_q256.err
+# the zero-copy sequence-parallel path (no all-to-all; the exchange fused into PASA's kernels)
+timeout 400 python bench.py --config hunyuan_720p --ulysses zc --no-cpu --no-dense > gpurun_out/bench_hunyuan_720p_zc.json 2> gpurun_out/bench_hunyuan_720p_zc.err
 # the NCCL plumbing at N = 1 (init, barriers, MAX all-reduce), as the driver launches N > 1
 timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 \
   --master-port 29511 bench.py --gpus 1 --no-cpu --no-dense > gpurun_out/bench_wan14b_torchrun1.json 2> gpurun_out/bench_wan14b_torchrun1.err
