@@ -67,6 +67,12 @@ constexpr bool kD128QT = PASA_D128_QTMEM != 0;
 #ifndef PASA_WARP_ARRIVE
 #define PASA_WARP_ARRIVE 0
 #endif
+// prologue (A/B knob): 1 = thread 0 issues the Q tile and the first kept blocks' K / V
+// loads right after initialising the barriers, before the op-list tail, TMEM allocation and
+// the CTA barrier (the per-CTA fixed cost is ~6 us per wave: tools/ops_scaling.py)
+#ifndef PASA_EARLY_LOADS
+#define PASA_EARLY_LOADS 0
+#endif
 #ifndef PASA_CRIT_WAIT
 #define PASA_CRIT_WAIT 0
 #endif
@@ -197,6 +203,76 @@ __global__ void __launch_bounds__(kThreads, 2)
     const int64_t NK = p.NK;
     const int nchunks = (int)((NK + 63) / 64);
 
+    // ---------------- loads (K ring: warp 0, V ring: warp 2; the first ones by thread 0) ----
+    auto load_q = [&]() {
+        if constexpr (F8) {
+            mbar_arrive_expect_tx(&ctl.q_full, kBQ * D);
+            tma_load_3d(smem + G_::OFF_Q, &tmQ, &ctl.q_full, 0, (int)(i * kBQ), (int)bh);
+        } else {
+            mbar_arrive_expect_tx(&ctl.q_full, kBQ * D * 2);
+#pragma unroll
+            for (int a = 0; a < G_::NBOX; ++a)
+                tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
+                            (int)(i * kBQ), (int)h, (int)b);
+        }
+    };
+    auto load_k = [&](int n, int32_t op) {   // op n into K slot n % NKS (slot known free)
+        const int s = n % G_::NKS;
+        uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
+        const int v = op_val(op);
+        if (DIAG && (p.dbg & 2)) {
+            mbar_arrive(&ctl.k_full[s]);
+        } else if (op_type(op) == OP_F) {
+            mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
+            tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
+        } else if constexpr (F8) {   // E4M3 K tile or Kbar chunk: 64 rows x 128 B
+            mbar_arrive_expect_tx(&ctl.k_full[s], kBK * D);
+            tma_load_3d(dst, op_type(op) == OP_E ? &tmK : &tmKb, &ctl.k_full[s], 0,
+                        v * kBK, (int)bh);
+        } else {
+            mbar_arrive_expect_tx(&ctl.k_full[s], G_::SLOT);
+#pragma unroll
+            for (int a = 0; a < G_::NBOX; ++a) {
+                if (op_type(op) == OP_E)
+                    tma_load_4d(dst + a * G_::KVBOX, &tmK, &ctl.k_full[s], 64 * a, v * kBK,
+                                (int)h, (int)b);
+                else
+                    tma_load_3d(dst + a * G_::KVBOX, &tmKb, &ctl.k_full[s], 64 * a, v * 64,
+                                (int)bh);
+            }
+        }
+    };
+    auto load_v = [&](int n, int32_t op) {   // op n into V slot n & 1 (slot known free)
+        const int s = n & 1, pb = n % G_::NB;
+        uint64_t* vbar = G_::NB == 1 ? &ctl.v_full[s] : &ctl.p_full[pb];
+        uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
+        const int v = op_val(op);
+        if (DIAG && (p.dbg & 2)) {
+            mbar_arrive(vbar);
+        } else if (op_type(op) == OP_F) {
+            if (G_::NBOX == 2) {
+                mbar_arrive_expect_tx(vbar, G_::HTBOX);
+                tma_load_3d(dst, &tmHt, vbar, 64, v * D, (int)bh);
+            } else {
+                mbar_arrive(vbar);
+            }
+        } else {
+            mbar_arrive_expect_tx(vbar, G_::SLOT);
+#pragma unroll
+            for (int a = 0; a < G_::NBOX; ++a) {
+                if (op_type(op) == OP_E)
+                    tma_load_4d(dst + a * G_::KVBOX, &tmV, vbar, 64 * a, v * kBK,
+                                (int)h, (int)b);
+                else
+                    tma_load_3d(dst + a * G_::KVBOX, &tmVs, vbar, 64 * a, v * 64, (int)bh);
+            }
+        }
+    };
+    // ops whose loads thread 0 issues in the prologue: kept blocks only (their index comes
+    // straight from the route), as many as the rings hold without waiting
+    const int n_pre_k = PASA_EARLY_LOADS ? min(cnt, G_::NKS) : 0;
+    const int n_pre_v = PASA_EARLY_LOADS ? min(cnt, 2) : 0;
+
     // ---------------- setup: op list, mask row, barriers, TMEM ----------------
     for (int w = tid; w < p.W; w += blockDim.x) ctl.mask[w] = p.mask[row * p.W + w];
     for (int q = tid; q < cnt; q += blockDim.x) ctl.ops[q] = op_make(OP_E, p.idx[row * NK + q]);
@@ -217,6 +293,15 @@ __global__ void __launch_bounds__(kThreads, 2)
         mbar_init(&ctl.pv_done[0], 1);
         mbar_init(&ctl.pv_done[1], 1);
         fence_barrier_init();
+        if (PASA_EARLY_LOADS) {   // thread 0 = the K producer's issuing lane
+            tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV);
+            load_q();
+            for (int n = 0; n < max(n_pre_k, n_pre_v); ++n) {
+                const int32_t op = op_make(OP_E, p.idx[row * NK + n]);
+                if (n < n_pre_k) load_k(n, op);
+                if (n < n_pre_v) load_v(n, op);
+            }
+        }
     }
     if (warp == 1) {
         tmem_alloc(&ctl.tmem_base, kTmemCols);
@@ -268,77 +353,19 @@ __global__ void __launch_bounds__(kThreads, 2)
     if (warp == 0) {
         // ======================= K-ring producer =======================
         if (lane == 0) {
-            if constexpr (F8) {
-                mbar_arrive_expect_tx(&ctl.q_full, kBQ * D);
-                tma_load_3d(smem + G_::OFF_Q, &tmQ, &ctl.q_full, 0, (int)(i * kBQ), (int)bh);
-            } else {
-                mbar_arrive_expect_tx(&ctl.q_full, kBQ * D * 2);
-#pragma unroll
-                for (int a = 0; a < G_::NBOX; ++a)
-                    tma_load_4d(smem + G_::OFF_Q + a * G_::QBOX, &tmQ, &ctl.q_full, 64 * a,
-                                (int)(i * kBQ), (int)h, (int)b);
-            }
-            for (int n = 0; n < nops; ++n) {
-                const int s = n % G_::NKS;
-                mbar_wait_sleep(&ctl.k_empty[s], ((n / G_::NKS) & 1) ^ 1);
-                uint8_t* dst = smem + G_::OFF_K + s * G_::SLOT;
-                const int32_t op = ctl.ops[n];
-                const int v = op_val(op);
-                if (DIAG && (p.dbg & 2)) {
-                    mbar_arrive(&ctl.k_full[s]);
-                } else if (op_type(op) == OP_F) {
-                    mbar_arrive_expect_tx(&ctl.k_full[s], G_::HTBOX);
-                    tma_load_3d(dst, &tmHt, &ctl.k_full[s], 0, v * D, (int)bh);
-                } else if constexpr (F8) {   // E4M3 K tile or Kbar chunk: 64 rows x 128 B
-                    mbar_arrive_expect_tx(&ctl.k_full[s], kBK * D);
-                    tma_load_3d(dst, op_type(op) == OP_E ? &tmK : &tmKb, &ctl.k_full[s], 0,
-                                v * kBK, (int)bh);
-                } else {
-                    mbar_arrive_expect_tx(&ctl.k_full[s], G_::SLOT);
-#pragma unroll
-                    for (int a = 0; a < G_::NBOX; ++a) {
-                        if (op_type(op) == OP_E)
-                            tma_load_4d(dst + a * G_::KVBOX, &tmK, &ctl.k_full[s], 64 * a, v * kBK,
-                                        (int)h, (int)b);
-                        else
-                            tma_load_3d(dst + a * G_::KVBOX, &tmKb, &ctl.k_full[s], 64 * a, v * 64,
-                                        (int)bh);
-                    }
-                }
+            if (!PASA_EARLY_LOADS) load_q();
+            for (int n = n_pre_k; n < nops; ++n) {
+                mbar_wait_sleep(&ctl.k_empty[n % G_::NKS], ((n / G_::NKS) & 1) ^ 1);
+                load_k(n, ctl.ops[n]);
             }
         }
         __syncwarp();
     } else if (warp == 2) {
         // ======================= V-ring producer =======================
         if (lane == 0) {
-            for (int n = 0; n < nops; ++n) {
-                const int s = n & 1, pb = n % G_::NB;
-                uint64_t* vbar = G_::NB == 1 ? &ctl.v_full[s] : &ctl.p_full[pb];
-                mbar_wait_sleep(&ctl.pv_done[s], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
-                uint8_t* dst = smem + G_::OFF_V + s * G_::SLOT;
-                const int32_t op = ctl.ops[n];
-                const int v = op_val(op);
-                if (DIAG && (p.dbg & 2)) {
-                    mbar_arrive(vbar);
-                } else if (op_type(op) == OP_F) {
-                    if (G_::NBOX == 2) {
-                        mbar_arrive_expect_tx(vbar, G_::HTBOX);
-                        tma_load_3d(dst, &tmHt, vbar, 64, v * D, (int)bh);
-                    } else {
-                        mbar_arrive(vbar);
-                    }
-                } else {
-                    mbar_arrive_expect_tx(vbar, G_::SLOT);
-#pragma unroll
-                    for (int a = 0; a < G_::NBOX; ++a) {
-                        if (op_type(op) == OP_E)
-                            tma_load_4d(dst + a * G_::KVBOX, &tmV, vbar, 64 * a, v * kBK,
-                                        (int)h, (int)b);
-                        else
-                            tma_load_3d(dst + a * G_::KVBOX, &tmVs, vbar, 64 * a, v * 64,
-                                        (int)bh);
-                    }
-                }
+            for (int n = n_pre_v; n < nops; ++n) {
+                mbar_wait_sleep(&ctl.pv_done[n & 1], ((n >> 1) & 1) ^ 1);   // PV(n-2) read the slot
+                load_v(n, ctl.ops[n]);
             }
         }
         __syncwarp();
