@@ -66,10 +66,12 @@ struct Params {
     const uint32_t* mask;
     __nv_bfloat16* out;
     int64_t osB, osS, osH;
+    int32_t* counter;   // dynamic item scheduler (zeroed before the launch)
 };
 
 struct List {
-    int32_t nops;
+    int32_t nops;           // -1: no more items (the scheduler ran past the range)
+    int32_t item;
     uint32_t mask[kMaxNK / 32];
     uint16_t ops[kMaxOps];
 };
@@ -98,10 +100,9 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t NK = p.NK;
-    // this CTA's items: it0 + blockIdx.x + j gridDim.x (head-major, so the CTAs in flight
-    // work on neighbouring q-blocks of the same heads: their K / V stay in L2)
-    const int64_t nitems = (p.it1 - p.it0 - (int64_t)blockIdx.x + gridDim.x - 1) / gridDim.x;
-    auto item_of = [&](int64_t j) { return p.it0 + (int64_t)blockIdx.x + j * gridDim.x; };
+    // items come from a global counter in head-major order, so the CTAs in flight always
+    // work on neighbouring q-blocks of the same heads and their K / V stay in L2 (a static
+    // stride lets the CTAs drift apart: the dual-tile kernel saw 3x the DRAM traffic)
 
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
@@ -136,11 +137,20 @@ __global__ void __launch_bounds__(kThreads, 2)
 
     if (warp == 3) {
         // ======================= op lists (one item ahead) =======================
-        for (int64_t j = 0; j < nitems; ++j) {
-            const int bb = (int)(j & 1);
+        for (int j = 0;; ++j) {
+            const int bb = j & 1;
             mbar_wait_sleep(&ctl.list_empty[bb], (uint32_t)(((j >> 1) & 1) ^ 1));
             List& L = ctl.list[bb];
-            const int64_t item = item_of(j);
+            int64_t item = 0;
+            if (lane == 0) item = p.it0 + atomicAdd(p.counter, 1);
+            item = __shfl_sync(0xffffffffu, item, 0);
+            if (item >= p.it1) {
+                if (lane == 0) {
+                    L.nops = -1;
+                    mbar_arrive(&ctl.list_full[bb]);
+                }
+                break;
+            }
             const int64_t row = item;   // item = bh * NQ + i
             const int32_t cnt = p.count[row];
             for (int w = lane; w < p.W; w += 32) L.mask[w] = p.mask[row * p.W + w];
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                     }
                 }
                 L.nops = n;
+                L.item = (int32_t)item;
                 mbar_arrive(&ctl.list_full[bb]);   // the warp's writes precede it (__syncwarp)
             }
             __syncwarp();
@@ -184,11 +195,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ======================= Q tiles + K ring =======================
         if (lane == 0) {
             int g0 = 0;
-            for (int64_t j = 0; j < nitems; ++j) {
-                const int bb = (int)(j & 1);
+            for (int j = 0;; ++j) {
+                const int bb = j & 1;
                 mbar_wait_sleep(&ctl.list_full[bb], (uint32_t)((j >> 1) & 1));
                 const List& L = ctl.list[bb];
-                const int64_t item = item_of(j);
+                if (L.nops < 0) break;
+                const int64_t item = L.item;
                 const int64_t i = item % p.NQ, bh = item / p.NQ;
                 const int64_t b = bh / p.H, h = bh % p.H;
                 // Q tile of item j into buffer j & 1 once item j-2 no longer reads it
@@ -224,11 +236,12 @@ __global__ void __launch_bounds__(kThreads, 2)
         // ======================= V ring =======================
         if (lane == 0) {
             int g0 = 0;
-            for (int64_t j = 0; j < nitems; ++j) {
-                const int bb = (int)(j & 1);
+            for (int j = 0;; ++j) {
+                const int bb = j & 1;
                 mbar_wait_sleep(&ctl.list_full[bb], (uint32_t)((j >> 1) & 1));
                 const List& L = ctl.list[bb];
-                const int64_t item = item_of(j);
+                if (L.nops < 0) break;
+                const int64_t item = L.item;
                 const int64_t bh = item / p.NQ;
                 const int64_t b = bh / p.H, h = bh % p.H;
                 const int nops = L.nops;
@@ -279,11 +292,12 @@ __global__ void __launch_bounds__(kThreads, 2)
             __syncwarp();
         };
         int g0 = 0;
-        for (int64_t j = 0; j < nitems; ++j) {
-            const int bb = (int)(j & 1);
+        for (int j = 0;; ++j) {
+            const int bb = j & 1;
             mbar_wait_sleep(&ctl.list_full[bb], (uint32_t)((j >> 1) & 1));
             const List& L = ctl.list[bb];
             const int nops = L.nops;
+            if (nops < 0) break;
             mbar_wait_sleep(&ctl.q_tmem, (uint32_t)(j & 1));   // item j's Q in TMEM
             tc_fence_after();
             if (nops > 0 && op_type(L.ops[0]) != OP_F) issue_qk(g0);
@@ -325,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 2)
         const int r = (warp & 3) * 32 + lane;
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t t_o = tbase + lane_off;
-        const int64_t n_last = NK - 1;
-        const int nlast_len = (int)(p.S - n_last * 64);
+        const int n_last = (int)NK - 1;
+        const int nlast_len = (int)(p.S - (int64_t)n_last * 64);
         const float cs = p.scale_log2;
         const int G32 = (int)p.G, NK32 = (int)NK;
         int sc0 = 0, sc1 = 0;   // S-type ops seen per S buffer (s_full parity), all items
@@ -335,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2)
             mbar_wait_sleep(&ctl.pv_done[g & 1], (uint32_t)((g >> 1) & 1));
         };
         // Q row r of item j's tile -> TMEM lane r, columns kQCol.. (bf16 pairs)
-        auto q_to_tmem = [&](int64_t j) {
+        auto q_to_tmem = [&](int j) {
             const int qb = (int)(j & 1);
             mbar_wait_sleep(&ctl.q_full[qb], (uint32_t)((j >> 1) & 1));
             const uint8_t* qrow = smem + kOffQ + qb * kQBox;
@@ -351,16 +365,19 @@ __global__ void __launch_bounds__(kThreads, 2)
             tc_fence_before();
             mbar_arrive(&ctl.q_tmem);
         };
-        if (nitems > 0) q_to_tmem(0);
+        mbar_wait_sleep(&ctl.list_full[0], 0);
+        if (ctl.list[0].nops >= 0) q_to_tmem(0);
         int g0 = 0;
-        for (int64_t j = 0; j < nitems; ++j) {
-            const int bb = (int)(j & 1);
+        for (int j = 0;; ++j) {
+            const int bb = j & 1;
             mbar_wait_sleep(&ctl.list_full[bb], (uint32_t)((j >> 1) & 1));
             const List& L = ctl.list[bb];
             const int nops = L.nops;
-            const int64_t item = item_of(j);
-            const int64_t i = item % p.NQ, bh = item / p.NQ;
-            const int64_t b = bh / p.H, h = bh % p.H;
+            if (nops < 0) break;
+            const int item = L.item;
+            const int NQ32 = (int)p.NQ, H32 = (int)p.H;
+            const int i = item % NQ32, bh = item / NQ32;
+            const int b = bh / H32, h = bh % H32;
             const uint8_t* qrow = smem + kOffQ + bb * kQBox;
             float m = -INFINITY, l = 0.f;
             float A_cur = 0.f, A_done = 0.f;
@@ -513,14 +530,18 @@ __global__ void __launch_bounds__(kThreads, 2)
             }
             // ---- transition: the next item's Q into TMEM (item j's last QK^T has completed:
             // its S was consumed above), so its first QK^T runs during this epilogue ----
-            if (j + 1 < nitems) q_to_tmem(j + 1);
+            {
+                const int nb = (j + 1) & 1;
+                mbar_wait_sleep(&ctl.list_full[nb], (uint32_t)(((j + 1) >> 1) & 1));
+                if (ctl.list[nb].nops >= 0) q_to_tmem(j + 1);
+            }
             // ---- epilogue of item j: O / l -> bf16 -> global ----
             consume_op(g0 + nops - 2);
             consume_op(g0 + nops - 1);
             tc_fence_after();
-            const int64_t t = i * kBQ + r;
+            const int t = i * kBQ + r;
             const float inv = 1.f / l;
-            __nv_bfloat16* orow = p.out + b * p.osB + h * p.osH + t * p.osS;
+            __nv_bfloat16* orow = p.out + (int64_t)b * p.osB + (int64_t)h * p.osH + (int64_t)t * p.osS;
 #pragma unroll 1
             for (int c0 = 0; c0 < kD; c0 += 32) {
                 uint32_t o[32];
@@ -601,6 +622,9 @@ cudaError_t launch_attn_sm100_persist(const pasa_tensor& q, const pasa_tensor& k
     prm.idx = r->idx; prm.count = r->count; prm.mask = r->mask;
     prm.out = reinterpret_cast<__nv_bfloat16*>(out.data);
     prm.osB = out.sB; prm.osS = out.sS; prm.osH = out.sH;
+    prm.counter = r->hdr + 1;   // a free word of the route header
+    cudaError_t ez = cudaMemsetAsync(prm.counter, 0, sizeof(int32_t), st);
+    if (ez != cudaSuccess) return ez;
     // 80 KB of dynamic shared memory (+ ~19 KB static): two CTAs per SM, never three
     const size_t smem = 80 * 1024;
     static_assert(kBytes + 1024 <= 80 * 1024, "shared memory budget");
